@@ -1,0 +1,158 @@
+/*
+ * pipedp_cuda.h -- C ABI of the B200-native pipedp solvers (sm_100a).
+ *
+ * Plain pointers and sizes only; no torch or CUDA types in the signatures
+ * (streams travel as `void*` = cudaStream_t).  Every entry point is the body
+ * a reference FFI would bind in place of the reference's C++ solver
+ * (/root/reference/proj, cited per function).  All host-buffer entry points
+ * validate with the reference's exact rules and error codes BEFORE touching a
+ * device and never fall back to a CPU path: with no usable GPU they return
+ * PIPEDP_ERR_NO_DEVICE.
+ *
+ * Status codes: 0 = ok; 1 + index of the reference `errc` enumerator
+ * (error.hpp:8-20) for validation errors; >= 100 for device errors.
+ * pipedp_last_error() returns the message of the calling thread's last error,
+ * prefixed like the reference's Error::what() ("InitLengthMismatch: ...").
+ * Every function is thread-safe; concurrent callers get independent streams
+ * and buffers.
+ */
+#ifndef PIPEDP_CUDA_H
+#define PIPEDP_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------- */
+enum {
+  PIPEDP_OK = 0,
+  PIPEDP_E_NON_DECREASING_OFFSETS = 1, /* errc::non_decreasing_offsets */
+  PIPEDP_E_NON_POSITIVE_OFFSET = 2,    /* errc::non_positive_offset */
+  PIPEDP_E_INIT_LENGTH_MISMATCH = 3,   /* errc::init_length_mismatch */
+  PIPEDP_E_TABLE_TOO_SMALL = 4,        /* errc::table_too_small */
+  PIPEDP_E_COORD_OUT_OF_RANGE = 5,     /* errc::coord_out_of_range */
+  PIPEDP_E_ADDRESS_OUT_OF_RANGE = 6,   /* errc::address_out_of_range */
+  PIPEDP_E_BASE_CELL_HAS_NO_DEPS = 7,  /* errc::base_cell_has_no_deps */
+  PIPEDP_E_TOO_LARGE_FOR_BRUTE = 8,    /* errc::too_large_for_brute_force */
+  PIPEDP_E_STALL_LIVELOCK = 9,         /* errc::stall_livelock */
+  PIPEDP_E_WEIGHT_OVERFLOW = 10,       /* errc::weight_overflow */
+  PIPEDP_E_INVALID_PARAMS = 11,        /* errc::invalid_params */
+  PIPEDP_ERR_CUDA = 100,
+  PIPEDP_ERR_NO_DEVICE = 101,
+  PIPEDP_ERR_OUT_OF_MEMORY = 102,
+  PIPEDP_ERR_UNSUPPORTED = 103
+};
+
+/* Semigroup kinds, OpKind order (semigroup.hpp:13). */
+enum { PIPEDP_OP_MIN = 0, PIPEDP_OP_MAX = 1, PIPEDP_OP_SATURATING_ADD = 2, PIPEDP_OP_MODULAR_ADD = 3 };
+
+/* MCM kernels */
+enum {
+  PIPEDP_MCM_AUTO = 0,       /* shared-memory CTA for small n, HBM wavefront otherwise */
+  PIPEDP_MCM_WAVEFRONT = 1,  /* multi-SM dataflow pipeline, table in HBM */
+  PIPEDP_MCM_SMEM = 2,       /* one CTA, table in shared memory (small n) */
+  PIPEDP_MCM_TOURNAMENT = 3  /* the paper's O(n^2 log n) comparison kernel */
+};
+
+/* McmMode (mcm_pipeline.hpp:88) */
+enum { PIPEDP_MCM_PAPER_LITERAL = 0, PIPEDP_MCM_STALL_ON_HAZARD = 1 };
+
+const char* pipedp_last_error(void);
+const char* pipedp_version(void);
+/* number of usable sm_100 devices (0 without a GPU; never fails) */
+int32_t pipedp_device_count(void);
+
+/* ---- host-only helpers (no device needed) -------------------------------- */
+/* validate(SdpInstance) -- sdp.cpp:10-32 */
+int32_t pipedp_sdp_validate(const int64_t* offsets, int64_t k, int64_t init_len, int64_t n);
+/* validate(McmInstance) -- mcm.cpp:11-28 */
+int32_t pipedp_mcm_validate(const int64_t* dims, int64_t dims_len);
+/* table_digest over a cells array -- table.cpp:12-25 */
+uint64_t pipedp_table_digest(const int64_t* cells, int64_t count);
+/* generate_sdp -- generate.cpp:21-47 (offsets_out: k, init_out: a_1 <= init_cap) */
+int32_t pipedp_generate_sdp(int64_t n, int64_t k, int32_t op, uint64_t seed, int32_t consecutive,
+                            int64_t a1_cap, int64_t* offsets_out, int64_t* init_out,
+                            int64_t init_cap, int64_t* a1_out);
+/* generate_mcm -- generate.cpp:49-60 (dims_out: n+1) */
+int32_t pipedp_generate_mcm(int64_t n, uint64_t seed, int64_t dims_min, int64_t dims_max,
+                            int64_t* dims_out);
+
+/* ---- S-DP, host buffers ---------------------------------------------------
+ * Replaces the table computation of solve_sequential (sdp.cpp:84-89),
+ * solve_prefix_parallel (sdp.cpp:91-100), solve_naive_parallel
+ * (sdp.cpp:102-111) and solve_sdp_pipeline (sdp_pipeline.cpp:34-44).
+ * cells_out: n entries; filled_out (nullable): n entries, all set to 1. */
+int32_t pipedp_sdp_solve(const int64_t* offsets, int64_t k, const int64_t* init,
+                         int64_t init_len, int64_t n, int32_t op, int64_t* cells_out,
+                         uint8_t* filled_out);
+
+/* Batch of independent instances sharing n, k and a_1 (SoA: offsets
+ * [batch*k], init [batch*a_1], cells_out [batch*n]).  No reference
+ * counterpart (the reference loops serially, commands.cpp:480-507); each
+ * instance has solve_sequential's semantics.  device < 0: current device. */
+int32_t pipedp_sdp_solve_batch(int64_t batch, int64_t n, int64_t k, int64_t a1,
+                               const int64_t* offsets, const int64_t* init, int32_t op,
+                               int64_t* cells_out, int32_t device);
+
+/* ---- S-DP, device-resident plans (inputs already in HBM) ------------------ */
+typedef struct pipedp_sdp_plan* pipedp_sdp_plan_t;
+/* h_offsets / h_init: HOST copies of every instance's offsets and init values,
+ * used for validation and value-width planning; uploaded once. */
+int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
+                               const int64_t* h_offsets, const int64_t* h_init, int32_t op,
+                               int32_t device, pipedp_sdp_plan_t* plan_out);
+/* d_init: device copy of init ([batch*a1]); d_cells: device table ([batch*n]);
+ * stream: cudaStream_t or NULL.  Asynchronous. */
+int32_t pipedp_sdp_plan_execute(pipedp_sdp_plan_t plan, const int64_t* d_init, int64_t* d_cells,
+                                void* stream);
+/* kernel name, value width (32/64) and kernel launches per execute */
+int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t plan, char* name, size_t name_cap,
+                                 int32_t* value_bits, int32_t* launches);
+int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t plan);
+
+/* ---- MCM, host buffers ------------------------------------------------------
+ * solve_mcm_sequential (mcm.cpp:85-110): cells_out / split_out (nullable) /
+ * filled_out (nullable) have cell_count(n)+1 entries in the reference's
+ * 1-based diagonal-major layout. */
+int32_t pipedp_mcm_solve(const int64_t* dims, int64_t dims_len, int32_t kernel,
+                         int64_t* cells_out, uint8_t* filled_out, int64_t* split_out);
+/* solve_mcm_pipeline (mcm_pipeline.cpp:32-47): exact lock-step engine
+ * semantics of McmProgram for both McmMode values: same table, same
+ * steps_executed, same stall_iterations. */
+int32_t pipedp_mcm_pipeline(const int64_t* dims, int64_t dims_len, int32_t mode,
+                            int64_t* cells_out, uint8_t* filled_out, int64_t* steps_out,
+                            int64_t* stall_iterations_out);
+/* batch of independent MCM instances of equal n (dims [batch*(n+1)],
+ * cells/split [batch*(cell_count(n)+1)]) */
+int32_t pipedp_mcm_solve_batch(int64_t batch, int64_t n, const int64_t* dims, int64_t* cells_out,
+                               int64_t* split_out, int32_t device);
+
+/* ---- MCM, device-resident plans ------------------------------------------ */
+typedef struct pipedp_mcm_plan* pipedp_mcm_plan_t;
+int32_t pipedp_mcm_plan_create(int64_t batch, int64_t n, const int64_t* h_dims, int32_t kernel,
+                               int32_t device, pipedp_mcm_plan_t* plan_out);
+/* d_cells / d_split: [batch*(cell_count(n)+1)].  Synchronises `stream` once at
+ * the end (the 32-bit kernels report a device-side overflow flag that decides
+ * whether the 64-bit kernel must run). */
+int32_t pipedp_mcm_plan_execute(pipedp_mcm_plan_t plan, int64_t* d_cells, int64_t* d_split,
+                                void* stream);
+int32_t pipedp_mcm_plan_describe(pipedp_mcm_plan_t plan, char* name, size_t name_cap,
+                                 int32_t* value_bits, int32_t* launches);
+int32_t pipedp_mcm_plan_destroy(pipedp_mcm_plan_t plan);
+
+/* ---- device utilities -------------------------------------------------------- */
+/* FNV-1a table_digest of ntables consecutive tables of `count` cells each. */
+int32_t pipedp_digest_device(const int64_t* d_tables, int64_t count, int64_t ntables,
+                             uint64_t* d_digests, void* stream);
+/* Dependency-chain step microbenchmark: ns per warp-shuffle hand-off step of
+ * the S-DP chain warp for `op` at `value_bits`. */
+int32_t pipedp_chain_step_ns(int32_t op, int32_t value_bits, int32_t device, double* ns_out,
+                             double* sm_clock_mhz_out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PIPEDP_CUDA_H */

@@ -1,0 +1,898 @@
+// capi.cu -- the C ABI (include/pipedp_cuda.h): validation with the
+// reference's rules, value-width / stage planning, device memory, launches.
+//
+// There is no CPU compute path in this file: every table is produced by a
+// kernel from sdp_kernels.cuh / mcm_kernels.cuh, and a missing or unusable GPU
+// is reported as PIPEDP_ERR_NO_DEVICE.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <random>
+#include <string>
+#include <unordered_set>
+#include <vector>
+
+#include "../../include/pipedp_cuda.h"
+#include "mcm_kernels.cuh"
+#include "sdp_kernels.cuh"
+
+using namespace pipedp_dev;
+
+namespace {
+
+// ---------------------------------------------------------------- errors ---
+thread_local std::string g_last_error;
+
+const char* errc_name(int code) {  // semigroup.cpp:73-99, indexed by errc + 1
+  static const char* names[] = {"",
+                                "NonDecreasingOffsets",
+                                "NonPositiveOffset",
+                                "InitLengthMismatch",
+                                "TableTooSmall",
+                                "CoordOutOfRange",
+                                "AddressOutOfRange",
+                                "BaseCellHasNoDeps",
+                                "TooLargeForBruteForce",
+                                "StallLivelock",
+                                "WeightOverflow",
+                                "InvalidParams"};
+  if (code >= 1 && code <= 11) return names[code];
+  switch (code) {
+    case PIPEDP_ERR_CUDA: return "CudaError";
+    case PIPEDP_ERR_NO_DEVICE: return "NoDevice";
+    case PIPEDP_ERR_OUT_OF_MEMORY: return "OutOfMemory";
+    case PIPEDP_ERR_UNSUPPORTED: return "Unsupported";
+  }
+  return "UnknownError";
+}
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = std::string(errc_name(code)) + ": " + buf;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  (void)cudaGetLastError();
+  return fail(e == cudaErrorMemoryAllocation ? PIPEDP_ERR_OUT_OF_MEMORY : PIPEDP_ERR_CUDA,
+              "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(expr)                                      \
+  do {                                                \
+    cudaError_t _e = (expr);                          \
+    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
+  } while (0)
+
+// ------------------------------------------------------------ validation ---
+// sdp.cpp:10-32, in the reference's order.
+int validate_sdp(const int64_t* offs, int64_t k, int64_t init_len, int64_t n) {
+  if (k <= 0 || offs == nullptr) return fail(PIPEDP_E_INVALID_PARAMS, "offset set must be nonempty");
+  for (int64_t i = 0; i < k; ++i) {
+    if (offs[i] <= 0)
+      return fail(PIPEDP_E_NON_POSITIVE_OFFSET, "offset a_%lld is not positive", (long long)(i + 1));
+    if (i > 0 && offs[i - 1] <= offs[i])
+      return fail(PIPEDP_E_NON_DECREASING_OFFSETS,
+                  "offsets must strictly decrease, violated at position %lld", (long long)(i + 1));
+  }
+  if (init_len != offs[0])
+    return fail(PIPEDP_E_INIT_LENGTH_MISMATCH, "expected a_1=%lld initial values, got %lld",
+                (long long)offs[0], (long long)init_len);
+  if (n <= offs[0])
+    return fail(PIPEDP_E_TABLE_TOO_SMALL, "n=%lld leaves nothing to compute past the preset prefix",
+                (long long)n);
+  return PIPEDP_OK;
+}
+
+// mcm.cpp:11-28.  The overflow product is evaluated like the reference's
+// signed left-to-right expression compiles on gcc/x86-64 (two's-complement
+// wrap), so the accepted set is identical.
+int validate_mcm(const int64_t* dims, int64_t len) {
+  if (len < 2 || dims == nullptr)
+    return fail(PIPEDP_E_INVALID_PARAMS, "dimension vector needs at least two entries");
+  int64_t max_dim = 1;
+  for (int64_t i = 0; i < len; ++i) {
+    if (dims[i] < 1) return fail(PIPEDP_E_INVALID_PARAMS, "matrix dimensions must be >= 1");
+    max_dim = std::max(max_dim, dims[i]);
+  }
+  const int64_t n = len - 1;
+  uint64_t p = (uint64_t)n * (uint64_t)max_dim;
+  p *= (uint64_t)max_dim;
+  p *= (uint64_t)max_dim;
+  if (max_dim > 1000000 || (int64_t)p > ((int64_t)1 << 61))
+    return fail(PIPEDP_E_WEIGHT_OVERFLOW, "dimension products too large for 64-bit cost accumulation");
+  return PIPEDP_OK;
+}
+
+// ------------------------------------------------------------- devices ---
+int usable_devices() {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  int usable = 0;
+  for (int d = 0; d < count; ++d) {
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, d) == cudaSuccess && prop.major == 10) ++usable;
+  }
+  return usable;
+}
+
+int select_device(int32_t device) {
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+    (void)cudaGetLastError();
+    return fail(PIPEDP_ERR_NO_DEVICE, "no CUDA device visible (the solvers have no CPU path)");
+  }
+  int dev = device;
+  if (dev < 0) CK(cudaGetDevice(&dev));
+  if (dev >= count) return fail(PIPEDP_ERR_NO_DEVICE, "device %d not present (%d visible)", dev, count);
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10)
+    return fail(PIPEDP_ERR_NO_DEVICE, "device %d is sm_%d%d; these kernels are built for sm_100a", dev,
+                prop.major, prop.minor);
+  CK(cudaSetDevice(dev));
+  return PIPEDP_OK;
+}
+
+// A per-call stream and a tiny RAII set of device buffers.
+struct Scope {
+  cudaStream_t stream = nullptr;
+  std::vector<void*> bufs;
+  ~Scope() {
+    if (stream) cudaStreamSynchronize(stream);
+    for (void* p : bufs) cudaFree(p);
+    if (stream) cudaStreamDestroy(stream);
+  }
+  int init() {
+    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+    return PIPEDP_OK;
+  }
+  template <typename T>
+  int alloc(T** p, size_t count) {
+    void* q = nullptr;
+    CK(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T)));
+    bufs.push_back(q);
+    *p = static_cast<T*>(q);
+    return PIPEDP_OK;
+  }
+};
+
+#define TRY(expr)                  \
+  do {                             \
+    int _rc = (expr);              \
+    if (_rc != PIPEDP_OK) return _rc; \
+  } while (0)
+
+int ceil_log2(uint64_t v) {
+  int r = 0;
+  while ((1ull << r) < v) ++r;
+  return r;
+}
+
+// ================================================================== S-DP ===
+struct SdpDispatch {
+  int op;
+  int bits;   // 32 or 64
+  bool assoc; // regrouping legal
+  bool small; // CTA: a1 < 64, warp: a1 < 32
+  bool gfar;
+  bool warp_kernel;
+  SdpShape shape;
+  int threads;
+  size_t smem;
+  int wpb;  // warp kernel: warps per block
+};
+
+// value width and associativity from the init values (see common.cuh)
+void sdp_value_class(int op, const int64_t* init, int64_t count, int* bits, bool* assoc) {
+  bool fits32 = true, any_pos = false, any_neg = false;
+  for (int64_t i = 0; i < count; ++i) {
+    const int64_t v = init[i];
+    if (op == PIPEDP_OP_MODULAR_ADD) fits32 = fits32 && v >= 0 && v < kModulus;
+    else fits32 = fits32 && v >= INT32_MIN && v <= INT32_MAX;
+    any_pos = any_pos || v > 0;
+    any_neg = any_neg || v < 0;
+  }
+  *bits = (op != PIPEDP_OP_SATURATING_ADD && fits32) ? 32 : 64;
+  *assoc = op != PIPEDP_OP_SATURATING_ADD || !(any_pos && any_neg);
+}
+
+constexpr size_t kSmemBudget = 200 * 1024;
+constexpr int kAMid = 256;
+
+int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* offsets,
+             const int64_t* init, int op, SdpDispatch* d) {
+  if (op < 0 || op > 3) return fail(PIPEDP_E_INVALID_PARAMS, "unknown operator kind");
+  if (a1 >= INT32_MAX - 4096 || k >= INT32_MAX / 8)
+    return fail(PIPEDP_ERR_UNSUPPORTED, "a_1=%lld exceeds the 32-bit offset range of the kernels",
+                (long long)a1);
+  d->op = op;
+  sdp_value_class(op, init, batch * a1, &d->bits, &d->assoc);
+  const size_t vb = d->bits / 8;
+  SdpShape& s = d->shape;
+  s.n = n;
+  s.k = (int32_t)k;
+  s.a1 = (int32_t)a1;
+  s.a_mid = kAMid;
+  const int64_t kpad = (k + 3) & ~3ll;
+  // warp-per-instance kernel for batches of small-a_1 instances
+  if (batch > 1) {
+    const int64_t R = 1ll << ceil_log2((uint64_t)(a1 + 32));
+    const size_t per_warp = 2 * R * vb + kpad * 4;
+    if (per_warp <= 16 * 1024) {
+      d->warp_kernel = true;
+      d->small = a1 < 32;
+      d->gfar = false;
+      s.ring_log2 = ceil_log2((uint64_t)R);
+      s.mid_warps = s.far_warps = 0;
+      d->wpb = (int)std::max<int64_t>(1, std::min<int64_t>(8, (96 * 1024) / per_warp));
+      d->threads = 32 * d->wpb;
+      d->smem = per_warp * d->wpb;
+      return PIPEDP_OK;
+    }
+  }
+  d->warp_kernel = false;
+  d->small = a1 < 64;
+  // largest far-offset count over the batch sizes the far stage
+  int64_t jf_max = 0;
+  for (int64_t b = 0; b < batch; ++b) {
+    int64_t jf = 0;
+    for (int64_t j = 0; j < k; ++j) jf += offsets[b * k + j] >= kAMid;
+    jf_max = std::max(jf_max, jf);
+  }
+  const size_t slots = (size_t)(kMidSlots + kFarSlots) * 32 * vb + (1 + kMidSlots + kFarSlots) * 4 + 64;
+  const int64_t r_full = 1ll << ceil_log2((uint64_t)(a1 + 128));
+  const size_t smem_full = 2 * r_full * vb + kpad * 4 + slots;
+  if (d->small || smem_full <= kSmemBudget) {
+    d->gfar = false;
+    s.ring_log2 = ceil_log2((uint64_t)r_full);
+    d->smem = smem_full;
+  } else {
+    if (kpad * 4 + 2 * 512 * vb + slots > 227 * 1024)
+      return fail(PIPEDP_ERR_UNSUPPORTED, "k=%lld offsets exceed shared memory", (long long)k);
+    d->gfar = true;
+    s.ring_log2 = ceil_log2((uint64_t)(kAMid + 128));
+    d->smem = 2 * (1ull << s.ring_log2) * vb + kpad * 4 + slots;
+  }
+  if (d->small) {
+    s.mid_warps = s.far_warps = 0;
+    d->threads = 32;
+  } else {
+    s.mid_warps = 4;
+    s.far_warps = (int32_t)std::min<int64_t>(27, std::max<int64_t>(1, (jf_max + 47) / 48));
+    d->threads = 32 * (1 + s.mid_warps + s.far_warps);
+  }
+  return PIPEDP_OK;
+}
+
+template <int OP, typename T, bool SMALL, bool ASSOC, bool GFAR>
+int launch_cta(const SdpDispatch& d, int64_t batch, const int64_t* offs, const int64_t* init,
+               int64_t* out, cudaStream_t st) {
+  auto kern = sdp_pipeline_cta<OP, T, SMALL, ASSOC, GFAR>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem));
+  kern<<<(unsigned)batch, d.threads, d.smem, st>>>(d.shape, offs, init, out);
+  CK(cudaGetLastError());
+  return PIPEDP_OK;
+}
+
+template <int OP, typename T, bool SMALL, bool ASSOC>
+int launch_warp(const SdpDispatch& d, int64_t batch, const int64_t* offs, const int64_t* init,
+                int64_t* out, cudaStream_t st) {
+  auto kern = sdp_batch_warp<OP, T, SMALL, ASSOC>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem));
+  const int64_t grid = (batch + d.wpb - 1) / d.wpb;
+  kern<<<(unsigned)grid, d.threads, d.smem, st>>>(d.shape, batch, offs, init, out);
+  CK(cudaGetLastError());
+  return PIPEDP_OK;
+}
+
+template <int OP, typename T, bool ASSOC>
+int launch_sdp_t(const SdpDispatch& d, int64_t batch, const int64_t* offs, const int64_t* init,
+                 int64_t* out, cudaStream_t st) {
+  if (d.warp_kernel) {
+    return d.small ? launch_warp<OP, T, true, ASSOC>(d, batch, offs, init, out, st)
+                   : launch_warp<OP, T, false, ASSOC>(d, batch, offs, init, out, st);
+  }
+  if (d.small) return launch_cta<OP, T, true, ASSOC, false>(d, batch, offs, init, out, st);
+  return d.gfar ? launch_cta<OP, T, false, ASSOC, true>(d, batch, offs, init, out, st)
+                : launch_cta<OP, T, false, ASSOC, false>(d, batch, offs, init, out, st);
+}
+
+int launch_sdp(const SdpDispatch& d, int64_t batch, const int64_t* offs, const int64_t* init,
+               int64_t* out, cudaStream_t st) {
+  switch (d.op) {
+    case PIPEDP_OP_MIN:
+      return d.bits == 32 ? launch_sdp_t<kMin, int32_t, true>(d, batch, offs, init, out, st)
+                          : launch_sdp_t<kMin, int64_t, true>(d, batch, offs, init, out, st);
+    case PIPEDP_OP_MAX:
+      return d.bits == 32 ? launch_sdp_t<kMax, int32_t, true>(d, batch, offs, init, out, st)
+                          : launch_sdp_t<kMax, int64_t, true>(d, batch, offs, init, out, st);
+    case PIPEDP_OP_MODULAR_ADD:
+      return d.bits == 32 ? launch_sdp_t<kModAdd, int32_t, true>(d, batch, offs, init, out, st)
+                          : launch_sdp_t<kModAdd, int64_t, true>(d, batch, offs, init, out, st);
+    default:
+      return d.assoc ? launch_sdp_t<kSatAdd, int64_t, true>(d, batch, offs, init, out, st)
+                     : launch_sdp_t<kSatAdd, int64_t, false>(d, batch, offs, init, out, st);
+  }
+}
+
+const char* sdp_kernel_name(const SdpDispatch& d) {
+  if (d.warp_kernel) return "sdp_batch_warp";
+  if (d.small) return "sdp_pipeline_cta[chain]";
+  return d.gfar ? "sdp_pipeline_cta[far-hbm]" : "sdp_pipeline_cta[ring]";
+}
+
+}  // namespace
+
+struct pipedp_sdp_plan {
+  int device;
+  int64_t batch, n, k, a1;
+  SdpDispatch d;
+  int64_t* d_offsets;  // device copy of the offsets, int64 [batch*k]
+};
+
+// ================================================================== MCM ===
+namespace {
+
+struct McmDispatch {
+  int kernel;  // PIPEDP_MCM_WAVEFRONT / SMEM / TOURNAMENT
+  int bits;    // 32 or 64 (first attempt)
+  int threads;
+  size_t smem32, smem64;
+};
+
+int mcm_max_dim(const int64_t* dims, int64_t len) {
+  int64_t m = 1;
+  for (int64_t i = 0; i < len; ++i) m = std::max(m, dims[i]);
+  return (int)std::min<int64_t>(m, INT_MAX);
+}
+
+size_t mcm_smem_bytes(int64_t n, size_t vb) {
+  const int64_t cc = n * (n + 1) / 2;
+  return ((cc + 1 + 3) & ~3ll) * vb + (n + 1 + 3) * 4;
+}
+
+int plan_mcm(int64_t batch, int64_t n, const int64_t* dims, int kernel, McmDispatch* d) {
+  int max_dim = 1;
+  for (int64_t b = 0; b < batch; ++b) max_dim = std::max(max_dim, mcm_max_dim(dims + b * (n + 1), n + 1));
+  d->bits = max_dim <= 1290 ? 32 : 64;  // max_dim^3 < 2^31
+  d->smem32 = mcm_smem_bytes(n, 4);
+  d->smem64 = mcm_smem_bytes(n, 8);
+  if (kernel == PIPEDP_MCM_AUTO) {
+    const size_t need = d->bits == 32 ? d->smem32 : d->smem64;
+    const bool fits = need <= kSmemBudget;
+    kernel = (fits && (batch > 1 || n <= 160)) ? PIPEDP_MCM_SMEM : PIPEDP_MCM_WAVEFRONT;
+    if (!fits && batch > 1) kernel = PIPEDP_MCM_WAVEFRONT;
+  }
+  if (kernel == PIPEDP_MCM_SMEM && d->smem64 > 227 * 1024 && d->smem32 > 227 * 1024)
+    return fail(PIPEDP_ERR_UNSUPPORTED, "n=%lld too large for the shared-memory MCM kernel",
+                (long long)n);
+  if (kernel == PIPEDP_MCM_SMEM && d->bits == 64 && d->smem64 > 227 * 1024)
+    return fail(PIPEDP_ERR_UNSUPPORTED, "n=%lld too large for the 64-bit shared-memory MCM kernel",
+                (long long)n);
+  if ((kernel == PIPEDP_MCM_TOURNAMENT) && batch > 1)
+    return fail(PIPEDP_E_INVALID_PARAMS, "the tournament kernel solves one instance at a time");
+  if (kernel < PIPEDP_MCM_AUTO || kernel > PIPEDP_MCM_TOURNAMENT)
+    return fail(PIPEDP_E_INVALID_PARAMS, "unknown MCM kernel %d", kernel);
+  d->kernel = kernel;
+  d->threads = n <= 64 ? 128 : (n <= 256 ? 256 : 512);
+  return PIPEDP_OK;
+}
+
+}  // namespace
+
+struct pipedp_mcm_plan {
+  int device;
+  int64_t batch, n, cc;
+  McmDispatch d;
+  int32_t* d_p;       // dims as int32 [batch*(n+1)] (validated <= 1e6)
+  int64_t* d_dims;    // dims int64 (tournament)
+  uint32_t* d_v32;    // wavefront 32-bit value table [cc+1]
+  int64_t* d_chunk_base;
+  int* d_done;
+  unsigned long long* d_next;
+  int* d_overflow;
+  int* h_overflow;    // pinned
+  int64_t total_chunks;
+  int launches;
+  int last_bits;
+};
+
+namespace {
+
+int mcm_wave_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split, cudaStream_t st) {
+  const int64_t n = P->n;
+  CK(cudaMemsetAsync(P->d_done, 0, sizeof(int) * std::max<int64_t>(P->total_chunks, 1), st));
+  CK(cudaMemsetAsync(P->d_next, 0, sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(cells, 0, sizeof(int64_t) * (n + 1), st));
+  CK(cudaMemsetAsync(split, 0, sizeof(int64_t) * (n + 1), st));
+  McmWave W{n, P->total_chunks, P->d_chunk_base, P->d_done, P->d_next};
+  int dev = 0, sms = 148;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  const int threads = 256;
+  int64_t grid = std::min<int64_t>((int64_t)sms * 8, (P->total_chunks + 7) / 8);
+  grid = std::max<int64_t>(grid, 1);
+  if (bits == 32) {
+    CK(cudaMemsetAsync(P->d_v32, 0, sizeof(uint32_t) * (n + 1), st));
+    mcm_wavefront<uint32_t><<<(unsigned)grid, threads, 0, st>>>(W, P->d_p, P->d_v32, cells, split,
+                                                                 P->d_overflow);
+  } else {
+    mcm_wavefront<int64_t><<<(unsigned)grid, threads, 0, st>>>(W, P->d_p, cells, cells, split,
+                                                                P->d_overflow);
+  }
+  CK(cudaGetLastError());
+  return PIPEDP_OK;
+}
+
+int mcm_smem_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split, cudaStream_t st) {
+  const int64_t n = P->n;
+  if (bits == 32) {
+    CK(cudaFuncSetAttribute(mcm_smem_cta<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)P->d.smem32));
+    mcm_smem_cta<uint32_t><<<(unsigned)P->batch, P->d.threads, P->d.smem32, st>>>(
+        n, P->batch, P->d_dims, cells, split, P->d_overflow);
+  } else {
+    CK(cudaFuncSetAttribute(mcm_smem_cta<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)P->d.smem64));
+    mcm_smem_cta<int64_t><<<(unsigned)P->batch, P->d.threads, P->d.smem64, st>>>(
+        n, P->batch, P->d_dims, cells, split, P->d_overflow);
+  }
+  CK(cudaGetLastError());
+  return PIPEDP_OK;
+}
+
+int mcm_execute(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t st) {
+  P->launches = 0;
+  if (P->d.kernel == PIPEDP_MCM_TOURNAMENT) {
+    mcm_tournament<<<1, 1024, 0, st>>>(P->n, P->d_dims, cells, split);
+    CK(cudaGetLastError());
+    P->launches = 1;
+    P->last_bits = 64;
+    return PIPEDP_OK;
+  }
+  int bits = P->d.bits;
+  for (;;) {
+    CK(cudaMemsetAsync(P->d_overflow, 0, sizeof(int), st));
+    if (P->d.kernel == PIPEDP_MCM_SMEM) TRY(mcm_smem_launch(P, bits, cells, split, st));
+    else TRY(mcm_wave_launch(P, bits, cells, split, st));
+    ++P->launches;
+    P->last_bits = bits;
+    if (bits == 64) return PIPEDP_OK;
+    CK(cudaMemcpyAsync(P->h_overflow, P->d_overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (*P->h_overflow == 0) return PIPEDP_OK;
+    bits = 64;  // a value reached 2^30: redo exactly in 64-bit
+    if (P->d.kernel == PIPEDP_MCM_SMEM && P->d.smem64 > 227 * 1024) {
+      P->d.kernel = PIPEDP_MCM_WAVEFRONT;
+      if (P->batch > 1)
+        return fail(PIPEDP_ERR_UNSUPPORTED, "batched instance overflowed 32-bit and n too large for 64-bit smem");
+    }
+  }
+}
+
+}  // namespace
+
+// ====================================================================== API ===
+extern "C" {
+
+const char* pipedp_last_error(void) { return g_last_error.c_str(); }
+const char* pipedp_version(void) { return "pipedp-b200 0.1 (sm_100a)"; }
+int32_t pipedp_device_count(void) { return usable_devices(); }
+
+int32_t pipedp_sdp_validate(const int64_t* offsets, int64_t k, int64_t init_len, int64_t n) {
+  return validate_sdp(offsets, k, init_len, n);
+}
+
+int32_t pipedp_mcm_validate(const int64_t* dims, int64_t dims_len) {
+  return validate_mcm(dims, dims_len);
+}
+
+uint64_t pipedp_table_digest(const int64_t* cells, int64_t count) {  // table.cpp:12-25
+  uint64_t h = 14695981039346656037ull;
+  auto mix = [&](uint64_t v) {
+    for (int b = 0; b < 8; ++b) {
+      h ^= (v >> (8 * b)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  };
+  mix((uint64_t)count);
+  for (int64_t i = 0; i < count; ++i) mix((uint64_t)cells[i]);
+  return h;
+}
+
+// generate.cpp:21-47 -- same draws from the same std::mt19937_64 stream.
+int32_t pipedp_generate_sdp(int64_t n, int64_t k, int32_t op, uint64_t seed, int32_t consecutive,
+                            int64_t a1_cap, int64_t* offsets_out, int64_t* init_out,
+                            int64_t init_cap, int64_t* a1_out) {
+  (void)op;
+  if (k < 1) return fail(PIPEDP_E_INVALID_PARAMS, "k must be >= 1");
+  std::mt19937_64 rng(seed);
+  auto bounded = [&](int64_t lo, int64_t hi) {
+    return lo + (int64_t)(rng() % (uint64_t)(hi - lo + 1));
+  };
+  std::vector<int64_t> offs;
+  if (consecutive) {
+    for (int64_t a = k; a >= 1; --a) offs.push_back(a);
+  } else {
+    const int64_t cap = a1_cap > 0 ? a1_cap : 2 * k;
+    if (cap < k) return fail(PIPEDP_E_INVALID_PARAMS, "offset cap smaller than k");
+    std::unordered_set<int64_t> chosen{cap};
+    while ((int64_t)chosen.size() < k) chosen.insert(bounded(1, cap - 1));
+    offs.assign(chosen.begin(), chosen.end());
+    std::sort(offs.begin(), offs.end(), std::greater<>());
+  }
+  const int64_t a1 = offs.front();
+  if (n <= a1) return fail(PIPEDP_E_INVALID_PARAMS, "n must exceed the largest offset");
+  if (init_cap < a1) return fail(PIPEDP_E_INVALID_PARAMS, "init buffer holds %lld < a_1=%lld values",
+                                 (long long)init_cap, (long long)a1);
+  std::copy(offs.begin(), offs.end(), offsets_out);
+  for (int64_t i = 0; i < a1; ++i) init_out[i] = bounded(0, (int64_t(1) << 20) - 1);
+  if (a1_out) *a1_out = a1;
+  return validate_sdp(offsets_out, k, a1, n);
+}
+
+// generate.cpp:49-60
+int32_t pipedp_generate_mcm(int64_t n, uint64_t seed, int64_t dims_min, int64_t dims_max,
+                            int64_t* dims_out) {
+  if (n < 1) return fail(PIPEDP_E_INVALID_PARAMS, "n must be >= 1");
+  if (dims_min < 1 || dims_min > dims_max) return fail(PIPEDP_E_INVALID_PARAMS, "bad dimension range");
+  std::mt19937_64 rng(seed);
+  for (int64_t i = 0; i <= n; ++i)
+    dims_out[i] = dims_min + (int64_t)(rng() % (uint64_t)(dims_max - dims_min + 1));
+  return validate_mcm(dims_out, n + 1);
+}
+
+// ------------------------------------------------------------- S-DP ---
+int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
+                               const int64_t* h_offsets, const int64_t* h_init, int32_t op,
+                               int32_t device, pipedp_sdp_plan_t* plan_out) {
+  if (!plan_out) return fail(PIPEDP_E_INVALID_PARAMS, "plan_out is NULL");
+  *plan_out = nullptr;
+  if (batch < 1) return fail(PIPEDP_E_INVALID_PARAMS, "batch must be >= 1");
+  for (int64_t b = 0; b < batch; ++b) {
+    TRY(validate_sdp(h_offsets + b * k, k, a1, n));
+    if (h_offsets[b * k] != a1) return fail(PIPEDP_E_INIT_LENGTH_MISMATCH,
+                                            "instance %lld has a_1=%lld, batch a_1=%lld",
+                                            (long long)b, (long long)h_offsets[b * k], (long long)a1);
+  }
+  SdpDispatch d{};
+  TRY(plan_sdp(batch, n, k, a1, h_offsets, h_init, op, &d));
+  TRY(select_device(device));
+  auto* P = new pipedp_sdp_plan{};
+  CK(cudaGetDevice(&P->device));
+  P->batch = batch;
+  P->n = n;
+  P->k = k;
+  P->a1 = a1;
+  P->d = d;
+  cudaError_t e = cudaMalloc(&P->d_offsets, sizeof(int64_t) * batch * k);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(P->d_offsets, h_offsets, sizeof(int64_t) * batch * k, cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(P->d_offsets);
+    delete P;
+    return cuda_fail(e, "sdp plan upload");
+  }
+  *plan_out = P;
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_sdp_plan_execute(pipedp_sdp_plan_t P, const int64_t* d_init, int64_t* d_cells,
+                                void* stream) {
+  if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
+  CK(cudaSetDevice(P->device));
+  return launch_sdp(P->d, P->batch, P->d_offsets, d_init, d_cells, (cudaStream_t)stream);
+}
+
+int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, int32_t* bits,
+                                 int32_t* launches) {
+  if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
+  if (name && cap) snprintf(name, cap, "%s", sdp_kernel_name(P->d));
+  if (bits) *bits = P->d.bits;
+  if (launches) *launches = 1;
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t P) {
+  if (!P) return PIPEDP_OK;
+  cudaSetDevice(P->device);
+  cudaFree(P->d_offsets);
+  delete P;
+  return PIPEDP_OK;
+}
+
+static int32_t sdp_solve_host(int64_t batch, int64_t n, int64_t k, int64_t a1,
+                              const int64_t* offsets, const int64_t* init, int32_t op,
+                              int64_t* cells_out, int32_t device) {
+  pipedp_sdp_plan_t P = nullptr;
+  TRY(pipedp_sdp_plan_create(batch, n, k, a1, offsets, init, op, device, &P));
+  struct Guard {
+    pipedp_sdp_plan_t p;
+    ~Guard() { pipedp_sdp_plan_destroy(p); }
+  } guard{P};
+  Scope sc;
+  TRY(sc.init());
+  int64_t *d_init = nullptr, *d_cells = nullptr;
+  TRY(sc.alloc(&d_init, batch * a1));
+  TRY(sc.alloc(&d_cells, batch * n));
+  CK(cudaMemcpyAsync(d_init, init, sizeof(int64_t) * batch * a1, cudaMemcpyHostToDevice, sc.stream));
+  TRY(pipedp_sdp_plan_execute(P, d_init, d_cells, sc.stream));
+  CK(cudaMemcpyAsync(cells_out, d_cells, sizeof(int64_t) * batch * n, cudaMemcpyDeviceToHost,
+                     sc.stream));
+  CK(cudaStreamSynchronize(sc.stream));
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_sdp_solve(const int64_t* offsets, int64_t k, const int64_t* init,
+                         int64_t init_len, int64_t n, int32_t op, int64_t* cells_out,
+                         uint8_t* filled_out) {
+  TRY(validate_sdp(offsets, k, init_len, n));
+  TRY(sdp_solve_host(1, n, k, init_len, offsets, init, op, cells_out, -1));
+  if (filled_out) memset(filled_out, 1, (size_t)n);
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_sdp_solve_batch(int64_t batch, int64_t n, int64_t k, int64_t a1,
+                               const int64_t* offsets, const int64_t* init, int32_t op,
+                               int64_t* cells_out, int32_t device) {
+  return sdp_solve_host(batch, n, k, a1, offsets, init, op, cells_out, device);
+}
+
+// -------------------------------------------------------------- MCM ---
+int32_t pipedp_mcm_plan_create(int64_t batch, int64_t n, const int64_t* h_dims, int32_t kernel,
+                               int32_t device, pipedp_mcm_plan_t* plan_out) {
+  if (!plan_out) return fail(PIPEDP_E_INVALID_PARAMS, "plan_out is NULL");
+  *plan_out = nullptr;
+  if (batch < 1) return fail(PIPEDP_E_INVALID_PARAMS, "batch must be >= 1");
+  if (n < 1) return fail(PIPEDP_E_INVALID_PARAMS, "dimension vector needs at least two entries");
+  for (int64_t b = 0; b < batch; ++b) TRY(validate_mcm(h_dims + b * (n + 1), n + 1));
+  McmDispatch d{};
+  TRY(plan_mcm(batch, n, h_dims, kernel, &d));
+  TRY(select_device(device));
+  auto* P = new pipedp_mcm_plan{};
+  P->batch = batch;
+  P->n = n;
+  P->cc = n * (n + 1) / 2;
+  P->d = d;
+  auto cleanup = [&](cudaError_t e, const char* what) {
+    pipedp_mcm_plan_destroy(P);
+    return cuda_fail(e, what);
+  };
+  cudaError_t e = cudaGetDevice(&P->device);
+  std::vector<int32_t> p32((size_t)(batch * (n + 1)));
+  for (size_t i = 0; i < p32.size(); ++i) p32[i] = (int32_t)h_dims[i];
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_p, sizeof(int32_t) * p32.size());
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_p, p32.data(), sizeof(int32_t) * p32.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_dims, sizeof(int64_t) * p32.size());
+  if (e == cudaSuccess) e = cudaMemcpy(P->d_dims, h_dims, sizeof(int64_t) * p32.size(), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_overflow, sizeof(int));
+  if (e == cudaSuccess) e = cudaMallocHost(&P->h_overflow, sizeof(int));
+  if (e == cudaSuccess && d.kernel == PIPEDP_MCM_WAVEFRONT) {
+    std::vector<int64_t> base((size_t)n + 1, 0);
+    int64_t total = 0;
+    for (int64_t D = 1; D < n; ++D) {
+      base[(size_t)D] = total;
+      const int cpw = 32 / mcm_wave_group(D);
+      total += (n - D + cpw - 1) / cpw;
+    }
+    P->total_chunks = total;
+    e = cudaMalloc(&P->d_chunk_base, sizeof(int64_t) * (n + 1));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(P->d_chunk_base, base.data(), sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_done, sizeof(int) * std::max<int64_t>(total, 1));
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_next, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_v32, sizeof(uint32_t) * (P->cc + 1));
+  }
+  if (e != cudaSuccess) return cleanup(e, "mcm plan setup");
+  *plan_out = P;
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_mcm_plan_execute(pipedp_mcm_plan_t P, int64_t* d_cells, int64_t* d_split, void* stream) {
+  if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
+  CK(cudaSetDevice(P->device));
+  return mcm_execute(P, d_cells, d_split, (cudaStream_t)stream);
+}
+
+int32_t pipedp_mcm_plan_describe(pipedp_mcm_plan_t P, char* name, size_t cap, int32_t* bits,
+                                 int32_t* launches) {
+  if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
+  const char* nm = P->d.kernel == PIPEDP_MCM_SMEM ? "mcm_smem_cta"
+                   : P->d.kernel == PIPEDP_MCM_TOURNAMENT ? "mcm_tournament"
+                                                          : "mcm_wavefront";
+  if (name && cap) snprintf(name, cap, "%s", nm);
+  if (bits) *bits = P->last_bits ? P->last_bits : P->d.bits;
+  if (launches) *launches = P->launches;
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_mcm_plan_destroy(pipedp_mcm_plan_t P) {
+  if (!P) return PIPEDP_OK;
+  cudaSetDevice(P->device);
+  cudaFree(P->d_p);
+  cudaFree(P->d_dims);
+  cudaFree(P->d_v32);
+  cudaFree(P->d_chunk_base);
+  cudaFree(P->d_done);
+  cudaFree(P->d_next);
+  cudaFree(P->d_overflow);
+  if (P->h_overflow) cudaFreeHost(P->h_overflow);
+  delete P;
+  return PIPEDP_OK;
+}
+
+static int32_t mcm_solve_host(int64_t batch, int64_t n, const int64_t* dims, int32_t kernel,
+                              int64_t* cells_out, int64_t* split_out, int32_t device) {
+  pipedp_mcm_plan_t P = nullptr;
+  TRY(pipedp_mcm_plan_create(batch, n, dims, kernel, device, &P));
+  struct Guard {
+    pipedp_mcm_plan_t p;
+    ~Guard() { pipedp_mcm_plan_destroy(p); }
+  } guard{P};
+  const int64_t size = batch * (n * (n + 1) / 2 + 1);
+  Scope sc;
+  TRY(sc.init());
+  int64_t *d_cells = nullptr, *d_split = nullptr;
+  TRY(sc.alloc(&d_cells, size));
+  TRY(sc.alloc(&d_split, size));
+  TRY(pipedp_mcm_plan_execute(P, d_cells, d_split, sc.stream));
+  CK(cudaMemcpyAsync(cells_out, d_cells, sizeof(int64_t) * size, cudaMemcpyDeviceToHost, sc.stream));
+  if (split_out)
+    CK(cudaMemcpyAsync(split_out, d_split, sizeof(int64_t) * size, cudaMemcpyDeviceToHost, sc.stream));
+  CK(cudaStreamSynchronize(sc.stream));
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_mcm_solve(const int64_t* dims, int64_t dims_len, int32_t kernel,
+                         int64_t* cells_out, uint8_t* filled_out, int64_t* split_out) {
+  TRY(validate_mcm(dims, dims_len));
+  const int64_t n = dims_len - 1;
+  TRY(mcm_solve_host(1, n, dims, kernel, cells_out, split_out, -1));
+  if (filled_out) memset(filled_out, 1, (size_t)(n * (n + 1) / 2 + 1));
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_mcm_solve_batch(int64_t batch, int64_t n, const int64_t* dims, int64_t* cells_out,
+                               int64_t* split_out, int32_t device) {
+  return mcm_solve_host(batch, n, dims, PIPEDP_MCM_AUTO, cells_out, split_out, device);
+}
+
+int32_t pipedp_mcm_pipeline(const int64_t* dims, int64_t dims_len, int32_t mode,
+                            int64_t* cells_out, uint8_t* filled_out, int64_t* steps_out,
+                            int64_t* stall_out) {
+  TRY(validate_mcm(dims, dims_len));
+  const int64_t n = dims_len - 1;
+  if (n < 2) return fail(PIPEDP_E_INVALID_PARAMS, "pipeline needs at least two matrices");
+  if (mode != PIPEDP_MCM_PAPER_LITERAL && mode != PIPEDP_MCM_STALL_ON_HAZARD)
+    return fail(PIPEDP_E_INVALID_PARAMS, "unknown McmMode %d", mode);
+  TRY(select_device(-1));
+  const int64_t cc = n * (n + 1) / 2;
+  Scope sc;
+  TRY(sc.init());
+  int64_t *d_dims, *d_cells, *d_vhead, *d_wval, *d_steps;
+  int32_t *d_row, *d_diag, *d_wcount;
+  int8_t *d_state, *d_exec;
+  TRY(sc.alloc(&d_dims, n + 1));
+  TRY(sc.alloc(&d_cells, cc + 1));
+  TRY(sc.alloc(&d_vhead, n));
+  TRY(sc.alloc(&d_wval, n));
+  TRY(sc.alloc(&d_steps, 2));
+  TRY(sc.alloc(&d_row, cc + 1));
+  TRY(sc.alloc(&d_diag, cc + 1));
+  TRY(sc.alloc(&d_wcount, cc + 1));
+  TRY(sc.alloc(&d_state, n));
+  TRY(sc.alloc(&d_exec, n));
+  CK(cudaMemcpyAsync(d_dims, dims, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, sc.stream));
+  CK(cudaMemsetAsync(d_cells, 0, sizeof(int64_t) * (cc + 1), sc.stream));
+  CK(cudaMemsetAsync(d_wcount, 0, sizeof(int32_t) * (cc + 1), sc.stream));
+  CK(cudaMemsetAsync(d_steps, 0, sizeof(int64_t) * 2, sc.stream));
+  mcm_coord_table<<<(unsigned)std::min<int64_t>(4096, (cc + 255) / 256), 256, 0, sc.stream>>>(n, d_row, d_diag);
+  CK(cudaGetLastError());
+  McmLockstep S{n, mode == PIPEDP_MCM_STALL_ON_HAZARD, d_row, d_diag, d_wcount, d_vhead,
+                d_state, d_exec, d_wval, d_steps};
+  mcm_lockstep<<<1, 1024, 0, sc.stream>>>(S, d_dims, d_cells);
+  CK(cudaGetLastError());
+  int64_t h_steps[2];
+  CK(cudaMemcpyAsync(h_steps, d_steps, sizeof h_steps, cudaMemcpyDeviceToHost, sc.stream));
+  CK(cudaMemcpyAsync(cells_out, d_cells, sizeof(int64_t) * (cc + 1), cudaMemcpyDeviceToHost, sc.stream));
+  CK(cudaStreamSynchronize(sc.stream));
+  if (h_steps[1]) return fail(PIPEDP_E_STALL_LIVELOCK, "no lane can make progress");
+  if (filled_out) memset(filled_out, 1, (size_t)(cc + 1));
+  const int64_t heads = (cc + n - 2) - (n + 1) + 1;
+  if (steps_out) *steps_out = h_steps[0];
+  if (stall_out) *stall_out = h_steps[0] - heads;
+  return PIPEDP_OK;
+}
+
+// ------------------------------------------------------------ utilities ---
+}  // extern "C"
+
+namespace {
+__global__ void fnv_digest_kernel(const int64_t* __restrict__ t, int64_t count, int64_t ntables,
+                                  uint64_t* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= ntables) return;
+  const int64_t* c = t + i * count;
+  uint64_t h = 14695981039346656037ull;
+  auto mix = [&](uint64_t v) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      h ^= (v >> (8 * b)) & 0xffu;
+      h *= 1099511628211ull;
+    }
+  };
+  mix((uint64_t)count);
+  for (int64_t j = 0; j < count; ++j) mix((uint64_t)__ldg(c + j));
+  out[i] = h;
+}
+}  // namespace
+
+extern "C" {
+
+int32_t pipedp_digest_device(const int64_t* d_tables, int64_t count, int64_t ntables,
+                             uint64_t* d_digests, void* stream) {
+  if (ntables <= 0) return PIPEDP_OK;
+  fnv_digest_kernel<<<(unsigned)((ntables + 127) / 128), 128, 0, (cudaStream_t)stream>>>(
+      d_tables, count, ntables, d_digests);
+  CK(cudaGetLastError());
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_chain_step_ns(int32_t op, int32_t value_bits, int32_t device, double* ns_out,
+                             double* mhz_out) {
+  TRY(select_device(device));
+  Scope sc;
+  TRY(sc.init());
+  long long* d_cyc = nullptr;
+  int64_t* d_sink = nullptr;
+  TRY(sc.alloc(&d_cyc, 1));
+  TRY(sc.alloc(&d_sink, 32));
+  const int64_t batches = 1 << 16;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  auto run = [&]() -> int {
+    CK(cudaEventRecord(e0, sc.stream));
+    switch (op * 100 + value_bits) {
+      case 32: sdp_chain_step_probe<kMin, int32_t><<<1, 32, 0, sc.stream>>>(batches, 1, d_cyc, (int32_t*)d_sink); break;
+      case 64: sdp_chain_step_probe<kMin, int64_t><<<1, 32, 0, sc.stream>>>(batches, 1, d_cyc, d_sink); break;
+      case 132: sdp_chain_step_probe<kMax, int32_t><<<1, 32, 0, sc.stream>>>(batches, 1, d_cyc, (int32_t*)d_sink); break;
+      case 164: sdp_chain_step_probe<kMax, int64_t><<<1, 32, 0, sc.stream>>>(batches, 1, d_cyc, d_sink); break;
+      case 264: sdp_chain_step_probe<kSatAdd, int64_t><<<1, 32, 0, sc.stream>>>(batches, 1, d_cyc, d_sink); break;
+      case 332: sdp_chain_step_probe<kModAdd, int32_t><<<1, 32, 0, sc.stream>>>(batches, 1, d_cyc, (int32_t*)d_sink); break;
+      case 364: sdp_chain_step_probe<kModAdd, int64_t><<<1, 32, 0, sc.stream>>>(batches, 1, d_cyc, d_sink); break;
+      default: return fail(PIPEDP_E_INVALID_PARAMS, "no chain probe for op %d at %d bits", op, value_bits);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e1, sc.stream));
+    CK(cudaEventSynchronize(e1));
+    return PIPEDP_OK;
+  };
+  TRY(run());  // warm-up
+  TRY(run());
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  long long cyc = 0;
+  CK(cudaMemcpy(&cyc, d_cyc, sizeof cyc, cudaMemcpyDeviceToHost));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double steps = (double)batches * 32.0;
+  if (ns_out) *ns_out = ms * 1e6 / steps;
+  if (mhz_out) *mhz_out = (double)cyc / (ms * 1e3);
+  return PIPEDP_OK;
+}
+
+}  // extern "C"

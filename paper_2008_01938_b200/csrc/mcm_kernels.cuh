@@ -1,0 +1,388 @@
+// mcm_kernels.cuh -- matrix-chain-multiplication table fill for sm_100a.
+//
+// Reference semantics (mcm.cpp:85-110, terms from mcm.cpp:55-75): cells are
+// addressed 1-based in diagonal-major order, lin(r,c) = D*n - D(D-1)/2 + r with
+// D = c - r; slot 0 and the n base cells are 0.  For a computed cell (r, c)
+//   best = min_{j=1..D} cells[lin(r, r+j-1)] + cells[lin(r+j, c)] + p[r-1]*p[r+j-1]*p[c]
+// with the FIRST minimal j recorded as split (strict '<' while scanning j up).
+// Every kernel here reduces on the pair (value, j) lexicographically, which is
+// order-free and equals that first-min rule exactly.
+//
+// Layout: the kernels keep the reference's diagonal-major layout.  It is the
+// layout the dataflow wavefront wants: for 32 consecutive cells (r .. r+31) of
+// one diagonal, the left operand of term j lies on diagonal j-1 at rows
+// r..r+31 and the right operand on diagonal D-j at rows r+j..r+j+31 -- both
+// contiguous, so every warp load is one coalesced 128-byte line.
+//
+// Value width: 'uint32_t' kernels are used when max_dim^3 < 2^31; they keep
+// every finalised value below 2^30 (so v_l + v_r + w never wraps) and raise a
+// device flag if a value reaches 2^30, in which case the host reruns the
+// instance with the int64 kernel (both on the GPU).
+#pragma once
+
+#include "common.cuh"
+
+namespace pipedp_dev {
+
+constexpr uint32_t kMcm32Limit = 1u << 30;
+
+__host__ __device__ __forceinline__ int64_t mcm_dbase(int64_t d, int64_t n) {
+  return d * n - d * (d - 1) / 2;  // lin(r, r+d) = dbase(d) + r   (mcm.cpp:35-36)
+}
+
+template <typename T>
+__device__ __forceinline__ T ldcg_t(const T* p);
+template <>
+__device__ __forceinline__ uint32_t ldcg_t<uint32_t>(const uint32_t* p) { return __ldcg(p); }
+template <>
+__device__ __forceinline__ int64_t ldcg_t<int64_t>(const int64_t* p) {
+  return (int64_t)__ldcg(reinterpret_cast<const long long*>(p));
+}
+
+template <typename T>
+struct McmBest {
+  T v;
+  int32_t j;
+};
+
+template <typename T>
+__device__ __forceinline__ void mcm_take(McmBest<T>& b, T v, int32_t j) {
+  if (v < b.v || (v == b.v && j < b.j)) {
+    b.v = v;
+    b.j = j;
+  }
+}
+
+template <typename T>
+__device__ __forceinline__ McmBest<T> mcm_group_reduce(McmBest<T> b, int group) {
+  for (int s = group >> 1; s > 0; s >>= 1) {
+    const T ov = __shfl_xor_sync(0xffffffffu, b.v, s);
+    const int32_t oj = __shfl_xor_sync(0xffffffffu, b.j, s);
+    mcm_take(b, ov, oj);
+  }
+  return b;
+}
+
+template <typename T>
+__device__ __forceinline__ T mcm_max_value();
+template <>
+__device__ __forceinline__ uint32_t mcm_max_value<uint32_t>() { return 0xFFFFFFFFu; }
+template <>
+__device__ __forceinline__ int64_t mcm_max_value<int64_t>() { return INT64_MAX; }
+
+// Terms j = j0, j0+G, ... <= D of cell (r, r+D) over a diagonal-major table V.
+template <typename T, typename Load>
+__device__ __forceinline__ McmBest<T> mcm_cell_terms(const T* V, const int32_t* __restrict__ p,
+                                                     int64_t n, int64_t r, int64_t D, int j0,
+                                                     int G, Load load) {
+  McmBest<T> best{mcm_max_value<T>(), 0};
+  const int64_t c = r + D;
+  const T prc = (T)p[r - 1] * (T)p[c];
+  for (int64_t j = j0; j <= D; j += G) {
+    const T left = load(V + mcm_dbase(j - 1, n) + r);
+    const T right = load(V + mcm_dbase(D - j, n) + r + j);
+    const T cost = left + right + prc * (T)p[r + j - 1];
+    mcm_take(best, cost, (int32_t)j);
+  }
+  return best;
+}
+
+// -----------------------------------------------------------------------------
+// Small n: one CTA per instance, the whole triangle in shared memory,
+// diagonal by diagonal (n-1 __syncthreads).  Also the batched kernel.
+// Output per instance: cells / split int64 in the reference layout.
+template <typename T>
+__global__ void __launch_bounds__(512)
+    mcm_smem_cta(int64_t n, int64_t batch, const int64_t* __restrict__ g_dims,
+                 int64_t* __restrict__ out_cells, int64_t* __restrict__ out_split,
+                 int* __restrict__ overflow) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t inst = blockIdx.x;
+  if (inst >= batch) return;
+  const int64_t cc = n * (n + 1) / 2;
+  T* V = reinterpret_cast<T*>(smem);  // cc + 1 entries
+  int32_t* p = reinterpret_cast<int32_t*>(V + ((cc + 1 + 3) & ~3ll));
+  const int64_t* gd = g_dims + inst * (n + 1);
+  int64_t* oc = out_cells + inst * (cc + 1);
+  int64_t* os = out_split + inst * (cc + 1);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int64_t i = tid; i <= n; i += nt) {
+    p[i] = (int32_t)gd[i];
+    V[i] = T(0);
+    oc[i] = 0;
+    os[i] = 0;
+  }
+  __syncthreads();
+  bool ovf = false;
+  for (int64_t D = 1; D < n; ++D) {
+    const int64_t ncell = n - D;
+    int G = 1;  // lanes per cell: spread the terms when the diagonal is short
+    while (G < 32 && ncell * G * 2 <= nt && G < D) G <<= 1;
+    const int64_t slots = (int64_t)(nt / G) * G;
+    const int64_t db = mcm_dbase(D, n);
+    for (int64_t base = 0; base < ncell * G; base += slots) {
+      const int64_t t = base + tid;
+      const bool live = tid < slots && t < ncell * G;
+      McmBest<T> best{mcm_max_value<T>(), 0};
+      const int64_t r = 1 + t / G;
+      if (live) {
+        best = mcm_cell_terms<T>(V, p, n, r, D, 1 + (int)(t % G), G,
+                                 [](const T* a) { return *a; });
+      }
+      if (G > 1) best = mcm_group_reduce(best, G);
+      if (live && (t % G) == 0) {
+        V[db + r] = best.v;
+        oc[db + r] = (int64_t)best.v;
+        os[db + r] = best.j;
+        if (sizeof(T) == 4 && (uint64_t)best.v >= kMcm32Limit) ovf = true;
+      }
+    }
+    __syncthreads();
+  }
+  if (ovf) atomicOr(overflow, 1);
+}
+
+// -----------------------------------------------------------------------------
+// Large n: persistent multi-SM dataflow wavefront.  Work items ("chunks") are
+// CPW = 32/G consecutive cells of one diagonal, handed out in address order by
+// an atomic counter; G = lanes per cell grows with D so per-lane work stays
+// bounded.  A chunk on diagonal D waits only for the (at most two) chunks of
+// diagonal D-1 holding rows r_lo .. r_hi+1 -- the cells (r, c-1) and (r+1, c)
+// whose finality implies that of every other operand.  Flags are released with
+// st.release.gpu after a gpu-scope fence; operands are read with ld.global.cg
+// (L2) so no stale L1 line can be observed.
+struct McmWave {
+  int64_t n;
+  int64_t total_chunks;
+  const int64_t* chunk_base;  // [n]: first chunk index of diagonal D (D = 1..n-1), [0] unused
+  int* done;                  // [total_chunks] completion flags
+  unsigned long long* next;   // work counter
+};
+
+__host__ __device__ __forceinline__ int mcm_wave_group(int64_t D) {
+  int G = 1;
+  while (G < 32 && D > 48 * G) G <<= 1;
+  return G;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+    mcm_wavefront(const McmWave W, const int32_t* __restrict__ p, T* V, int64_t* out_cells,
+                  int64_t* __restrict__ out_split,
+                  int* __restrict__ overflow) {
+  const int lane = threadIdx.x & 31;
+  const int64_t n = W.n;
+  for (;;) {
+    unsigned long long idx = 0;
+    if (lane == 0) idx = atomicAdd(W.next, 1ull);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if ((int64_t)idx >= W.total_chunks) return;
+    // diagonal of this chunk: chunk_base is increasing over D = 1..n-1
+    int64_t lo = 1, hi = n - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (__ldg(W.chunk_base + mid) <= (int64_t)idx) lo = mid; else hi = mid - 1;
+    }
+    const int64_t D = lo;
+    const int64_t q = (int64_t)idx - __ldg(W.chunk_base + D);
+    const int G = mcm_wave_group(D);
+    const int cpw = 32 / G;
+    const int64_t r_lo = q * cpw + 1;
+    const int64_t r_hi = min(r_lo + cpw - 1, n - D);
+    if (D > 1) {  // wait for rows r_lo .. r_hi+1 of diagonal D-1
+      const int cpw1 = 32 / mcm_wave_group(D - 1);
+      const int64_t b1 = __ldg(W.chunk_base + D - 1);
+      const int64_t q1 = (r_lo - 1) / cpw1, q2 = r_hi / cpw1;
+      for (int64_t qq = q1; qq <= q2; ++qq) {
+        while (ld_acquire_gpu_i32(W.done + b1 + qq) == 0) __nanosleep(32);
+      }
+    }
+    const int64_t r = r_lo + lane / G;
+    const bool live = r <= r_hi;
+    McmBest<T> best{mcm_max_value<T>(), 0};
+    if (live) {
+      best = mcm_cell_terms<T>(V, p, n, r, D, 1 + (lane % G), G,
+                               [](const T* a) { return ldcg_t<T>(a); });
+    }
+    if (G > 1) best = mcm_group_reduce(best, G);
+    if (live && (lane % G) == 0) {
+      const int64_t a = mcm_dbase(D, n) + r;
+      V[a] = best.v;
+      if (sizeof(T) == 4) {
+        out_cells[a] = (int64_t)best.v;
+        if ((uint64_t)best.v >= kMcm32Limit) atomicOr(overflow, 1);
+      }
+      out_split[a] = best.j;
+    }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) st_release_gpu_i32(W.done + idx, 1);
+  }
+}
+
+// -----------------------------------------------------------------------------
+// The paper's O(n^2 log n) comparison method: cells one
+// at a time in address order; the CTA evaluates the D terms of the cell in
+// parallel and reduces them in a ceil(log2 D)-level tournament with a barrier
+// per level.  Single CTA; the table lives in global memory.
+__global__ void __launch_bounds__(1024, 1)
+    mcm_tournament(int64_t n, const int64_t* __restrict__ g_dims, int64_t* __restrict__ cells,
+                   int64_t* __restrict__ split) {
+  __shared__ int64_t sv[1024];
+  __shared__ int32_t sj[1024];
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t cc = n * (n + 1) / 2;
+  for (int64_t i = tid; i <= n; i += nt) {
+    cells[i] = 0;
+    split[i] = 0;
+  }
+  __syncthreads();
+  int64_t addr = n + 1;
+  for (int64_t D = 1; D < n; ++D) {
+    int P = 1;
+    while (P < D && P < nt) P <<= 1;
+    for (int64_t r = 1; r + D <= n; ++r, ++addr) {
+      const int64_t c = r + D;
+      McmBest<int64_t> best{INT64_MAX, 0};
+      if (tid < P) {
+        const int64_t prc = g_dims[r - 1] * g_dims[c];
+        for (int64_t j = tid + 1; j <= D; j += P) {
+          const int64_t cost = cells[mcm_dbase(j - 1, n) + r] + cells[mcm_dbase(D - j, n) + r + j] +
+                               prc * g_dims[r + j - 1];
+          mcm_take(best, cost, (int32_t)j);
+        }
+        sv[tid] = best.v;
+        sj[tid] = best.j;
+      }
+      __syncthreads();
+      for (int s = P >> 1; s > 0; s >>= 1) {  // tournament levels
+        if (tid < s) {
+          McmBest<int64_t> a{sv[tid], sj[tid]};
+          mcm_take(a, sv[tid + s], sj[tid + s]);
+          sv[tid] = a.v;
+          sj[tid] = a.j;
+        }
+        __syncthreads();
+      }
+      if (tid == 0) {
+        cells[addr] = sv[0];
+        split[addr] = sj[0];
+      }
+      __syncthreads();
+    }
+  }
+  (void)cc;
+}
+
+// -----------------------------------------------------------------------------
+// Exact lock-step emulation of the reference engine running McmProgram
+// (engine.hpp:134-433 + mcm_pipeline.hpp:22-84): lanes j = 1..n-1 with their
+// own vhead; per iteration a plan phase (stall mode: operands must have all
+// their writes, own cell exactly j-1), a read/compute phase against the table
+// of the previous iteration, and a write phase.  Reproduces the table, the
+// step count and the stall count of both McmMode values bit-for-bit.
+struct McmLockstep {
+  int64_t n;
+  int stall;
+  const int32_t* row;   // [cc+1]
+  const int32_t* diag;  // [cc+1]
+  int32_t* wcount;      // [cc+1] writes applied
+  int64_t* vhead;       // [n]
+  int8_t* state;        // [n] 0 running, 1 done
+  int8_t* exec;         // [n]
+  int64_t* wval;        // [n]
+  int64_t* steps_out;   // [2] steps, error flag
+};
+
+__global__ void mcm_coord_table(int64_t n, int32_t* row, int32_t* diag) {
+  // one thread per (D, r); the grid covers all cells
+  const int64_t cc = n * (n + 1) / 2;
+  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + 1; a <= cc;
+       a += (int64_t)gridDim.x * blockDim.x) {
+    // invert dbase: largest D with dbase(D) < a
+    double nn = (double)n + 0.5;
+    int64_t D = (int64_t)(nn - sqrt(nn * nn - 2.0 * (double)(a - 1)));
+    if (D < 0) D = 0;
+    if (D > n - 1) D = n - 1;
+    while (D > 0 && mcm_dbase(D, n) >= a) --D;
+    while (D + 1 <= n - 1 && mcm_dbase(D + 1, n) < a) ++D;
+    row[a] = (int32_t)(a - mcm_dbase(D, n));
+    diag[a] = (int32_t)D;
+  }
+}
+
+__global__ void __launch_bounds__(1024, 1)
+    mcm_lockstep(const McmLockstep S, const int64_t* __restrict__ g_dims, int64_t* cells) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int64_t n = S.n;
+  const int64_t cc = n * (n + 1) / 2;
+  const int64_t first = n + 1, last = cc + n - 2;
+  const int64_t lanes = n - 1;
+  const int64_t budget = (last - first + 1) * (lanes + 2) + 16;
+  for (int64_t j = tid + 1; j <= lanes; j += nt) {
+    S.vhead[j] = first;
+    S.state[j] = 0;
+  }
+  __syncthreads();
+  int64_t steps = 0;
+  for (;;) {
+    bool all_done = true, any_exec = false;
+    for (int64_t j = tid + 1; j <= lanes; j += nt) {
+      int8_t e = 0;
+      if (!S.state[j]) {
+        all_done = false;
+        const int64_t cell = S.vhead[j] - j + 1;
+        const bool active = cell >= n + 1 && cell <= cc && j <= S.diag[cell];
+        if (!active) {
+          e = 2;
+        } else {
+          bool ready = true;
+          if (S.stall) {
+            const int64_t r = S.row[cell], D = S.diag[cell];
+            const int64_t left = mcm_dbase(j - 1, n) + r;
+            const int64_t right = mcm_dbase(D - j, n) + r + j;
+            if (left > n && S.wcount[left] < S.diag[left]) ready = false;
+            if (right > n && S.wcount[right] < S.diag[right]) ready = false;
+            if (S.wcount[cell] != j - 1) ready = false;
+          }
+          e = ready ? 1 : 0;
+        }
+        if (e) any_exec = true;
+        if (e == 1) {
+          const int64_t r = S.row[cell], D = S.diag[cell], c = r + D;
+          const int64_t vs = cells[mcm_dbase(j - 1, n) + r] + cells[mcm_dbase(D - j, n) + r + j] +
+                             g_dims[r - 1] * g_dims[r + j - 1] * g_dims[c];
+          const int64_t own = cells[cell];
+          S.wval[j] = j == 1 ? vs : (own < vs ? own : vs);
+        }
+      }
+      S.exec[j] = e;
+    }
+    all_done = __syncthreads_and(all_done);
+    if (all_done) break;
+    any_exec = __syncthreads_or(any_exec);
+    if (!any_exec || steps > budget) {
+      if (tid == 0) S.steps_out[1] = 1;  // livelock (engine.hpp:352-362)
+      return;
+    }
+    for (int64_t j = tid + 1; j <= lanes; j += nt) {
+      const int8_t e = S.exec[j];
+      if (e == 1) {
+        const int64_t cell = S.vhead[j] - j + 1;
+        cells[cell] = S.wval[j];
+        S.wcount[cell] += 1;
+      }
+      if (e) {
+        if (++S.vhead[j] > last) S.state[j] = 1;
+      }
+    }
+    ++steps;
+    __syncthreads();
+  }
+  if (tid == 0) {
+    S.steps_out[0] = steps;
+    S.steps_out[1] = 0;
+  }
+}
+
+}  // namespace pipedp_dev

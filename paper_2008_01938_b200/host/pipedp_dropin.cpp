@@ -1,0 +1,348 @@
+// pipedp_dropin.cpp -- the reference's C++ solver entry points (namespace
+// pipedp, include/pipedp/*.hpp) implemented over the C ABI of
+// include/pipedp_cuda.h.  Same signatures, same validation order and errc,
+// same returned values; the tables come from the sm_100a kernels.  A C ABI
+// status >= 100 (no GPU, CUDA error) becomes pipedp::DeviceError -- there is no
+// CPU solver behind these functions.
+#include <algorithm>
+#include <cstdio>
+#include <string>
+
+#include "pipedp/error.hpp"
+#include "pipedp/generate.hpp"
+#include "pipedp/mcm.hpp"
+#include "pipedp/mcm_pipeline.hpp"
+#include "pipedp/sdp.hpp"
+#include "pipedp/sdp_pipeline.hpp"
+#include "pipedp/semigroup.hpp"
+#include "pipedp/table.hpp"
+#include "pipedp_cuda.h"
+
+namespace pipedp {
+
+namespace {
+
+void check(int32_t status) {
+  if (status == PIPEDP_OK) return;
+  std::string msg = pipedp_last_error();
+  if (status >= 1 && status <= 11) {
+    // strip the "Name: " prefix the C layer adds; Error re-adds it
+    const auto colon = msg.find(": ");
+    throw Error(static_cast<errc>(status - 1), colon == std::string::npos ? msg : msg.substr(colon + 2));
+  }
+  throw DeviceError(status, msg);
+}
+
+SolutionTable full_table(std::int64_t size) {
+  SolutionTable t;
+  t.cells.assign(static_cast<std::size_t>(size), 0);
+  t.filled.assign(static_cast<std::size_t>(size), 1);
+  return t;
+}
+
+std::int64_t ceil_log2(std::int64_t k) {  // sdp.cpp:78-80
+  std::int64_t r = 0;
+  while ((std::int64_t{1} << r) < k) ++r;
+  return r;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ L0 ---
+const char* errc_name(errc code) {
+  static const char* names[] = {"NonDecreasingOffsets", "NonPositiveOffset", "InitLengthMismatch",
+                                "TableTooSmall",        "CoordOutOfRange",   "AddressOutOfRange",
+                                "BaseCellHasNoDeps",    "TooLargeForBruteForce",
+                                "StallLivelock",        "WeightOverflow",    "InvalidParams"};
+  const int i = static_cast<int>(code);
+  return i >= 0 && i < 11 ? names[i] : "UnknownError";
+}
+
+std::int64_t SemigroupOp::apply(std::int64_t a, std::int64_t b) const {
+  switch (kind) {
+    case OpKind::min:
+      return std::min(a, b);
+    case OpKind::max:
+      return std::max(a, b);
+    case OpKind::saturating_add: {
+      std::int64_t out;
+      if (__builtin_add_overflow(a, b, &out)) return b > 0 ? INT64_MAX : INT64_MIN;
+      return out;
+    }
+    case OpKind::modular_add: {
+      auto norm = [](std::int64_t v) {
+        const std::int64_t r = v % kModulus;
+        return r < 0 ? r + kModulus : r;
+      };
+      return (norm(a) + norm(b)) % kModulus;
+    }
+  }
+  fail(errc::invalid_params, "unknown operator kind");
+}
+
+std::string_view SemigroupOp::name() const {
+  switch (kind) {
+    case OpKind::min: return "min";
+    case OpKind::max: return "max";
+    case OpKind::saturating_add: return "saturating-add";
+    case OpKind::modular_add: return "modular-add";
+  }
+  return "?";
+}
+
+SemigroupOp SemigroupOp::from_name(std::string_view name) {
+  for (const SemigroupOp& op : catalog())
+    if (op.name() == name) return op;
+  fail(errc::invalid_params, "unknown operator name: " + std::string(name));
+}
+
+const std::array<SemigroupOp, 4>& SemigroupOp::catalog() {
+  static const std::array<SemigroupOp, 4> ops = {SemigroupOp{OpKind::min}, SemigroupOp{OpKind::max},
+                                                 SemigroupOp{OpKind::saturating_add},
+                                                 SemigroupOp{OpKind::modular_add}};
+  return ops;
+}
+
+bool SolutionTable::all_filled() const {
+  return std::all_of(filled.begin(), filled.end(), [](std::uint8_t f) { return f != 0; });
+}
+
+std::uint64_t table_digest(const SolutionTable& table) {
+  return pipedp_table_digest(table.cells.data(), static_cast<std::int64_t>(table.cells.size()));
+}
+
+std::string digest_hex(std::uint64_t digest) {
+  char buf[17];
+  std::snprintf(buf, sizeof buf, "%016llx", static_cast<unsigned long long>(digest));
+  return buf;
+}
+
+// ----------------------------------------------------------------- S-DP ---
+const SdpInstance& validate(const SdpInstance& inst) {
+  check(pipedp_sdp_validate(inst.offsets.offsets.data(), inst.offsets.k(),
+                            static_cast<std::int64_t>(inst.init.size()), inst.n));
+  return inst;
+}
+
+SolutionTable initial_table(const SdpInstance& inst) {  // sdp.cpp:34-41
+  SolutionTable table(inst.n);
+  for (std::size_t i = 0; i < inst.init.size(); ++i) {
+    table.cells[i] = inst.init[i];
+    table.filled[i] = 1;
+  }
+  return table;
+}
+
+SolutionTable solve_sequential(const SdpInstance& inst) {
+  validate(inst);
+  SolutionTable t = full_table(inst.n);
+  check(pipedp_sdp_solve(inst.offsets.offsets.data(), inst.offsets.k(), inst.init.data(),
+                         static_cast<std::int64_t>(inst.init.size()), inst.n,
+                         static_cast<int32_t>(inst.op.kind), t.cells.data(), nullptr));
+  return t;
+}
+
+PrefixParallelResult solve_prefix_parallel(const SdpInstance& inst) {  // sdp.cpp:91-100
+  PrefixParallelResult r;
+  r.table = solve_sequential(inst);
+  r.depth_per_cell = ceil_log2(inst.offsets.k());
+  r.modeled_steps = (inst.n - inst.offsets.a1()) * std::max<std::int64_t>(r.depth_per_cell, 1);
+  return r;
+}
+
+NaiveParallelResult solve_naive_parallel(const SdpInstance& inst) {  // sdp.cpp:102-111
+  NaiveParallelResult r;
+  r.table = solve_sequential(inst);
+  r.serialized_accesses_per_cell = inst.offsets.k() - 1;
+  r.modeled_steps = (inst.n - inst.offsets.a1()) * inst.offsets.k();
+  return r;
+}
+
+std::vector<SolutionTable> solve_sequential_batch(const std::vector<SdpInstance>& insts, int device) {
+  std::vector<SolutionTable> out;
+  if (insts.empty()) return out;
+  const SdpInstance& f = insts.front();
+  const std::int64_t n = f.n, k = f.offsets.k(), a1 = f.offsets.a1(), b = (std::int64_t)insts.size();
+  std::vector<std::int64_t> offs, init, cells(static_cast<std::size_t>(b * n));
+  for (const SdpInstance& s : insts) {
+    validate(s);
+    if (s.n != n || s.offsets.k() != k || s.offsets.a1() != a1 || s.op != f.op)
+      fail(errc::invalid_params, "batched instances must share n, k, a_1 and the operator");
+    offs.insert(offs.end(), s.offsets.offsets.begin(), s.offsets.offsets.end());
+    init.insert(init.end(), s.init.begin(), s.init.end());
+  }
+  check(pipedp_sdp_solve_batch(b, n, k, a1, offs.data(), init.data(), static_cast<int32_t>(f.op.kind),
+                               cells.data(), device));
+  out.reserve(insts.size());
+  for (std::int64_t i = 0; i < b; ++i) {
+    SolutionTable t;
+    t.cells.assign(cells.begin() + i * n, cells.begin() + (i + 1) * n);
+    t.filled.assign(static_cast<std::size_t>(n), 1);
+    out.push_back(std::move(t));
+  }
+  return out;
+}
+
+ConflictRunAnalysis analyze_conflict_runs(const OffsetSet& offsets) {  // sdp_pipeline.cpp:17-32
+  ConflictRunAnalysis a;
+  const auto& v = offsets.offsets;
+  const int k = static_cast<int>(v.size());
+  int start = 1;
+  for (int r = 1; r <= k; ++r) {
+    if (r < k && v[r - 1] == v[r] + 1) continue;
+    a.runs.emplace_back(start, r);
+    a.run_lengths.push_back(r - start + 1);
+    a.longest_run = std::max(a.longest_run, r - start + 1);
+    start = r + 1;
+  }
+  return a;
+}
+
+SdpPipelineResult solve_sdp_pipeline(const SdpInstance& inst, const SdpRunConfig&) {
+  SdpPipelineResult r;
+  r.table = solve_sequential(inst);
+  // SdpProgram head range [a_1, n+k-2] (sdp_pipeline.hpp:20), never stalls
+  r.trace.first_head = inst.offsets.a1();
+  r.trace.steps_executed = inst.n + inst.offsets.k() - inst.offsets.a1() - 1;
+  r.trace.stall_iterations = 0;
+  r.trace.collected = false;
+  return r;
+}
+
+// ------------------------------------------------------------------ MCM ---
+const McmInstance& validate(const McmInstance& inst) {
+  check(pipedp_mcm_validate(inst.dims.data(), static_cast<std::int64_t>(inst.dims.size())));
+  return inst;
+}
+
+std::int64_t lin(TriCoord c, std::int64_t n) {  // mcm.cpp:30-37
+  if (c.row < 1 || c.row > c.col || c.col > n)
+    fail(errc::coord_out_of_range, "(" + std::to_string(c.row) + "," + std::to_string(c.col) +
+                                       ") outside the order-" + std::to_string(n) + " triangle");
+  const std::int64_t d = c.col - c.row;
+  return d * n - d * (d - 1) / 2 + c.row;
+}
+
+TriCoord coord(std::int64_t address, std::int64_t n) {  // mcm.cpp:39-53
+  if (address < 1 || address > cell_count(n))
+    fail(errc::address_out_of_range, "address " + std::to_string(address) + " outside table of " +
+                                         std::to_string(cell_count(n)) + " cells");
+  std::int64_t d = 0, base = 0;
+  while (address > base + (n - d)) {
+    base += n - d;
+    ++d;
+  }
+  const std::int64_t row = address - base;
+  return TriCoord{row, row + d};
+}
+
+std::vector<DependencyTerm> deps(std::int64_t address, const McmInstance& inst) {  // mcm.cpp:55-75
+  const std::int64_t n = inst.n();
+  const TriCoord cell = coord(address, n);
+  if (cell.diagonal() == 0)
+    fail(errc::base_cell_has_no_deps,
+         "cell " + std::to_string(address) + " is preset and has no dependencies");
+  std::vector<DependencyTerm> terms;
+  terms.reserve(static_cast<std::size_t>(cell.diagonal()));
+  const auto& p = inst.dims;
+  for (std::int64_t j = 1; j <= cell.diagonal(); ++j) {
+    terms.push_back({lin({cell.row, cell.row + j - 1}, n), lin({cell.row + j, cell.col}, n),
+                     p[cell.row - 1] * p[cell.row + j - 1] * p[cell.col]});
+  }
+  return terms;
+}
+
+SolutionTable mcm_initial_table(const McmInstance& inst) {  // mcm.cpp:77-83
+  const std::int64_t n = inst.n();
+  SolutionTable table(cell_count(n) + 1);
+  for (std::int64_t i = 0; i <= n; ++i) table.filled[static_cast<std::size_t>(i)] = 1;
+  return table;
+}
+
+namespace {
+SolutionTable mcm_solve(const McmInstance& inst, std::vector<std::int64_t>* split, int32_t kernel) {
+  validate(inst);
+  const std::int64_t size = cell_count(inst.n()) + 1;
+  SolutionTable t = full_table(size);
+  if (split) split->assign(static_cast<std::size_t>(size), 0);
+  check(pipedp_mcm_solve(inst.dims.data(), static_cast<std::int64_t>(inst.dims.size()), kernel,
+                         t.cells.data(), nullptr, split ? split->data() : nullptr));
+  return t;
+}
+}  // namespace
+
+SolutionTable solve_mcm_sequential(const McmInstance& inst, std::vector<std::int64_t>* split) {
+  return mcm_solve(inst, split, PIPEDP_MCM_AUTO);
+}
+
+SolutionTable solve_mcm_tournament(const McmInstance& inst, std::vector<std::int64_t>* split) {
+  return mcm_solve(inst, split, PIPEDP_MCM_TOURNAMENT);
+}
+
+std::vector<SolutionTable> solve_mcm_batch(const std::vector<McmInstance>& insts,
+                                           std::vector<std::vector<std::int64_t>>* splits, int device) {
+  std::vector<SolutionTable> out;
+  if (insts.empty()) return out;
+  const std::int64_t n = insts.front().n(), b = (std::int64_t)insts.size();
+  const std::int64_t size = cell_count(n) + 1;
+  std::vector<std::int64_t> dims, cells(static_cast<std::size_t>(b * size)),
+      split(static_cast<std::size_t>(b * size));
+  for (const McmInstance& m : insts) {
+    validate(m);
+    if (m.n() != n) fail(errc::invalid_params, "batched MCM instances must share n");
+    dims.insert(dims.end(), m.dims.begin(), m.dims.end());
+  }
+  check(pipedp_mcm_solve_batch(b, n, dims.data(), cells.data(), split.data(), device));
+  if (splits) splits->clear();
+  for (std::int64_t i = 0; i < b; ++i) {
+    SolutionTable t;
+    t.cells.assign(cells.begin() + i * size, cells.begin() + (i + 1) * size);
+    t.filled.assign(static_cast<std::size_t>(size), 1);
+    out.push_back(std::move(t));
+    if (splits) splits->emplace_back(split.begin() + i * size, split.begin() + (i + 1) * size);
+  }
+  return out;
+}
+
+McmPipelineResult solve_mcm_pipeline(const McmInstance& inst, const McmScheduleConfig& cfg) {
+  validate(inst);  // build_mcm_program: validate, then n >= 2 (mcm_pipeline.cpp:26-30)
+  if (inst.n() < 2) fail(errc::invalid_params, "pipeline needs at least two matrices");
+  McmPipelineResult r;
+  r.table = full_table(cell_count(inst.n()) + 1);
+  std::int64_t steps = 0, stalls = 0;
+  check(pipedp_mcm_pipeline(inst.dims.data(), static_cast<std::int64_t>(inst.dims.size()),
+                            cfg.mode == McmMode::stall_on_hazard ? PIPEDP_MCM_STALL_ON_HAZARD
+                                                                 : PIPEDP_MCM_PAPER_LITERAL,
+                            r.table.cells.data(), nullptr, &steps, &stalls));
+  r.trace.first_head = inst.n() + 1;
+  r.trace.steps_executed = steps;
+  r.trace.stall_iterations = stalls;
+  r.trace.collected = false;
+  return r;
+}
+
+// ------------------------------------------------------------ generators ---
+SdpInstance generate_sdp(const SdpGenParams& p) {
+  if (p.k < 1) fail(errc::invalid_params, "k must be >= 1");
+  const std::int64_t cap = p.consecutive ? p.k : (p.a1_cap > 0 ? p.a1_cap : 2 * p.k);
+  SdpInstance inst;
+  inst.n = p.n;
+  inst.op = p.op;
+  inst.offsets.offsets.assign(static_cast<std::size_t>(p.k), 0);
+  inst.init.assign(static_cast<std::size_t>(std::max(cap, p.k)), 0);
+  std::int64_t a1 = 0;
+  check(pipedp_generate_sdp(p.n, p.k, static_cast<int32_t>(p.op.kind), p.seed, p.consecutive ? 1 : 0,
+                            p.a1_cap, inst.offsets.offsets.data(), inst.init.data(),
+                            static_cast<std::int64_t>(inst.init.size()), &a1));
+  inst.init.resize(static_cast<std::size_t>(a1));
+  return inst;
+}
+
+McmInstance generate_mcm(const McmGenParams& p) {
+  McmInstance inst;
+  if (p.n >= 1) inst.dims.assign(static_cast<std::size_t>(p.n + 1), 0);
+  check(pipedp_generate_mcm(p.n, p.seed, p.dims_min, p.dims_max, inst.dims.data()));
+  return inst;
+}
+
+}  // namespace pipedp

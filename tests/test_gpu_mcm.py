@@ -1,0 +1,80 @@
+"""MCM parity on the GPU: cells AND split tables bit-exact against the C
+restatement of solve_mcm_sequential, lock-step pipeline tables / step counts
+against the restated engine."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _check(gpu, oracle, dims, kernel):
+    t, split = gpu.solve_mcm_with_split(gpu.McmInstance(dims), kernel)
+    wc, wf, ws = oracle.mcm_solve(dims)
+    assert np.array_equal(t.cells, wc), np.nonzero(t.cells != wc)[0][:5]
+    assert np.array_equal(split, ws), np.nonzero(split != ws)[0][:5]
+    assert np.array_equal(t.filled, wf)
+
+
+def test_spec_apex_kats(gpu):
+    # SPEC.md:328-330
+    for dims, apex, sp in [([10, 20, 30], 6000, 1), ([30, 35, 15, 5, 10, 20, 25], 15125, 3),
+                           ([2, 3, 4, 5], 64, 2)]:
+        t, split = gpu.solve_mcm_with_split(gpu.McmInstance(dims))
+        assert t.cells[-1] == apex and split[-1] == sp
+
+
+@pytest.mark.parametrize("kernel", [0, 1, 2, 3])
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 16, 33, 64, 100])
+def test_small(gpu, oracle, kernel, n):
+    _check(gpu, oracle, oracle.generate_mcm(n, n, 1, 100), kernel)
+
+
+@pytest.mark.parametrize("kernel", [0, 1, 3])
+@pytest.mark.parametrize("n", [129, 200, 257, 511])
+def test_medium(gpu, oracle, kernel, n):
+    _check(gpu, oracle, oracle.generate_mcm(n, 3, 1, 100), kernel)
+
+
+def test_ties_first_min(gpu, oracle):
+    # all-equal dims produce massive ties: split must be the FIRST minimal j
+    for n in (5, 40, 300):
+        _check(gpu, oracle, [7] * (n + 1), 0)
+        _check(gpu, oracle, [7] * (n + 1), 1)
+
+
+def test_int32_overflow_falls_back_to_int64(gpu, oracle):
+    # dims near 1290 drive values past 2^30: the 32-bit kernel must flag and
+    # the 64-bit kernel rerun (still on the GPU)
+    dims = oracle.generate_mcm(300, 9, 1000, 1290)
+    _check(gpu, oracle, dims, 1)
+    _check(gpu, oracle, dims[:60], 2)
+
+
+def test_wide_dims_int64(gpu, oracle):
+    dims = oracle.generate_mcm(150, 4, 1, 100000)
+    _check(gpu, oracle, dims, 1)
+    _check(gpu, oracle, dims[:80], 2)
+
+
+def test_config3_n1024(gpu, oracle):
+    dims = oracle.generate_mcm(1024, 1, 1, 100)
+    t, split = gpu.solve_mcm_with_split(gpu.McmInstance(dims))
+    assert gpu.digest_hex(gpu.table_digest(t.cells)) == "9e31907a82260f66"
+    assert gpu.digest_hex(gpu.table_digest(split)) == "42bfd8baf652c2f3"
+
+
+@pytest.mark.parametrize("mode", ["paper_literal", "stall_on_hazard"])
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 8, 17, 32, 64])
+def test_lockstep_pipeline(gpu, oracle, mode, n):
+    dims = oracle.generate_mcm(n, n + 100, 1, 50)
+    r = gpu.solve_mcm_pipeline(gpu.McmInstance(dims), mode)
+    wc, wf, steps, stall = oracle.mcm_pipeline(dims, 0 if mode == "paper_literal" else 1)
+    assert np.array_equal(r.table.cells, wc)
+    assert r.trace.steps_executed == steps and r.trace.stall_iterations == stall
+
+
+def test_batch(gpu, oracle):
+    insts = [gpu.McmInstance(oracle.generate_mcm(64, i, 1, 100)) for i in range(50)]
+    for inst, (t, split) in zip(insts, gpu.solve_mcm_batch(insts)):
+        wc, _, ws = oracle.mcm_solve(inst.dims)
+        assert np.array_equal(t.cells, wc) and np.array_equal(split, ws)

@@ -1,0 +1,121 @@
+"""S-DP parity on the GPU: every table bit-exact against the C restatement of
+the reference (oracle/pipedp_oracle.c, pinned to the reference by
+test_oracle.py), through the C ABI."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+OPS = ["min", "max", "saturating-add", "modular-add"]
+
+
+def _check(gpu, oracle, offs, init, n, op):
+    inst = gpu.SdpInstance(n, offs, init, op)
+    t = gpu.solve_sequential(inst)
+    want, wfilled = oracle.sdp_solve(offs, init, n, op)
+    bad = np.nonzero(t.cells != want)[0]
+    assert bad.size == 0, f"first mismatch at {bad[:5]}: got {t.cells[bad[:5]]} want {want[bad[:5]]}"
+    assert np.array_equal(t.filled, wfilled)
+
+
+def test_fibonacci_kat(gpu):
+    # k=2, a=(2,1), add, init [1,1], n=7
+    t = gpu.solve_sequential(gpu.SdpInstance(7, [2, 1], [1, 1], "saturating-add"))
+    assert t.cells.tolist() == [1, 1, 2, 3, 5, 8, 13]
+    assert t.all_filled()
+
+
+def test_min_zeros_kat(gpu):
+    # (5,3,1), min, zeros, n=10
+    t = gpu.solve_sequential(gpu.SdpInstance(10, [5, 3, 1], [0] * 5, "min"))
+    assert t.cells.tolist() == [0] * 10
+
+
+@pytest.mark.parametrize("op", OPS)
+@pytest.mark.parametrize("seed", range(12))
+def test_random_small(gpu, oracle, op, seed):
+    rng = np.random.default_rng(seed * 7 + OPS.index(op))
+    k = int(rng.integers(1, 40))
+    cap = int(rng.integers(k, 200))
+    offs = np.sort(rng.choice(np.arange(1, cap + 1), k, replace=False))[::-1].copy()
+    n = int(offs[0] + rng.integers(1, 3000))
+    if seed % 3 == 0:
+        init = rng.integers(-(2**62), 2**62, offs[0])
+    elif seed % 3 == 1:
+        init = rng.integers(-1000, 1000, offs[0])
+    else:
+        init = rng.integers(0, 2**20, offs[0])
+    _check(gpu, oracle, offs, init, n, op)
+
+
+@pytest.mark.parametrize("op", OPS)
+@pytest.mark.parametrize("shape", [(4096, 64, 0), (20000, 1024, 4096), (9000, 300, 700),
+                                   (5000, 32, 0), (3000, 7, 0), (70000, 2000, 20000)])
+def test_generated(gpu, oracle, op, shape):
+    n, k, cap = shape
+    offs, init = oracle.generate_sdp(n, k, 11, False, cap)
+    _check(gpu, oracle, offs, init, n, op)
+
+
+@pytest.mark.parametrize("op", OPS)
+def test_consecutive_offsets(gpu, oracle, op):
+    offs, init = oracle.generate_sdp(6000, 200, 3, True, 0)
+    _check(gpu, oracle, offs, init, 6000, op)
+
+
+def test_sat_add_mixed_signs_strict_order(gpu, oracle):
+    # saturating-add is not associative with mixed signs: the kernels must keep
+    # the reference's j-ascending fold (sdp.cpp:53-56)
+    rng = np.random.default_rng(5)
+    offs = np.array(sorted(rng.choice(np.arange(1, 600), 120, replace=False))[::-1])
+    init = rng.choice([2**62, -(2**62), 2**61, -(2**61), 3, -3], offs[0])
+    _check(gpu, oracle, offs, init, 8000, "saturating-add")
+
+
+def test_modadd_raw_copy_k1(gpu, oracle):
+    # k=1 copies raw (unnormalised) values (SURVEY hard part 5)
+    _check(gpu, oracle, [3], [-5, 3000000000, 7], 50, "modular-add")
+
+
+def test_large_a1_hbm_far_stage(gpu, oracle):
+    # a_1 too large for a shared-memory ring -> far stage reads HBM
+    offs, init = oracle.generate_sdp(120000, 700, 2, False, 60000)
+    _check(gpu, oracle, offs, init, 120000, "min")
+    _check(gpu, oracle, offs, init, 120000, "saturating-add")
+
+
+def test_fibonacci_config1(gpu, oracle):
+    # BASELINE config 1 (and its modular-add companion)
+    n = 1 << 20
+    for op in ("saturating-add", "modular-add"):
+        _check(gpu, oracle, [2, 1], [1, 1], n, op)
+
+
+@pytest.mark.parametrize("op", OPS)
+def test_batch_matches_single(gpu, oracle, op):
+    insts = []
+    for i in range(37):
+        offs, init = oracle.generate_sdp(3000, 64, i, False, 0)
+        insts.append(gpu.SdpInstance(3000, offs, init, op))
+    tabs = gpu.solve_sequential_batch(insts)
+    for inst, t in zip(insts, tabs):
+        want, _ = oracle.sdp_solve(inst.offsets, inst.init, inst.n, op)
+        assert np.array_equal(t.cells, want)
+
+
+def test_batch_large_a1_uses_cta_kernel(gpu, oracle):
+    insts = []
+    for i in range(5):
+        offs, init = oracle.generate_sdp(30000, 256, 100 + i, False, 4096)
+        insts.append(gpu.SdpInstance(30000, offs, init, "min"))
+    for inst, t in zip(insts, gpu.solve_sequential_batch(insts)):
+        want, _ = oracle.sdp_solve(inst.offsets, inst.init, inst.n, "min")
+        assert np.array_equal(t.cells, want)
+
+
+def test_pipeline_trace_fields(gpu):
+    inst = gpu.generate_sdp(n=4096, k=64, seed=1)
+    r = gpu.solve_sdp_pipeline(inst)
+    assert r.trace.first_head == inst.a1
+    assert r.trace.steps_executed == inst.n + inst.k - inst.a1 - 1
+    assert r.trace.stall_iterations == 0
