@@ -188,9 +188,11 @@ struct SdpDispatch {
   bool assoc; // regrouping legal
   bool small; // CTA: a1 < 64, warp: a1 < 32
   bool gfar;
+  bool remote;  // multi-CTA: producer CTAs on other SMs
   bool warp_kernel;
   SdpShape shape;
   int threads;
+  int grid_extra;  // producer CTAs (remote)
   size_t smem;
   int wpb;  // warp kernel: warps per block
 };
@@ -211,12 +213,32 @@ void sdp_value_class(int op, const int64_t* init, int64_t count, int* bits, bool
 
 constexpr size_t kSmemBudget = 200 * 1024;
 constexpr int kAMid = 256;
+constexpr int kARemote = 1024;
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
+int sm_count() {
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 148;
+  }
+  return sms;
+}
+
+size_t sdp_cta_smem(int64_t R, int64_t kpad, size_t vb) {
+  return 2 * R * vb + 3 * kpad * 4 + (size_t)(kMidSlots + kFarSlots) * 32 * vb +
+         (size_t)(2 * kBatchBars + kMidSlots + kFarSlots) * 8 + 64;
+}
 
 int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* offsets,
              const int64_t* init, int op, SdpDispatch* d) {
   if (op < 0 || op > 3) return fail(PIPEDP_E_INVALID_PARAMS, "unknown operator kind");
-  if (a1 >= INT32_MAX - 4096 || k >= INT32_MAX / 8)
-    return fail(PIPEDP_ERR_UNSUPPORTED, "a_1=%lld exceeds the 32-bit offset range of the kernels",
+  if (a1 >= (1ll << 27) || k >= (1ll << 24))
+    return fail(PIPEDP_ERR_UNSUPPORTED, "a_1=%lld exceeds the 32-bit byte-offset range of the kernels",
                 (long long)a1);
   d->op = op;
   sdp_value_class(op, init, batch * a1, &d->bits, &d->assoc);
@@ -226,16 +248,21 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
   s.k = (int32_t)k;
   s.a1 = (int32_t)a1;
   s.a_mid = kAMid;
+  s.a_remote = 1 << 30;
+  s.remote_warps = 0;
+  d->grid_extra = 0;
+  d->remote = false;
   const int64_t kpad = (k + 3) & ~3ll;
   // warp-per-instance kernel for batches of small-a_1 instances
   if (batch > 1) {
     const int64_t R = 1ll << ceil_log2((uint64_t)(a1 + 32));
-    const size_t per_warp = 2 * R * vb + kpad * 4;
+    const size_t per_warp = 2 * R * vb + 2 * kpad * 4;
     if (per_warp <= 16 * 1024) {
       d->warp_kernel = true;
       d->small = a1 < 32;
       d->gfar = false;
       s.ring_log2 = ceil_log2((uint64_t)R);
+      s.ring_cover = (int32_t)a1;
       s.mid_warps = s.far_warps = 0;
       d->wpb = (int)std::max<int64_t>(1, std::min<int64_t>(8, (96 * 1024) / per_warp));
       d->threads = 32 * d->wpb;
@@ -245,35 +272,60 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
   }
   d->warp_kernel = false;
   d->small = a1 < 64;
-  // largest far-offset count over the batch sizes the far stage
-  int64_t jf_max = 0;
-  for (int64_t b = 0; b < batch; ++b) {
-    int64_t jf = 0;
-    for (int64_t j = 0; j < k; ++j) jf += offsets[b * k + j] >= kAMid;
-    jf_max = std::max(jf_max, jf);
-  }
-  const size_t slots = (size_t)(kMidSlots + kFarSlots) * 32 * vb + (1 + kMidSlots + kFarSlots) * 4 + 64;
-  const int64_t r_full = 1ll << ceil_log2((uint64_t)(a1 + 128));
-  const size_t smem_full = 2 * r_full * vb + kpad * 4 + slots;
-  if (d->small || smem_full <= kSmemBudget) {
-    d->gfar = false;
-    s.ring_log2 = ceil_log2((uint64_t)r_full);
-    d->smem = smem_full;
-  } else {
-    if (kpad * 4 + 2 * 512 * vb + slots > 227 * 1024)
-      return fail(PIPEDP_ERR_UNSUPPORTED, "k=%lld offsets exceed shared memory", (long long)k);
-    d->gfar = true;
-    s.ring_log2 = ceil_log2((uint64_t)(kAMid + 128));
-    d->smem = 2 * (1ull << s.ring_log2) * vb + kpad * 4 + slots;
-  }
   if (d->small) {
+    s.ring_log2 = ceil_log2((uint64_t)(a1 + 128));
+    s.ring_cover = (int32_t)a1;
     s.mid_warps = s.far_warps = 0;
+    d->gfar = false;
     d->threads = 32;
-  } else {
-    s.mid_warps = 4;
-    s.far_warps = (int32_t)std::min<int64_t>(27, std::max<int64_t>(1, (jf_max + 47) / 48));
-    d->threads = 32 * (1 + s.mid_warps + s.far_warps);
+    d->smem = sdp_cta_smem(1ll << s.ring_log2, kpad, vb);
+    return PIPEDP_OK;
   }
+  // offset counts per stage (max over the batch sizes the stages)
+  int64_t jf_max = 0, jr_max = 0;
+  for (int64_t b = 0; b < batch; ++b) {
+    int64_t jf = 0, jr = 0;
+    for (int64_t j = 0; j < k; ++j) {
+      jf += offsets[b * k + j] >= kAMid;
+      jr += offsets[b * k + j] >= kARemote;
+    }
+    jf_max = std::max(jf_max, jf);
+    jr_max = std::max(jr_max, jr);
+  }
+  // multi-CTA: one large associative instance with enough remote work
+  const int64_t nb = (n - a1 + 31) / 32;
+  d->remote = batch == 1 && d->assoc && jr_max >= 128 && nb >= 256 &&
+              env_int("PIPEDP_SDP_MULTI", 1) != 0;
+  s.mid_warps = 4;
+  if (d->remote) {
+    s.a_remote = kARemote;
+    s.ring_cover = kARemote;
+    s.ring_log2 = ceil_log2((uint64_t)(kARemote + 512));
+    d->gfar = false;
+    s.far_warps = (int32_t)std::min<int64_t>(16, std::max<int64_t>(1, (jf_max - jr_max + 47) / 48));
+    s.remote_warps = env_int("PIPEDP_SDP_REMOTE_WARPS", 8);
+    d->grid_extra = std::min(sm_count() - 1, env_int("PIPEDP_SDP_REMOTE_CTAS", 32));
+    d->smem = sdp_cta_smem(1ll << s.ring_log2, kpad, vb);
+  } else {
+    const int64_t r_full = 1ll << ceil_log2((uint64_t)(a1 + 512));
+    const size_t smem_full = sdp_cta_smem(r_full, kpad, vb);
+    if (smem_full <= kSmemBudget) {
+      d->gfar = false;
+      s.ring_log2 = ceil_log2((uint64_t)r_full);
+      s.ring_cover = (int32_t)a1;
+      d->smem = smem_full;
+    } else {
+      d->gfar = true;
+      s.ring_log2 = ceil_log2((uint64_t)(kAMid + 512));
+      s.ring_cover = kAMid;
+      d->smem = sdp_cta_smem(1ll << s.ring_log2, kpad, vb);
+      if (d->smem > 227 * 1024)
+        return fail(PIPEDP_ERR_UNSUPPORTED, "k=%lld offsets exceed shared memory", (long long)k);
+    }
+    s.far_warps = (int32_t)std::min<int64_t>(24, std::max<int64_t>(1, (jf_max + 47) / 48));
+  }
+  d->threads = 32 * (1 + s.mid_warps + s.far_warps + 1);
+  d->threads = std::max(d->threads, 32 * s.remote_warps);
   return PIPEDP_OK;
 }
 
@@ -284,6 +336,17 @@ int launch_cta(const SdpDispatch& d, int64_t batch, const int64_t* offs, const i
   CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem));
   kern<<<(unsigned)batch, d.threads, d.smem, st>>>(d.shape, offs, init, out);
   CK(cudaGetLastError());
+  return PIPEDP_OK;
+}
+
+template <int OP, typename T>
+int launch_multi(const SdpDispatch& d, const int64_t* offs, const int64_t* init, int64_t* out,
+                 const SdpRemote& rm, cudaStream_t st) {
+  auto kern = sdp_pipeline_multi<OP, T, false>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem));
+  SdpShape shape = d.shape;
+  void* args[] = {(void*)&shape, (void*)&offs, (void*)&init, (void*)&out, (void*)&rm};
+  CK(cudaLaunchCooperativeKernel((void*)kern, dim3(1 + d.grid_extra), dim3(d.threads), args, d.smem, st));
   return PIPEDP_OK;
 }
 
@@ -300,47 +363,52 @@ int launch_warp(const SdpDispatch& d, int64_t batch, const int64_t* offs, const 
 
 template <int OP, typename T, bool ASSOC>
 int launch_sdp_t(const SdpDispatch& d, int64_t batch, const int64_t* offs, const int64_t* init,
-                 int64_t* out, cudaStream_t st) {
+                 int64_t* out, const SdpRemote& rm, cudaStream_t st) {
   if (d.warp_kernel) {
     return d.small ? launch_warp<OP, T, true, ASSOC>(d, batch, offs, init, out, st)
                    : launch_warp<OP, T, false, ASSOC>(d, batch, offs, init, out, st);
   }
   if (d.small) return launch_cta<OP, T, true, ASSOC, false>(d, batch, offs, init, out, st);
+  if (ASSOC && d.remote) return launch_multi<OP, T>(d, offs, init, out, rm, st);
   return d.gfar ? launch_cta<OP, T, false, ASSOC, true>(d, batch, offs, init, out, st)
                 : launch_cta<OP, T, false, ASSOC, false>(d, batch, offs, init, out, st);
 }
 
 int launch_sdp(const SdpDispatch& d, int64_t batch, const int64_t* offs, const int64_t* init,
-               int64_t* out, cudaStream_t st) {
+               int64_t* out, const SdpRemote& rm, cudaStream_t st) {
   switch (d.op) {
     case PIPEDP_OP_MIN:
-      return d.bits == 32 ? launch_sdp_t<kMin, int32_t, true>(d, batch, offs, init, out, st)
-                          : launch_sdp_t<kMin, int64_t, true>(d, batch, offs, init, out, st);
+      return d.bits == 32 ? launch_sdp_t<kMin, int32_t, true>(d, batch, offs, init, out, rm, st)
+                          : launch_sdp_t<kMin, int64_t, true>(d, batch, offs, init, out, rm, st);
     case PIPEDP_OP_MAX:
-      return d.bits == 32 ? launch_sdp_t<kMax, int32_t, true>(d, batch, offs, init, out, st)
-                          : launch_sdp_t<kMax, int64_t, true>(d, batch, offs, init, out, st);
+      return d.bits == 32 ? launch_sdp_t<kMax, int32_t, true>(d, batch, offs, init, out, rm, st)
+                          : launch_sdp_t<kMax, int64_t, true>(d, batch, offs, init, out, rm, st);
     case PIPEDP_OP_MODULAR_ADD:
-      return d.bits == 32 ? launch_sdp_t<kModAdd, int32_t, true>(d, batch, offs, init, out, st)
-                          : launch_sdp_t<kModAdd, int64_t, true>(d, batch, offs, init, out, st);
+      return d.bits == 32 ? launch_sdp_t<kModAdd, int32_t, true>(d, batch, offs, init, out, rm, st)
+                          : launch_sdp_t<kModAdd, int64_t, true>(d, batch, offs, init, out, rm, st);
     default:
-      return d.assoc ? launch_sdp_t<kSatAdd, int64_t, true>(d, batch, offs, init, out, st)
-                     : launch_sdp_t<kSatAdd, int64_t, false>(d, batch, offs, init, out, st);
+      return d.assoc ? launch_sdp_t<kSatAdd, int64_t, true>(d, batch, offs, init, out, rm, st)
+                     : launch_sdp_t<kSatAdd, int64_t, false>(d, batch, offs, init, out, rm, st);
   }
 }
 
 const char* sdp_kernel_name(const SdpDispatch& d) {
   if (d.warp_kernel) return "sdp_batch_warp";
   if (d.small) return "sdp_pipeline_cta[chain]";
+  if (d.remote) return "sdp_pipeline_multi";
   return d.gfar ? "sdp_pipeline_cta[far-hbm]" : "sdp_pipeline_cta[ring]";
 }
 
 }  // namespace
+
+constexpr size_t kRemoteBytes = kRemSlots * 32 * sizeof(int64_t) + kRemSlots * sizeof(int) + 64;
 
 struct pipedp_sdp_plan {
   int device;
   int64_t batch, n, k, a1;
   SdpDispatch d;
   int64_t* d_offsets;  // device copy of the offsets, int64 [batch*k]
+  void* d_remote;      // multi-CTA workspace: partial slots | ready flags | published
 };
 
 // ================================================================== MCM ===
@@ -581,8 +649,10 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
   cudaError_t e = cudaMalloc(&P->d_offsets, sizeof(int64_t) * batch * k);
   if (e == cudaSuccess)
     e = cudaMemcpy(P->d_offsets, h_offsets, sizeof(int64_t) * batch * k, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess && d.remote) e = cudaMalloc(&P->d_remote, kRemoteBytes);
   if (e != cudaSuccess) {
     cudaFree(P->d_offsets);
+    cudaFree(P->d_remote);
     delete P;
     return cuda_fail(e, "sdp plan upload");
   }
@@ -594,7 +664,19 @@ int32_t pipedp_sdp_plan_execute(pipedp_sdp_plan_t P, const int64_t* d_init, int6
                                 void* stream) {
   if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
   CK(cudaSetDevice(P->device));
-  return launch_sdp(P->d, P->batch, P->d_offsets, d_init, d_cells, (cudaStream_t)stream);
+  SdpRemote rm{};
+  if (P->d.remote) {
+    char* w = static_cast<char*>(P->d_remote);
+    rm.part = w;
+    rm.ready = reinterpret_cast<int*>(w + kRemSlots * 32 * sizeof(int64_t));
+    rm.published = reinterpret_cast<unsigned long long*>(w + kRemSlots * 32 * sizeof(int64_t) + kRemSlots * sizeof(int));
+    CK(cudaMemsetAsync(P->d_remote, 0, kRemoteBytes, (cudaStream_t)stream));
+    // producers read the preset prefix straight from the table before the
+    // finisher CTA has necessarily run: stage it there in stream order
+    CK(cudaMemcpyAsync(d_cells, d_init, sizeof(int64_t) * P->a1, cudaMemcpyDeviceToDevice,
+                       (cudaStream_t)stream));
+  }
+  return launch_sdp(P->d, P->batch, P->d_offsets, d_init, d_cells, rm, (cudaStream_t)stream);
 }
 
 int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, int32_t* bits,
@@ -602,7 +684,7 @@ int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, in
   if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
   if (name && cap) snprintf(name, cap, "%s", sdp_kernel_name(P->d));
   if (bits) *bits = P->d.bits;
-  if (launches) *launches = 1;
+  if (launches) *launches = 1;  // kernels (remote mode adds a memset + a prefix copy)
   return PIPEDP_OK;
 }
 
@@ -610,6 +692,7 @@ int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t P) {
   if (!P) return PIPEDP_OK;
   cudaSetDevice(P->device);
   cudaFree(P->d_offsets);
+  cudaFree(P->d_remote);
   delete P;
   return PIPEDP_OK;
 }

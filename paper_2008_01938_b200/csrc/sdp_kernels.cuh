@@ -3,32 +3,36 @@
 // Reference semantics (sdp.cpp:48-60 fill_table, sdp_pipeline.hpp:24-46): for
 // every cell i >= a_1, acc = ST[i - a_1] and then acc = acc (x) ST[i - a_j] for
 // j = 2..k IN THAT ORDER.  Saturating-add is not associative for mixed signs,
-// so the kernels keep the j-ascending left fold per cell (a_j descending) --
-// exactly the order in which the paper's k-stage pipeline hands the partial
+// so every kernel keeps the j-ascending left fold per cell (a_j descending) --
+// the order in which the paper's k-stage pipeline hands the partial
 // accumulator from lane j to lane j+1.  Regrouping (never reordering) is used
 // only when the host has proven the operator associative on the instance
 // (min, max, modular-add always; saturating-add when no two init values have
-// opposite signs) -- template flag ASSOC.
+// opposite signs): template flag ASSOC.
 //
 // B200 mapping:
 //  * cells are processed in batches of 32, one cell per lane, so a warp's ring
 //    read for one offset touches 32 consecutive words (conflict-free);
-//  * the offsets are split into three pipeline STAGES by size; each stage is a
-//    set of warps that hands the 32 partial accumulators of a batch to the
-//    next stage through shared-memory slots published with st.release.cta:
-//      far   (a_j >= a_mid): lookahead >= a_mid/32 batches, most of the work;
-//      mid   (64 <= a_j < a_mid): lookahead 2 batches;
-//      chain (a_j < 64): one warp.  Offsets in [32, 64) and the out-of-batch
-//            part of offsets < 32 come from the ring; the in-batch part is a
-//            31-step warp-shuffle broadcast (step t: lane t-1 is final and
-//            every lane l with l-t+1 in the offset set folds it).  This
-//            hand-off is the kernel's dependency-chain step;
+//  * the offsets are split into pipeline STAGES by size.  A stage is a set of
+//    warps; it hands the 32 partial accumulators of a batch to the next stage
+//    through a shared-memory slot guarded by an mbarrier (hardware-suspended
+//    waits, so idle stages burn no issue slots):
+//      remote (a >= a_remote): producer CTAs on other SMs (multi-CTA mode),
+//              operands read from the HBM table (L2), partials through global
+//              slots with gpu-scope release/acquire flags;
+//      far    (a_mid <= a < a_remote): lookahead >= a_mid/32 batches;
+//      mid    (64 <= a < a_mid): lookahead 2 batches;
+//      chain  (a < 64): one warp.  Offsets in [32, 64) and the out-of-batch
+//              part of offsets < 32 come from the ring; the in-batch part is a
+//              31-step warp-shuffle broadcast (step t: lane t-1 is final and
+//              every lane l with l-t+1 in the offset set folds it).  This
+//              hand-off is the kernel's dependency-chain step;
 //  * finalised values live in a MIRRORED shared-memory ring (value stored at p
-//    and p + R) so the operand of offset a is simply base_lane - a;
-//  * finished batches stream to HBM as coalesced int64 stores issued by the
-//    mid warps two batches behind the chain (GFAR=false), or by the chain warp
-//    itself when a_1 is too large for a shared-memory ring (GFAR=true: the far
-//    stage then reads its operands from the HBM table, L1/L2-resident).
+//    and p + R) so the operand of offset a is base_lane - a (offsets are kept
+//    pre-scaled to bytes: one IADD per term);
+//  * a writer warp streams finished batches to HBM (coalesced int64 stores)
+//    and, in multi-CTA mode, publishes the finished prefix to the producers
+//    with a gpu-scope release every few batches.
 #pragma once
 
 #include "common.cuh"
@@ -37,6 +41,9 @@ namespace pipedp_dev {
 
 constexpr int kMidSlots = 32;  // mid -> chain partial slots
 constexpr int kFarSlots = 64;  // far -> mid partial slots
+constexpr int kBatchBars = 64; // batch_done / written mbarrier rings
+constexpr int kRemSlots = 64;  // remote -> far partial slots (global)
+constexpr int kPubEvery = 4;   // writer publishes to the producers every 4 batches
 
 // Uniform launch shape (all instances of a launch share n, k, a_1).
 struct SdpShape {
@@ -44,58 +51,88 @@ struct SdpShape {
   int32_t k;
   int32_t a1;
   int32_t ring_log2;  // R = 1 << ring_log2 (ring holds 2R values)
-  int32_t a_mid;      // offsets >= a_mid belong to the far stage
+  int32_t a_mid;      // offsets >= a_mid: far stage (or remote)
+  int32_t a_remote;   // offsets >= a_remote: remote producers (multi-CTA mode only)
+  int32_t ring_cover; // largest offset read from the ring (a_1, a_mid or a_remote)
   int32_t mid_warps;
   int32_t far_warps;
+  int32_t remote_warps;  // warps per producer CTA
+};
+
+// Global workspace of the multi-CTA mode (zeroed before every launch).
+struct SdpRemote {
+  void* part;               // [kRemSlots][32] T
+  int* ready;               // [kRemSlots] batch+1
+  unsigned long long* published;  // batches written to the table and released
 };
 
 template <typename T, typename S>
 __device__ __forceinline__ T ldv(const S* p) {
   return (T)(*p);
 }
+template <typename T, typename S>
+__device__ __forceinline__ T ldv_cg(const S* p);
+template <>
+__device__ __forceinline__ int32_t ldv_cg<int32_t, int64_t>(const int64_t* p) {
+  return (int32_t)__ldcg(reinterpret_cast<const long long*>(p));
+}
+template <>
+__device__ __forceinline__ int64_t ldv_cg<int64_t, int64_t>(const int64_t* p) {
+  return (int64_t)__ldcg(reinterpret_cast<const long long*>(p));
+}
 
-// Fold offsets[j0, j1) into acc; operands at base[-a].  HAVE=false assigns the
-// first operand (sdp.cpp:53).  ASSOC splits the range into four contiguous
-// quarters folded independently and combined in order (regrouping only).
-template <int OP, typename T, bool ASSOC, typename S>
-__device__ __forceinline__ T fold_range(T acc, bool have, const S* __restrict__ base,
-                                        const int32_t* __restrict__ offs, int j0, int j1) {
+// Element at (char*)base - off_bytes.
+template <typename T, typename S, bool CG>
+__device__ __forceinline__ T at(const char* base, int32_t ob) {
+  const S* p = reinterpret_cast<const S*>(base - ob);
+  if constexpr (CG) return ldv_cg<T, S>(p);
+  else return ldv<T>(p);
+}
+
+// Fold the operands at byte offsets ob[j0, j1) below `base` into acc.
+// HAVE=false assigns the first operand (sdp.cpp:53).  ASSOC folds four
+// contiguous quarters independently and combines them in order (regrouping).
+template <int OP, typename T, bool ASSOC, typename S, bool CG = false>
+__device__ __forceinline__ T fold_range(T acc, bool have, const S* base_elem,
+                                        const int32_t* __restrict__ ob, int j0, int j1) {
   using O = SemiOp<OP, T>;
+  const char* base = reinterpret_cast<const char*>(base_elem);
   if (j0 >= j1) return acc;
   if (!have) {
-    acc = ldv<T>(base - offs[j0]);
+    acc = at<T, S, CG>(base, ob[j0]);
     ++j0;
   }
   if (ASSOC && j1 - j0 >= 16) {
     const int q = (j1 - j0) >> 2;
     const int s1 = j0 + q, s2 = j0 + 2 * q, s3 = j0 + 3 * q;
     T p0 = acc;
-    T p1 = ldv<T>(base - offs[s1]);
-    T p2 = ldv<T>(base - offs[s2]);
-    T p3 = ldv<T>(base - offs[s3]);
+    T p1 = at<T, S, CG>(base, ob[s1]);
+    T p2 = at<T, S, CG>(base, ob[s2]);
+    T p3 = at<T, S, CG>(base, ob[s3]);
+#pragma unroll 4
     for (int i = 1; i < q; ++i) {
-      const T v0 = ldv<T>(base - offs[j0 + i - 1]);
-      const T v1 = ldv<T>(base - offs[s1 + i]);
-      const T v2 = ldv<T>(base - offs[s2 + i]);
-      const T v3 = ldv<T>(base - offs[s3 + i]);
+      const T v0 = at<T, S, CG>(base, ob[j0 + i - 1]);
+      const T v1 = at<T, S, CG>(base, ob[s1 + i]);
+      const T v2 = at<T, S, CG>(base, ob[s2 + i]);
+      const T v3 = at<T, S, CG>(base, ob[s3 + i]);
       p0 = O::apply(p0, v0);
       p1 = O::apply(p1, v1);
       p2 = O::apply(p2, v2);
       p3 = O::apply(p3, v3);
     }
-    p0 = O::apply(p0, ldv<T>(base - offs[s1 - 1]));
-    for (int j = s3 + q; j < j1; ++j) p3 = O::apply(p3, ldv<T>(base - offs[j]));
+    p0 = O::apply(p0, at<T, S, CG>(base, ob[s1 - 1]));
+    for (int j = s3 + q; j < j1; ++j) p3 = O::apply(p3, at<T, S, CG>(base, ob[j]));
     return O::apply(O::apply(O::apply(p0, p1), p2), p3);
   }
   int j = j0;
   for (; j + 4 <= j1; j += 4) {
-    const T v0 = ldv<T>(base - offs[j]);
-    const T v1 = ldv<T>(base - offs[j + 1]);
-    const T v2 = ldv<T>(base - offs[j + 2]);
-    const T v3 = ldv<T>(base - offs[j + 3]);
+    const T v0 = at<T, S, CG>(base, ob[j]);
+    const T v1 = at<T, S, CG>(base, ob[j + 1]);
+    const T v2 = at<T, S, CG>(base, ob[j + 2]);
+    const T v3 = at<T, S, CG>(base, ob[j + 3]);
     acc = O::apply(O::apply(O::apply(O::apply(acc, v0), v1), v2), v3);
   }
-  for (; j < j1; ++j) acc = O::apply(acc, ldv<T>(base - offs[j]));
+  for (; j < j1; ++j) acc = O::apply(acc, at<T, S, CG>(base, ob[j]));
   return acc;
 }
 
@@ -104,11 +141,15 @@ __device__ __forceinline__ T fold_range(T acc, bool have, const S* __restrict__ 
 // descending order.  HAVE_ACC=false: no larger offset exists, the first
 // operand is ASSIGNED, possibly inside the shuffle chain.  ring_pos = position
 // of this lane's cell in the upper ring half; operand of offset a at
-// ring[ring_pos - a].
+// ring[ring_pos - a].  `bits` = chain_bits(mask32, lane), hoisted by the caller.
+__device__ __forceinline__ uint32_t chain_bits(uint32_t mask32, int lane) {
+  return (mask32 & ((2u << lane) - 1u) & ~1u) << (31 - lane);
+}
+
 template <int OP, typename T, bool HAVE_ACC>
 __device__ __forceinline__ T chain_fold(T acc, const T* __restrict__ ring, uint32_t ring_pos,
                                         const int32_t* __restrict__ offs, int jb, int j32, int k,
-                                        uint32_t mask32, int lane) {
+                                        uint32_t bits, int lane) {
   using O = SemiOp<OP, T>;
   bool have = HAVE_ACC;
   for (int j = jb; j < j32; ++j) {  // offsets in [32, 64): out of batch for all lanes
@@ -125,11 +166,10 @@ __device__ __forceinline__ T chain_fold(T acc, const T* __restrict__ ring, uint3
     }
   }
   // in-batch chain: step t folds offset a = lane - t + 1 with lane t-1's value
-  const uint32_t bits = (mask32 & ((2u << lane) - 1u) & ~1u) << (31 - lane);
 #pragma unroll
   for (int t = 1; t < 32; ++t) {
     const T v = shfl_idx(acc, t - 1);
-    const bool take = (bits >> (32 - t)) & 1u;
+    const bool take = (int32_t)(bits << (t - 1)) < 0;
     if (HAVE_ACC) {
       if (take) acc = O::apply(acc, v);
     } else {
@@ -140,56 +180,63 @@ __device__ __forceinline__ T chain_fold(T acc, const T* __restrict__ ring, uint3
   return acc;
 }
 
-__device__ __forceinline__ void spin_until_ge(const int* flag, int target) {
-  while (ld_acquire_cta(flag) < target) __nanosleep(16);
-}
-
-// Offset classes of one instance, from its offsets in shared memory.
+// Offset classes of one instance, from its raw offsets in shared memory.
 struct SdpClasses {
-  int jf, jn, j32, far_look;
+  int jr, jf, jn, j32;
+  int far_look, rem_look;
   uint32_t mask32;
 };
 
-__device__ __forceinline__ SdpClasses sdp_classes(const int32_t* offs, int k, int a_mid) {
-  SdpClasses c{0, 0, 0, 0, 0u};
+__device__ __forceinline__ SdpClasses sdp_classes(const int32_t* offs, int k, int a_mid,
+                                                  int a_remote) {
+  SdpClasses c{0, 0, 0, 0, 0, 0, 0u};
   for (int j = 0; j < k; ++j) {
     const int a = offs[j];
+    c.jr += a >= a_remote;
     c.jf += a >= a_mid;
     c.jn += a >= 64;
     c.j32 += a >= 32;
     if (a < 32) c.mask32 |= 1u << a;
   }
-  c.far_look = c.jf > 0 ? offs[c.jf - 1] / 32 : 0;
+  c.far_look = c.jf > c.jr ? offs[c.jf - 1] / 32 : 1 << 30;
+  c.rem_look = c.jr > 0 ? offs[c.jr - 1] / 32 : 1 << 30;
   return c;
 }
 
+__device__ __forceinline__ void wait_batches(uint64_t* bars, int64_t count) {
+  // wait until batches [0, count) passed the barrier ring
+  if (count <= 0) return;
+  const int64_t b = count - 1;
+  mbar_wait(&bars[b % kBatchBars], (unsigned)((b / kBatchBars) & 1));
+}
+
 // -----------------------------------------------------------------------------
-// One CTA per instance (blockIdx.x = instance; batch 1 = the single-instance
-// solver):
-//   warp 0                          chain stage
-//   warps 1 .. mid_warps            mid stage   (batch b -> warp 1 + b % mid_warps)
-//   warps mid_warps+1 .. +far_warps far stage   (batch b -> b % far_warps)
-// SMALL (a_1 < 64): chain warp only.
-template <int OP, typename T, bool SMALL, bool ASSOC, bool GFAR>
-__global__ void __launch_bounds__(1024, 1)
-    sdp_pipeline_cta(const SdpShape S, const int64_t* __restrict__ g_offsets,
-                     const int64_t* __restrict__ g_init, int64_t* __restrict__ g_out) {
+// Finisher: one CTA per instance (blockIdx.x = instance), or block 0 of a
+// multi-CTA launch (REMOTE) whose other blocks run sdp_remote_producer.
+//   warp 0                 chain
+//   warps 1 .. M           mid            (batch b -> 1 + b % M)
+//   warps M+1 .. M+F       far            (batch b -> b % F)
+//   warp  M+F+1            writer
+// SMALL (a_1 < 64): chain warp only, it writes the table itself.
+// GFAR: a_1 too large for the ring -- the far stage reads the HBM table.
+template <int OP, typename T, bool SMALL, bool ASSOC, bool GFAR, bool REMOTE>
+__device__ __forceinline__ void sdp_finisher(const SdpShape& S, const int64_t* __restrict__ offsets,
+                                             const int64_t* __restrict__ init, int64_t* out,
+                                             const SdpRemote& RM) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t R = 1u << S.ring_log2;
   const int kpad = (S.k + 3) & ~3;
   T* ring = reinterpret_cast<T*>(smem);
-  int32_t* offs = reinterpret_cast<int32_t*>(ring + 2 * R);
-  T* mid_part = reinterpret_cast<T*>(offs + kpad);
+  int32_t* offs = reinterpret_cast<int32_t*>(ring + 2 * R);  // raw a_j
+  int32_t* ob = offs + kpad;                                 // a_j * sizeof(T) (ring reads)
+  int32_t* obg = ob + kpad;                                  // a_j * 8 (HBM table reads)
+  T* mid_part = reinterpret_cast<T*>(obg + kpad);
   T* far_part = mid_part + kMidSlots * 32;
-  int* flags = reinterpret_cast<int*>(far_part + kFarSlots * 32);
-  int* final_count = flags;                // batches finalised by the chain warp
-  int* mid_ready = flags + 1;              // [kMidSlots] = batch+1 held by the slot
-  int* far_ready = mid_ready + kMidSlots;  // [kFarSlots]
-
-  const int64_t inst = blockIdx.x;
-  const int64_t* offsets = g_offsets + inst * S.k;
-  const int64_t* init = g_init + inst * S.a1;
-  int64_t* out = g_out + inst * S.n;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(far_part + kFarSlots * 32);
+  uint64_t* batch_done = bars;                  // [kBatchBars] chain -> all
+  uint64_t* written = batch_done + kBatchBars;  // [kBatchBars] writer -> far
+  uint64_t* mid_full = written + kBatchBars;    // [kMidSlots]
+  uint64_t* far_full = mid_full + kMidSlots;    // [kFarSlots]
 
   const int tid = threadIdx.x;
   const int lane = tid & 31;
@@ -197,7 +244,12 @@ __global__ void __launch_bounds__(1024, 1)
   const int64_t a1 = S.a1;
   const int64_t n = S.n;
 
-  for (int j = tid; j < S.k; j += blockDim.x) offs[j] = (int32_t)offsets[j];
+  for (int j = tid; j < S.k; j += blockDim.x) {
+    const int32_t a = (int32_t)offsets[j];
+    offs[j] = a;
+    ob[j] = a * (int32_t)sizeof(T);
+    obg[j] = a * 8;
+  }
   const int64_t ring_from = a1 > (int64_t)R ? a1 - (int64_t)R : 0;  // the last R preset cells
   for (int64_t i = tid; i < a1; i += blockDim.x) {
     const int64_t v = init[i];
@@ -208,87 +260,184 @@ __global__ void __launch_bounds__(1024, 1)
     }
     out[i] = v;
   }
-  if (tid == 0) *final_count = 0;
-  for (int s = tid; s < kMidSlots + kFarSlots; s += blockDim.x) mid_ready[s] = 0;
+  if (tid == 0) {
+    for (int s = 0; s < 2 * kBatchBars + kMidSlots + kFarSlots; ++s) mbar_init(&bars[s], 1);
+  }
   __syncthreads();
-  const SdpClasses C = sdp_classes(offs, S.k, S.a_mid);
+  const SdpClasses C = sdp_classes(offs, S.k, S.a_mid, REMOTE ? S.a_remote : (1 << 30));
   const int64_t nb = (n - a1 + 31) / 32;  // batches of 32 computed cells
+  const int M = S.mid_warps, F = S.far_warps;
 
   if (warp == 0) {
-    // ============================ chain stage ===============================
+    // ================================= chain ================================
+    const uint32_t bits = chain_bits(C.mask32, lane);
     for (int64_t b = 0; b < nb; ++b) {
       const int64_t c = a1 + 32 * b + lane;
       const uint32_t pos = ((uint32_t)c & (R - 1)) + R;
       T acc;
       if (!SMALL) {
         const int slot = (int)(b % kMidSlots);
-        while (ld_acquire_cta(&mid_ready[slot]) != (int)(b + 1)) {
-        }
+        mbar_wait(&mid_full[slot], (unsigned)((b / kMidSlots) & 1));
         acc = mid_part[slot * 32 + lane];
-        acc = chain_fold<OP, T, true>(acc, ring, pos, offs, C.jn, C.j32, S.k, C.mask32, lane);
+        acc = chain_fold<OP, T, true>(acc, ring, pos, offs, C.jn, C.j32, S.k, bits, lane);
       } else {
-        acc = chain_fold<OP, T, false>(T(0), ring, pos, offs, 0, C.j32, S.k, C.mask32, lane);
+        acc = chain_fold<OP, T, false>(T(0), ring, pos, offs, 0, C.j32, S.k, bits, lane);
       }
       if (c < n) {
         ring[pos - R] = acc;
         ring[pos] = acc;
-        if (SMALL || GFAR) out[c] = (int64_t)acc;
+        if (SMALL) out[c] = (int64_t)acc;
       }
       __syncwarp();
-      if (lane == 0) st_release_cta(final_count, (int)(b + 1));
+      if (!SMALL && lane == 0) mbar_arrive(&batch_done[b % kBatchBars]);
     }
-  } else if (!SMALL && warp <= S.mid_warps) {
-    // ============================ mid stage =================================
-    for (int64_t b = warp - 1; b < nb; b += S.mid_warps) {
-      spin_until_ge(final_count, (int)(b - 1));  // offsets >= 64 reach batches <= b-2
-      if (!GFAR && b >= 2) {  // stream batch b-2 (final, still in the ring) to HBM
-        const int64_t cw = a1 + 32 * (b - 2) + lane;
-        if (cw < n) out[cw] = (int64_t)ring[(uint32_t)cw & (R - 1)];
-      }
+  } else if (SMALL) {
+    // no other roles
+  } else if (warp <= M) {
+    // ================================== mid =================================
+    for (int64_t b = warp - 1; b < nb; b += M) {
+      wait_batches(batch_done, b - 1);  // offsets >= 64 reach batches <= b-2
       const int64_t c = a1 + 32 * b + lane;
       const T* base = ring + (((uint32_t)c & (R - 1)) + R);
       T acc = T(0);
       bool have = false;
       if (C.jf > 0) {
         const int fs = (int)(b % kFarSlots);
-        spin_until_ge(&far_ready[fs], (int)(b + 1));
+        mbar_wait(&far_full[fs], (unsigned)((b / kFarSlots) & 1));
         acc = far_part[fs * 32 + lane];
         have = true;
       }
-      acc = fold_range<OP, T, ASSOC>(acc, have, base, offs, C.jf, C.jn);
+      acc = fold_range<OP, T, ASSOC>(acc, have, base, ob, C.jf, C.jn);
       const int slot = (int)(b % kMidSlots);
       mid_part[slot * 32 + lane] = acc;
       __syncwarp();
-      if (lane == 0) st_release_cta(&mid_ready[slot], (int)(b + 1));
+      if (lane == 0) mbar_arrive(&mid_full[slot]);
     }
-  } else if (!SMALL && C.jf > 0 && warp <= S.mid_warps + S.far_warps) {
-    // ============================ far stage =================================
-    const int f = warp - 1 - S.mid_warps;
-    for (int64_t b = f; b < nb; b += S.far_warps) {
-      // operands final, and the slot's previous batch consumed by the mid stage
-      const int64_t need = b + 1 - C.far_look;
-      const int64_t need_slot = b + 1 - kFarSlots;
-      spin_until_ge(final_count, (int)(need > need_slot ? need : need_slot));
-      const int64_t c = a1 + 32 * b + lane;
-      T acc;
-      if (GFAR) {
-        acc = fold_range<OP, T, ASSOC>(T(0), false, out + c, offs, 0, C.jf);
-      } else {
-        const T* base = ring + (((uint32_t)c & (R - 1)) + R);
-        acc = fold_range<OP, T, ASSOC>(T(0), false, base, offs, 0, C.jf);
+  } else if (warp <= M + F) {
+    // ================================== far =================================
+    if (C.jf > 0) {
+      // ring slack: the writer may lag the chain; a far read must not reach a
+      // ring slot the chain is about to recycle before the writer copied it
+      const int64_t slack = ((int64_t)R - S.ring_cover - 64) / 32;
+      for (int64_t b = warp - 1 - M; b < nb; b += F) {
+        int64_t need = b + 1 - C.far_look;                       // operands written
+        need = max(need, b + 1 - (int64_t)kFarSlots);            // slot consumed
+        need = max(need, b + 1 - slack);                         // ring slack
+        wait_batches(written, need);
+        const int64_t c = a1 + 32 * b + lane;
+        T acc = T(0);
+        bool have = false;
+        if (REMOTE && C.jr > 0) {
+          const int rs = (int)(b % kRemSlots);
+          while (ld_acquire_gpu_i32(RM.ready + rs) != (int)(b + 1)) __nanosleep(64);
+          acc = ldv_cg<T, int64_t>(reinterpret_cast<const int64_t*>(RM.part) + rs * 32 + lane);
+          have = true;
+        }
+        if (GFAR) {
+          acc = fold_range<OP, T, ASSOC, int64_t>(acc, have, out + c, obg, C.jr, C.jf);
+        } else {
+          const T* base = ring + (((uint32_t)c & (R - 1)) + R);
+          acc = fold_range<OP, T, ASSOC>(acc, have, base, ob, C.jr, C.jf);
+        }
+        const int fs = (int)(b % kFarSlots);
+        far_part[fs * 32 + lane] = acc;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&far_full[fs]);
       }
-      const int fs = (int)(b % kFarSlots);
-      far_part[fs * 32 + lane] = acc;
+    }
+  } else if (warp == M + F + 1) {
+    // ================================= writer ===============================
+    for (int64_t b = 0; b < nb; ++b) {
+      mbar_wait(&batch_done[b % kBatchBars], (unsigned)((b / kBatchBars) & 1));
+      const int64_t c = a1 + 32 * b + lane;
+      if (c < n) out[c] = (int64_t)ring[(uint32_t)c & (R - 1)];
       __syncwarp();
-      if (lane == 0) st_release_cta(&far_ready[fs], (int)(b + 1));
+      if (lane == 0) mbar_arrive(&written[b % kBatchBars]);
+      if (REMOTE && ((b + 1) % kPubEvery == 0 || b + 1 == nb)) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_gpu(reinterpret_cast<long long*>(RM.published), (long long)(b + 1));
+      }
     }
   }
+}
+
+// The remote operand fold of one batch, split over the CTA's warps in
+// contiguous offset ranges and combined in order (requires ASSOC).
+template <int OP, typename T>
+__device__ __forceinline__ void sdp_producer(const SdpShape& S, const int64_t* __restrict__ offsets,
+                                             const int64_t* out, const SdpRemote& RM, int pid, int np) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  using O = SemiOp<OP, T>;
+  const int kpad = (S.k + 3) & ~3;
+  int32_t* offs = reinterpret_cast<int32_t*>(smem);
+  int32_t* obg = offs + kpad;
+  T* red = reinterpret_cast<T*>(obg + kpad);  // [warps][32]
+  __shared__ int s_jr;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = S.remote_warps;
+  for (int j = tid; j < S.k; j += 32 * W) {
+    offs[j] = (int32_t)offsets[j];
+    obg[j] = offs[j] * 8;
+  }
   __syncthreads();
-  if (!SMALL && !GFAR) {  // the last two batches were never streamed by a mid warp
-    const int64_t first = nb >= 2 ? nb - 2 : 0;
-    for (int64_t i = a1 + 32 * first + tid; i < n; i += blockDim.x) {
-      out[i] = (int64_t)ring[(uint32_t)i & (R - 1)];
+  if (tid == 0) {
+    int jr = 0;
+    for (int j = 0; j < S.k; ++j) jr += offs[j] >= S.a_remote;
+    s_jr = jr;
+  }
+  __syncthreads();
+  const int jr = s_jr;
+  if (jr == 0) return;
+  const int64_t look = offs[jr - 1] / 32;
+  const int per = (jr + W - 1) / W;
+  const int lo = min(jr, warp * per), hi = min(jr, lo + per);
+  const int64_t nb = (S.n - S.a1 + 31) / 32;
+  for (int64_t b = pid; b < nb; b += np) {
+    if (tid == 0) {
+      const long long need = (long long)max(b + 1 - look, b + 1 - (int64_t)kRemSlots);
+      while ((long long)ld_acquire_gpu(reinterpret_cast<const long long*>(RM.published)) < need)
+        __nanosleep(128);
     }
+    __syncthreads();
+    const int64_t c = S.a1 + 32 * b + lane;
+    if (lo < hi) {
+      red[warp * 32 + lane] = fold_range<OP, T, true, int64_t, true>(T(0), false, out + c, obg, lo, hi);
+    }
+    __syncthreads();
+    if (warp == 0) {
+      T acc = red[lane];
+      for (int w = 1; w < W; ++w) {
+        if (min(jr, w * per) < min(jr, w * per + per)) acc = O::apply(acc, red[w * 32 + lane]);
+      }
+      const int rs = (int)(b % kRemSlots);
+      reinterpret_cast<int64_t*>(RM.part)[rs * 32 + lane] = (int64_t)acc;
+      __threadfence();
+      __syncwarp();
+      if (lane == 0) st_release_gpu_i32(RM.ready + rs, (int)(b + 1));
+    }
+  }
+}
+
+template <int OP, typename T, bool SMALL, bool ASSOC, bool GFAR>
+__global__ void __launch_bounds__(1024, 1)
+    sdp_pipeline_cta(const SdpShape S, const int64_t* __restrict__ g_offsets,
+                     const int64_t* __restrict__ g_init, int64_t* __restrict__ g_out) {
+  const int64_t inst = blockIdx.x;
+  sdp_finisher<OP, T, SMALL, ASSOC, GFAR, false>(S, g_offsets + inst * S.k, g_init + inst * S.a1,
+                                                 g_out + inst * S.n, SdpRemote{});
+}
+
+// Multi-CTA single instance (cooperative launch: all CTAs co-resident).
+// Block 0 is the finisher, blocks 1.. are remote producers.
+template <int OP, typename T, bool GFAR>
+__global__ void __launch_bounds__(1024, 1)
+    sdp_pipeline_multi(const SdpShape S, const int64_t* __restrict__ g_offsets,
+                       const int64_t* __restrict__ g_init, int64_t* g_out, const SdpRemote RM) {
+  if (blockIdx.x == 0) {
+    sdp_finisher<OP, T, false, true, GFAR, true>(S, g_offsets, g_init, g_out, RM);
+  } else {
+    if (threadIdx.x >= 32 * S.remote_warps) return;
+    sdp_producer<OP, T>(S, g_offsets, g_out, RM, blockIdx.x - 1, gridDim.x - 1);
   }
 }
 
@@ -308,14 +457,18 @@ __global__ void __launch_bounds__(256)
   const int kpad = (S.k + 3) & ~3;
   T* ring = reinterpret_cast<T*>(smem) + (size_t)warp * 2 * R;
   int32_t* offs = reinterpret_cast<int32_t*>(reinterpret_cast<T*>(smem) + (size_t)wpb * 2 * R) +
-                  (size_t)warp * kpad;
+                  (size_t)warp * 2 * kpad;
+  int32_t* ob = offs + kpad;
   const int64_t inst = (int64_t)blockIdx.x * wpb + warp;
   if (inst >= batch) return;
   const int64_t a1 = S.a1, n = S.n;
   const int64_t* io = g_offsets + inst * S.k;
   const int64_t* ii = g_init + inst * a1;
   int64_t* o = out + inst * n;
-  for (int j = lane; j < S.k; j += 32) offs[j] = (int32_t)io[j];
+  for (int j = lane; j < S.k; j += 32) {
+    offs[j] = (int32_t)io[j];
+    ob[j] = offs[j] * (int32_t)sizeof(T);
+  }
   for (int64_t i = lane; i < a1; i += 32) {
     const int64_t v = ii[i];
     const uint32_t p = (uint32_t)i & (R - 1);
@@ -332,16 +485,17 @@ __global__ void __launch_bounds__(256)
     j32 = j;
     mask32 |= 1u << a;
   }
+  const uint32_t bits = chain_bits(mask32, lane);
   const int64_t nb = (n - a1 + 31) / 32;
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t c = a1 + 32 * b + lane;
     const uint32_t pos = ((uint32_t)c & (R - 1)) + R;
     T acc;
     if (!SMALL) {
-      acc = fold_range<OP, T, ASSOC>(T(0), false, ring + pos, offs, 0, j32);
-      acc = chain_fold<OP, T, true>(acc, ring, pos, offs, j32, j32, S.k, mask32, lane);
+      acc = fold_range<OP, T, ASSOC>(T(0), false, ring + pos, ob, 0, j32);
+      acc = chain_fold<OP, T, true>(acc, ring, pos, offs, j32, j32, S.k, bits, lane);
     } else {
-      acc = chain_fold<OP, T, false>(T(0), ring, pos, offs, 0, 0, S.k, mask32, lane);
+      acc = chain_fold<OP, T, false>(T(0), ring, pos, offs, 0, 0, S.k, bits, lane);
     }
     if (c < n) {
       ring[pos - R] = acc;
@@ -361,15 +515,14 @@ __global__ void sdp_chain_step_probe(int64_t batches, T seed, long long* cycles,
   using O = SemiOp<OP, T>;
   const int lane = threadIdx.x & 31;
   T acc = seed + (T)lane;
-  const uint32_t bits = ((2u << lane) - 1u) & ~1u;
-  const uint32_t rev = bits << (31 - lane);
+  const uint32_t bits = chain_bits(0xFFFFFFFEu, lane);
   __syncwarp();
   const long long t0 = clock64();
   for (int64_t b = 0; b < batches; ++b) {
 #pragma unroll
     for (int t = 1; t < 32; ++t) {
       const T v = shfl_idx(acc, t - 1);
-      if ((rev >> (32 - t)) & 1u) acc = O::apply(acc, v);
+      if ((int32_t)(bits << (t - 1)) < 0) acc = O::apply(acc, v);
     }
     acc = shfl_idx(acc, 31);
   }

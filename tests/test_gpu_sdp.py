@@ -119,3 +119,27 @@ def test_pipeline_trace_fields(gpu):
     assert r.trace.first_head == inst.a1
     assert r.trace.steps_executed == inst.n + inst.k - inst.a1 - 1
     assert r.trace.stall_iterations == 0
+
+
+def test_large_a1_mixed_signs_hbm_far(gpu, oracle):
+    # non-associative (mixed-sign saturating-add) + a_1 too large for the ring:
+    # single CTA, strict order, far stage reading the HBM table
+    rng = np.random.default_rng(9)
+    offs, _ = oracle.generate_sdp(90000, 300, 4, False, 50000)
+    init = rng.choice([2**62, -(2**62), 5, -7], offs[0])
+    _check(gpu, oracle, offs, init, 90000, "saturating-add")
+
+
+@pytest.mark.parametrize("op", ["min", "modular-add"])
+def test_single_cta_path_when_multi_disabled(gpu, oracle, op, monkeypatch):
+    monkeypatch.setenv("PIPEDP_SDP_MULTI", "0")
+    offs, init = oracle.generate_sdp(40000, 1024, 21, False, 4096)
+    _check(gpu, oracle, offs, init, 40000, op)
+
+
+@pytest.mark.parametrize("ctas,warps", [(1, 1), (3, 4), (64, 8)])
+def test_multi_cta_shapes(gpu, oracle, ctas, warps, monkeypatch):
+    monkeypatch.setenv("PIPEDP_SDP_REMOTE_CTAS", str(ctas))
+    monkeypatch.setenv("PIPEDP_SDP_REMOTE_WARPS", str(warps))
+    offs, init = oracle.generate_sdp(60000, 1500, 8, False, 6000)
+    _check(gpu, oracle, offs, init, 60000, "max")
