@@ -152,6 +152,10 @@ int32_t pipedp_digest_device(const int64_t* d_tables, int64_t count, int64_t nta
 int32_t pipedp_chain_step_ns(int32_t op, int32_t value_bits, int32_t device, double* ns_out,
                              double* sm_clock_mhz_out);
 
+/* Role-level cycle counters of the profiling build (-DPIPEDP_PROFILE,
+ * tools/build_profile.sh); returns PIPEDP_ERR_UNSUPPORTED otherwise. */
+int32_t pipedp_profile_read(uint64_t* out, int32_t count, int32_t reset);
+
 #ifdef __cplusplus
 }
 #endif

@@ -28,7 +28,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpipedp_cuda.so")
+LIB_PATH = os.environ.get("PIPEDP_LIB") or os.path.join(_HERE, "_lib", "libpipedp_cuda.so")
 DROPIN_PATH = os.path.join(_HERE, "_lib", "libpipedp_b200.so")
 
 ERRC = [
@@ -50,6 +50,7 @@ EXPORTS = (
     "pipedp_mcm_solve", "pipedp_mcm_pipeline", "pipedp_mcm_solve_batch",
     "pipedp_mcm_plan_create", "pipedp_mcm_plan_execute", "pipedp_mcm_plan_describe",
     "pipedp_mcm_plan_destroy", "pipedp_digest_device", "pipedp_chain_step_ns",
+    "pipedp_profile_read",
 )
 
 
@@ -480,6 +481,14 @@ class McmPlan:
 def digest_device(d_tables: int, count: int, ntables: int, d_out: int, stream: int = 0) -> None:
     _check(lib().pipedp_digest_device(C.c_void_p(d_tables), count, ntables, C.c_void_p(d_out),
                                       C.c_void_p(stream)))
+
+
+def profile_read(reset=True):
+    """Role cycle counters (profiling build only, PIPEDP_LIB=..._prof.so)."""
+    out = (C.c_uint64 * 128)()
+    lib().pipedp_profile_read.argtypes = [C.POINTER(C.c_uint64), C.c_int32, C.c_int32]
+    _check(lib().pipedp_profile_read(out, 128, int(reset)))
+    return list(out)
 
 
 def chain_step_ns(op="min", value_bits=32, device=-1):

@@ -30,6 +30,7 @@ INCLUDE = os.path.join(ROOT, "include")
 
 CUDA_SO = os.path.join(LIB, "libpipedp_cuda.so")
 DROPIN_SO = os.path.join(LIB, "libpipedp_b200.so")
+PROF_SO = os.path.join(LIB, "libpipedp_cuda_prof.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -52,17 +53,22 @@ def _sources(d, exts):
     return sorted(os.path.join(d, f) for f in os.listdir(d) if f.endswith(exts))
 
 
-def build(force: bool = False, verbose: bool = False) -> None:
+def build(force: bool = False, verbose: bool = False, profile: bool = False) -> None:
+    """profile=True builds _lib/libpipedp_cuda_prof.so with the role profiler."""
     os.makedirs(LIB, exist_ok=True)
     nvcc = _nvcc()
     cuda_srcs = _sources(CSRC, (".cu", ".cuh")) + [os.path.join(INCLUDE, "pipedp_cuda.h")]
-    if force or _newer(CUDA_SO, cuda_srcs):
+    target = PROF_SO if profile else CUDA_SO
+    if force or _newer(target, cuda_srcs):
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                "-Xptxas", "-v" if verbose else "-O3",
                "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static",
-               "-I", INCLUDE, os.path.join(CSRC, "capi.cu"), "-o", CUDA_SO + ".tmp"]
+               *(["-DPIPEDP_PROFILE"] if profile else []),
+               "-I", INCLUDE, os.path.join(CSRC, "capi.cu"), "-o", target + ".tmp"]
         _run(cmd, verbose)
-        os.replace(CUDA_SO + ".tmp", CUDA_SO)
+        os.replace(target + ".tmp", target)
+    if profile:
+        return
     host_srcs = _sources(HOST, (".cpp", ".hpp")) + _sources(os.path.join(INCLUDE, "pipedp"), (".hpp",))
     if force or _newer(DROPIN_SO, host_srcs + [CUDA_SO]):
         cmd = ["g++", "-std=c++20", "-O3", "-fPIC", "-shared", "-I", INCLUDE,
@@ -84,4 +90,4 @@ def _run(cmd, verbose):
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv, profile="--profile" in sys.argv)

@@ -259,7 +259,7 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
     const size_t per_warp = 2 * R * vb + 2 * kpad * 4;
     if (per_warp <= 16 * 1024) {
       d->warp_kernel = true;
-      d->small = a1 < 32;
+      d->small = a1 < 64;
       d->gfar = false;
       s.ring_log2 = ceil_log2((uint64_t)R);
       s.ring_cover = (int32_t)a1;
@@ -296,11 +296,12 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
   const int64_t nb = (n - a1 + 31) / 32;
   d->remote = batch == 1 && d->assoc && jr_max >= 128 && nb >= 256 &&
               env_int("PIPEDP_SDP_MULTI", 1) != 0;
-  s.mid_warps = 4;
+  s.mid_warps = env_int("PIPEDP_SDP_MID_WARPS", 4);
   if (d->remote) {
-    s.a_remote = kARemote;
-    s.ring_cover = kARemote;
-    s.ring_log2 = ceil_log2((uint64_t)(kARemote + 512));
+    const int a_rem = std::max(kAMid, env_int("PIPEDP_SDP_AREMOTE", kARemote));
+    s.a_remote = a_rem;
+    s.ring_cover = a_rem;
+    s.ring_log2 = ceil_log2((uint64_t)(a_rem + 512));
     d->gfar = false;
     s.far_warps = (int32_t)std::min<int64_t>(16, std::max<int64_t>(1, (jf_max - jr_max + 47) / 48));
     s.remote_warps = env_int("PIPEDP_SDP_REMOTE_WARPS", 8);
@@ -322,9 +323,9 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
       if (d->smem > 227 * 1024)
         return fail(PIPEDP_ERR_UNSUPPORTED, "k=%lld offsets exceed shared memory", (long long)k);
     }
-    s.far_warps = (int32_t)std::min<int64_t>(24, std::max<int64_t>(1, (jf_max + 47) / 48));
+    s.far_warps = (int32_t)std::min<int64_t>(19, std::max<int64_t>(1, (jf_max + 47) / 48));  // <= 32 warps
   }
-  d->threads = 32 * (1 + s.mid_warps + s.far_warps + 1);
+  d->threads = 32 * sdp_warps_for_roles(s.mid_warps + s.far_warps + 1);
   d->threads = std::max(d->threads, 32 * s.remote_warps);
   return PIPEDP_OK;
 }
@@ -932,6 +933,41 @@ int32_t pipedp_digest_device(const int64_t* d_tables, int64_t count, int64_t nta
       d_tables, count, ntables, d_digests);
   CK(cudaGetLastError());
   return PIPEDP_OK;
+}
+
+int32_t pipedp_chain_fold_cycles(uint32_t hi, uint32_t m32, int32_t mode, double* cycles_out) {
+  TRY(select_device(-1));
+  Scope sc;
+  TRY(sc.init());
+  long long* d_cyc = nullptr;
+  int32_t* d_sink = nullptr;
+  TRY(sc.alloc(&d_cyc, 1));
+  TRY(sc.alloc(&d_sink, 32));
+  for (int rep = 0; rep < 2; ++rep)
+    sdp_chain_fold_probe<kMin, int32_t><<<1, 32, 0, sc.stream>>>(1 << 14, hi, m32, mode, d_cyc, d_sink);
+  CK(cudaGetLastError());
+  long long c = 0;
+  CK(cudaMemcpyAsync(&c, d_cyc, sizeof c, cudaMemcpyDeviceToHost, sc.stream));
+  CK(cudaStreamSynchronize(sc.stream));
+  *cycles_out = (double)c;
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_profile_read(uint64_t* out, int32_t count, int32_t reset) {
+#ifdef PIPEDP_PROFILE
+  unsigned long long h[128];
+  CK(cudaMemcpyFromSymbol(h, pipedp_dev::g_prof, sizeof h));
+  for (int i = 0; i < count && i < 128; ++i) out[i] = h[i];
+  if (reset) {
+    memset(h, 0, sizeof h);
+    CK(cudaMemcpyToSymbol(pipedp_dev::g_prof, h, sizeof h));
+  }
+  return PIPEDP_OK;
+#else
+  for (int i = 0; i < count; ++i) out[i] = 0;
+  (void)reset;
+  return fail(PIPEDP_ERR_UNSUPPORTED, "library built without -DPIPEDP_PROFILE");
+#endif
 }
 
 int32_t pipedp_chain_step_ns(int32_t op, int32_t value_bits, int32_t device, double* ns_out,

@@ -84,6 +84,29 @@ struct SemiOp<kModAdd, int32_t> {
   }
 };
 
+// Identity elements, used only where the host proved the fold associative and
+// the accumulator already holds a real operand (min/max trivially; mod-add: 0
+// since (norm(a) + 0) mod M = norm(a) and the accumulator is normalised once
+// two operands were combined; saturating-add on same-signed values: 0).
+template <int OP, typename T>
+struct SemiId;
+template <typename T>
+struct SemiId<kMin, T> {
+  __device__ __forceinline__ static T value() { return sizeof(T) == 4 ? (T)INT32_MAX : (T)INT64_MAX; }
+};
+template <typename T>
+struct SemiId<kMax, T> {
+  __device__ __forceinline__ static T value() { return sizeof(T) == 4 ? (T)INT32_MIN : (T)INT64_MIN; }
+};
+template <typename T>
+struct SemiId<kModAdd, T> {
+  __device__ __forceinline__ static T value() { return T(0); }
+};
+template <typename T>
+struct SemiId<kSatAdd, T> {
+  __device__ __forceinline__ static T value() { return T(0); }
+};
+
 // ---- memory-model helpers --------------------------------------------------
 __device__ __forceinline__ int ld_acquire_cta(const int* p) {
   int v;
@@ -146,5 +169,21 @@ __device__ __forceinline__ T shfl_idx(T v, int src) {
 }
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
+
+// ---- opt-in role profiler (build with -DPIPEDP_PROFILE; compiled out otherwise)
+// Slots: role * 8 + counter; accumulated in cycles by lane 0 of each warp.
+#ifdef PIPEDP_PROFILE
+__device__ unsigned long long g_prof[128];
+#define PROF_DECL(name) long long name = 0
+#define PROF_NOW() clock64()
+#define PROF_ADD(acc, t0) (acc) += clock64() - (t0)
+#define PROF_FLUSH(slot, v) \
+  if ((threadIdx.x & 31) == 0) atomicAdd(&::pipedp_dev::g_prof[(slot)], (unsigned long long)(v))
+#else
+#define PROF_DECL(name)
+#define PROF_NOW() 0
+#define PROF_ADD(acc, t0)
+#define PROF_FLUSH(slot, v)
+#endif
 
 }  // namespace pipedp_dev

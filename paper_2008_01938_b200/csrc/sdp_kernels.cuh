@@ -146,38 +146,236 @@ __device__ __forceinline__ uint32_t chain_bits(uint32_t mask32, int lane) {
   return (mask32 & ((2u << lane) - 1u) & ~1u) << (31 - lane);
 }
 
-template <int OP, typename T, bool HAVE_ACC>
-__device__ __forceinline__ T chain_fold(T acc, const T* __restrict__ ring, uint32_t ring_pos,
-                                        const int32_t* __restrict__ offs, int jb, int j32, int k,
-                                        uint32_t bits, int lane) {
-  using O = SemiOp<OP, T>;
-  bool have = HAVE_ACC;
-  for (int j = jb; j < j32; ++j) {  // offsets in [32, 64): out of batch for all lanes
-    const T v = ring[ring_pos - offs[j]];
-    acc = (HAVE_ACC || have) ? O::apply(acc, v) : v;
-    have = true;
-  }
-  for (int j = j32; j < k; ++j) {  // offsets < 32 reaching into earlier batches (a > lane)
-    const int a = offs[j];
-    if (a > lane) {
-      const T v = ring[ring_pos - a];
-      acc = (HAVE_ACC || have) ? O::apply(acc, v) : v;
-      have = true;
-    }
-  }
-  // in-batch chain: step t folds offset a = lane - t + 1 with lane t-1's value
-#pragma unroll
-  for (int t = 1; t < 32; ++t) {
-    const T v = shfl_idx(acc, t - 1);
-    const bool take = (int32_t)(bits << (t - 1)) < 0;
+// Bit (32 - t) of `bits`, tested at step t.  asm volatile keeps the test at its
+// step: left to itself the compiler materialises all 31 predicates up front
+// (~100 bit-shuffling instructions per batch on the critical warp).
+template <int T_STEP>
+__device__ __forceinline__ bool chain_take(uint32_t bits) {
+  uint32_t r;
+  asm volatile("and.b32 %0, %1, %2;" : "=r"(r) : "r"(bits), "n"(1u << (32 - T_STEP)));
+  return r != 0;
+}
+
+template <int OP, typename T, bool HAVE_ACC, int T_STEP>
+struct ChainSteps {
+  __device__ __forceinline__ static void run(T& acc, bool& have, uint32_t bits) {
+    using O = SemiOp<OP, T>;
+    const T v = shfl_idx(acc, T_STEP - 1);
+    const bool take = chain_take<T_STEP>(bits);
     if (HAVE_ACC) {
       if (take) acc = O::apply(acc, v);
     } else {
       if (take) acc = have ? O::apply(acc, v) : v;
       have = have || take;
     }
+    ChainSteps<OP, T, HAVE_ACC, T_STEP + 1>::run(acc, have, bits);
   }
+};
+template <int OP, typename T, bool HAVE_ACC>
+struct ChainSteps<OP, T, HAVE_ACC, 32> {
+  __device__ __forceinline__ static void run(T&, bool&, uint32_t) {}
+};
+
+// Out-of-batch operands of the chain warp: offsets d in [32, 64) (all lanes)
+// and d < 32 with d > lane, in descending d.  Displacements are compile-time
+// immediates.  The 63 candidate slots are processed in groups of 16: all 16
+// loads are issued first (distinct registers, unconditional -- every slot lies
+// inside the ring), then
+//   ASSOC: absent slots become the operator's identity and the group is
+//          reduced as a tree, one (x) into the accumulator per group;
+//   strict: predicated left fold in descending d (saturating-add, mixed signs).
+template <int D>
+__device__ __forceinline__ bool pre_take(uint32_t hi, uint32_t lo) {
+  uint32_t r;
+  if (D >= 32) asm volatile("and.b32 %0, %1, %2;" : "=r"(r) : "r"(hi), "n"(1u << (D >= 32 ? D - 32 : 0)));
+  else asm volatile("and.b32 %0, %1, %2;" : "=r"(r) : "r"(lo), "n"(1u << (D < 32 ? D : 0)));
+  return r != 0;
+}
+
+template <int OP, typename T, int D0>  // slots D0, D0-1, ..., D0-15 (those >= 1)
+__device__ __forceinline__ void pre_group_assoc(T& acc, const T* p, uint32_t hi, uint32_t lo) {
+  using O = SemiOp<OP, T>;
+  const T id = SemiId<OP, T>::value();
+  T v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = (D0 - i >= 1) ? p[-(D0 - i)] : id;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    bool t = false;
+    switch (i) {  // keep the immediates compile-time
+#define PRE_CASE(I) case I: t = (D0 - I >= 1) && pre_take<(D0 - I >= 1 ? D0 - I : 1)>(hi, lo); break;
+      PRE_CASE(0) PRE_CASE(1) PRE_CASE(2) PRE_CASE(3) PRE_CASE(4) PRE_CASE(5) PRE_CASE(6)
+      PRE_CASE(7) PRE_CASE(8) PRE_CASE(9) PRE_CASE(10) PRE_CASE(11) PRE_CASE(12) PRE_CASE(13)
+      PRE_CASE(14) PRE_CASE(15)
+#undef PRE_CASE
+    }
+    if (!t) v[i] = id;
+  }
+#pragma unroll
+  for (int w = 8; w >= 1; w >>= 1) {
+#pragma unroll
+    for (int i = 0; i < w; ++i) v[i] = O::apply(v[i], v[i + w]);
+  }
+  acc = O::apply(acc, v[0]);
+}
+
+template <int OP, typename T, bool HAVE_ACC, int D0>
+__device__ __forceinline__ void pre_group_strict(T& acc, bool& have, const T* p, uint32_t hi,
+                                                 uint32_t lo) {
+  using O = SemiOp<OP, T>;
+  T v[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = (D0 - i >= 1) ? p[-(D0 - i)] : T(0);
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    bool t = false;
+    switch (i) {
+#define PRE_CASE(I) case I: t = (D0 - I >= 1) && pre_take<(D0 - I >= 1 ? D0 - I : 1)>(hi, lo); break;
+      PRE_CASE(0) PRE_CASE(1) PRE_CASE(2) PRE_CASE(3) PRE_CASE(4) PRE_CASE(5) PRE_CASE(6)
+      PRE_CASE(7) PRE_CASE(8) PRE_CASE(9) PRE_CASE(10) PRE_CASE(11) PRE_CASE(12) PRE_CASE(13)
+      PRE_CASE(14) PRE_CASE(15)
+#undef PRE_CASE
+    }
+    if (t) {
+      if (HAVE_ACC) {
+        acc = O::apply(acc, v[i]);
+      } else {
+        acc = have ? O::apply(acc, v[i]) : v[i];
+        have = true;
+      }
+    }
+  }
+}
+
+template <int OP, typename T, bool HAVE_ACC, bool ASSOC>
+__device__ __forceinline__ void pre_steps(T& acc, bool& have, const T* p, uint32_t hi, uint32_t lo) {
+  // 64-bit modular-add keeps the strict path: folding the identity would
+  // normalise a raw single operand (k = 1 copies raw values, sdp.cpp:53)
+  constexpr bool kTree = ASSOC && HAVE_ACC && !(OP == kModAdd && sizeof(T) == 8);
+  if (kTree) {
+    pre_group_assoc<OP, T, 63>(acc, p, hi, lo);
+    pre_group_assoc<OP, T, 47>(acc, p, hi, lo);
+    pre_group_assoc<OP, T, 31>(acc, p, hi, lo);
+    pre_group_assoc<OP, T, 15>(acc, p, hi, lo);
+  } else {
+    pre_group_strict<OP, T, HAVE_ACC, 63>(acc, have, p, hi, lo);
+    pre_group_strict<OP, T, HAVE_ACC, 47>(acc, have, p, hi, lo);
+    pre_group_strict<OP, T, HAVE_ACC, 31>(acc, have, p, hi, lo);
+    pre_group_strict<OP, T, HAVE_ACC, 15>(acc, have, p, hi, lo);
+  }
+}
+
+// Per-lane chain masks of one instance.
+struct ChainMasks {
+  uint32_t hi;    // bit d-32 for offsets d in [32, 64)
+  uint32_t lo;    // bit d for offsets d < 32 with d > lane (out of batch)
+  uint32_t bits;  // chain_bits(): in-batch steps
+};
+
+__device__ __forceinline__ ChainMasks chain_masks(const int32_t* offs, int k, int lane) {
+  uint32_t hi = 0, m32 = 0;
+  for (int j = k - 1; j >= 0; --j) {
+    const int a = offs[j];
+    if (a >= 64) break;
+    if (a >= 32) hi |= 1u << (a - 32);
+    else m32 |= 1u << a;
+  }
+  return ChainMasks{hi, m32 & ~((2u << lane) - 1u), chain_bits(m32, lane)};
+}
+
+// The chain warp's fold for one batch: every offset < 64, strictly in
+// descending order.  HAVE_ACC=false: no larger offset exists, the first
+// operand is ASSIGNED (possibly inside the shuffle chain).  ring_pos =
+// position of this lane's cell in the upper ring half.
+template <int OP, typename T, bool HAVE_ACC, bool ASSOC>
+__device__ __forceinline__ T chain_fold(T acc, const T* __restrict__ ring, uint32_t ring_pos,
+                                        const ChainMasks& m) {
+  bool have = HAVE_ACC;
+  pre_steps<OP, T, HAVE_ACC, ASSOC>(acc, have, ring + ring_pos, m.hi, m.lo);
+  // in-batch chain: step t folds offset a = lane - t + 1 with lane t-1's value
+  ChainSteps<OP, T, HAVE_ACC, 1>::run(acc, have, m.bits);
   return acc;
+}
+
+// ---- look-ahead chain (associative ops) -------------------------------------
+// While batch b's shuffle chain broadcasts cell t-1 of batch b, every lane l
+// also folds it into its accumulator for batch b+1 when offset d = l+33-t is in
+// the set (the cell c0+32+l-d of batch b+1's lane l).  Together with the ring
+// group d >= l+33 (cells of batch b-1, folded first) this covers every
+// out-of-batch offset < 64 of batch b+1 in descending d, so batch b+1 starts
+// with mid(b+1) (x) next -- regrouping only (ASSOC).  Step 32 broadcasts lane
+// 31 for d = l+1.
+struct LaMasks {
+  uint32_t bits;   // in-batch steps of the current batch (chain_bits)
+  uint32_t nbits;  // bit 32-t: offset l+33-t present (t = 1..32)
+  uint32_t far;    // bit d-32 for d in [l+33, 63] present
+};
+
+__device__ __forceinline__ LaMasks la_masks(const int32_t* offs, int k, int lane) {
+  uint64_t s64 = 0;
+  for (int j = k - 1; j >= 0; --j) {
+    const int a = offs[j];
+    if (a >= 64) break;
+    s64 |= 1ull << a;
+  }
+  const uint32_t hi = (uint32_t)(s64 >> 32);
+  return LaMasks{chain_bits((uint32_t)s64, lane), (uint32_t)(s64 >> (lane + 1)),
+                 hi & ~((2u << lane) - 1u)};
+}
+
+template <int T_STEP>
+__device__ __forceinline__ bool bit_at(uint32_t m) {
+  uint32_t r;
+  asm volatile("and.b32 %0, %1, %2;" : "=r"(r) : "r"(m), "n"(1u << (32 - T_STEP)));
+  return r != 0;
+}
+
+template <int OP, typename T, int T_STEP>
+struct LaSteps {
+  __device__ __forceinline__ static void run(T& acc, T& nxt, const LaMasks& m) {
+    using O = SemiOp<OP, T>;
+    const T v = shfl_idx(acc, T_STEP - 1);
+    if (bit_at<T_STEP>(m.bits)) acc = O::apply(acc, v);
+    if (bit_at<T_STEP>(m.nbits)) nxt = O::apply(nxt, v);
+    LaSteps<OP, T, T_STEP + 1>::run(acc, nxt, m);
+  }
+};
+template <int OP, typename T>
+struct LaSteps<OP, T, 32> {
+  __device__ __forceinline__ static void run(T& acc, T& nxt, const LaMasks& m) {
+    using O = SemiOp<OP, T>;
+    const T v = shfl_idx(acc, 31);  // last cell of the batch, offset l+1 of the next
+    uint32_t r;
+    asm volatile("and.b32 %0, %1, 1;" : "=r"(r) : "r"(m.nbits));
+    if (r) nxt = O::apply(nxt, v);
+  }
+};
+
+// Ring group of offsets d in [l+33, 63] below p (cells two batches back),
+// identity for absent slots, tree-reduced.  The identity select is arithmetic
+// (sign-extended mask bit + LOP3): 31 live predicates exhaust the 7 predicate
+// registers.
+template <typename T>
+__device__ __forceinline__ T sel_or_id(T x, T id, uint32_t word, int bit) {
+  const int32_t m32 = (int32_t)(word << (31 - bit)) >> 31;  // 0 or -1
+  const T m = (T)m32;
+  return (x & m) | (id & ~m);
+}
+
+template <int OP, typename T>
+__device__ __forceinline__ T la_ring_group(const T* p, uint32_t far) {
+  using O = SemiOp<OP, T>;
+  const T id = SemiId<OP, T>::value();
+  T v[32];
+#pragma unroll
+  for (int i = 0; i < 31; ++i) v[i] = sel_or_id(p[-(63 - i)], id, far, 31 - i);  // d = 63 - i
+  v[31] = id;
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+#pragma unroll
+    for (int i = 0; i < w; ++i) v[i] = O::apply(v[i], v[i + w]);
+  }
+  return v[0];
 }
 
 // Offset classes of one instance, from its raw offsets in shared memory.
@@ -201,6 +399,16 @@ __device__ __forceinline__ SdpClasses sdp_classes(const int32_t* offs, int k, in
   c.far_look = c.jf > c.jr ? offs[c.jf - 1] / 32 : 1 << 30;
   c.rem_look = c.jr > 0 ? offs[c.jr - 1] / 32 : 1 << 30;
   return c;
+}
+
+// Warp ids of the non-chain roles skip every id that is 0 mod 4: warps map to
+// SM sub-partitions by id % 4, so the chain warp (id 0) owns SMSP 0 alone and
+// its shuffle/(x) chain never waits behind another warp's issue.
+__host__ __device__ __forceinline__ int sdp_role_of_warp(int warp) {
+  return (warp % 4 == 0) ? -1 : warp - 1 - warp / 4;
+}
+__host__ __device__ __forceinline__ int sdp_warps_for_roles(int roles) {
+  return roles == 0 ? 1 : 2 + (roles - 1) + (roles - 1) / 3;
 }
 
 __device__ __forceinline__ void wait_batches(uint64_t* bars, int64_t count) {
@@ -267,21 +475,49 @@ __device__ __forceinline__ void sdp_finisher(const SdpShape& S, const int64_t* _
   const SdpClasses C = sdp_classes(offs, S.k, S.a_mid, REMOTE ? S.a_remote : (1 << 30));
   const int64_t nb = (n - a1 + 31) / 32;  // batches of 32 computed cells
   const int M = S.mid_warps, F = S.far_warps;
+  const int role = sdp_role_of_warp(warp);  // -1: chain warp or an idle SMSP-0 warp
 
   if (warp == 0) {
     // ================================= chain ================================
-    const uint32_t bits = chain_bits(C.mask32, lane);
+    const ChainMasks cm = chain_masks(offs, S.k, lane);
+    constexpr bool kLA = !SMALL && ASSOC && !(OP == kModAdd && sizeof(T) == 8);
+    const LaMasks lm = la_masks(offs, S.k, lane);
+    T nxt = T(0);  // look-ahead accumulator of the next batch (kLA)
+    if (kLA) {
+      // seed nxt for batch 0: offsets d in [l+1, l+32] over the preset cells,
+      // descending (what the look-ahead of a virtual batch -1 would have folded)
+      nxt = SemiId<OP, T>::value();
+      const uint32_t pos0 = ((uint32_t)(a1 + lane) & (R - 1)) + R;
+      for (int d = lane + 32; d >= lane + 1; --d) {
+        if ((lm.nbits >> (d - lane - 1)) & 1u) nxt = SemiOp<OP, T>::apply(nxt, ring[pos0 - d]);
+      }
+    }
+    PROF_DECL(p_wait);
+    PROF_DECL(p_fold);
+    PROF_DECL(p_all);
+    const long long p_start = PROF_NOW();
     for (int64_t b = 0; b < nb; ++b) {
       const int64_t c = a1 + 32 * b + lane;
       const uint32_t pos = ((uint32_t)c & (R - 1)) + R;
       T acc;
       if (!SMALL) {
         const int slot = (int)(b % kMidSlots);
+        const long long t0 = PROF_NOW();
         mbar_wait(&mid_full[slot], (unsigned)((b / kMidSlots) & 1));
+        PROF_ADD(p_wait, t0);
         acc = mid_part[slot * 32 + lane];
-        acc = chain_fold<OP, T, true>(acc, ring, pos, offs, C.jn, C.j32, S.k, bits, lane);
+        const long long t1 = PROF_NOW();
+        if (kLA) {
+          // mid(b) already holds the offsets >= l+33; nxt the ones in [l+1, l+32]
+          acc = SemiOp<OP, T>::apply(acc, nxt);
+          nxt = SemiId<OP, T>::value();
+          LaSteps<OP, T, 1>::run(acc, nxt, lm);
+        } else {
+          acc = chain_fold<OP, T, true, ASSOC>(acc, ring, pos, cm);
+        }
+        PROF_ADD(p_fold, t1);
       } else {
-        acc = chain_fold<OP, T, false>(T(0), ring, pos, offs, 0, C.j32, S.k, bits, lane);
+        acc = chain_fold<OP, T, false, ASSOC>(T(0), ring, pos, cm);
       }
       if (c < n) {
         ring[pos - R] = acc;
@@ -291,48 +527,78 @@ __device__ __forceinline__ void sdp_finisher(const SdpShape& S, const int64_t* _
       __syncwarp();
       if (!SMALL && lane == 0) mbar_arrive(&batch_done[b % kBatchBars]);
     }
-  } else if (SMALL) {
-    // no other roles
-  } else if (warp <= M) {
+    PROF_ADD(p_all, p_start);
+    PROF_FLUSH(0, p_wait);
+    PROF_FLUSH(1, p_fold);
+    PROF_FLUSH(2, p_all);
+    PROF_FLUSH(3, nb);
+  } else if (SMALL || role < 0) {
+    // no work: the chain warp keeps SMSP 0 to itself
+  } else if (role < M) {
     // ================================== mid =================================
-    for (int64_t b = warp - 1; b < nb; b += M) {
+    PROF_DECL(p_wfc);
+    PROF_DECL(p_wfar);
+    PROF_DECL(p_fold);
+    constexpr bool kMidLA = ASSOC && !(OP == kModAdd && sizeof(T) == 8);
+    const LaMasks mlm = la_masks(offs, S.k, lane);
+    for (int64_t b = role; b < nb; b += M) {
+      long long t0 = PROF_NOW();
       wait_batches(batch_done, b - 1);  // offsets >= 64 reach batches <= b-2
+      PROF_ADD(p_wfc, t0);
       const int64_t c = a1 + 32 * b + lane;
       const T* base = ring + (((uint32_t)c & (R - 1)) + R);
       T acc = T(0);
       bool have = false;
       if (C.jf > 0) {
         const int fs = (int)(b % kFarSlots);
+        t0 = PROF_NOW();
         mbar_wait(&far_full[fs], (unsigned)((b / kFarSlots) & 1));
+        PROF_ADD(p_wfar, t0);
         acc = far_part[fs * 32 + lane];
         have = true;
       }
+      t0 = PROF_NOW();
       acc = fold_range<OP, T, ASSOC>(acc, have, base, ob, C.jf, C.jn);
+      if (kMidLA) {  // the chain warp's look-ahead leaves offsets in [l+33, 63] to mid
+        acc = SemiOp<OP, T>::apply(acc, la_ring_group<OP, T>(base, mlm.far));
+      }
       const int slot = (int)(b % kMidSlots);
       mid_part[slot * 32 + lane] = acc;
       __syncwarp();
       if (lane == 0) mbar_arrive(&mid_full[slot]);
+      PROF_ADD(p_fold, t0);
     }
-  } else if (warp <= M + F) {
+    PROF_FLUSH(8, p_wfc);
+    PROF_FLUSH(9, p_wfar);
+    PROF_FLUSH(10, p_fold);
+  } else if (role < M + F) {
     // ================================== far =================================
     if (C.jf > 0) {
       // ring slack: the writer may lag the chain; a far read must not reach a
       // ring slot the chain is about to recycle before the writer copied it
       const int64_t slack = ((int64_t)R - S.ring_cover - 64) / 32;
-      for (int64_t b = warp - 1 - M; b < nb; b += F) {
+      PROF_DECL(p_ww);
+      PROF_DECL(p_wr);
+      PROF_DECL(p_fold);
+      for (int64_t b = role - M; b < nb; b += F) {
         int64_t need = b + 1 - C.far_look;                       // operands written
         need = max(need, b + 1 - (int64_t)kFarSlots);            // slot consumed
         need = max(need, b + 1 - slack);                         // ring slack
+        long long t0 = PROF_NOW();
         wait_batches(written, need);
+        PROF_ADD(p_ww, t0);
         const int64_t c = a1 + 32 * b + lane;
         T acc = T(0);
         bool have = false;
         if (REMOTE && C.jr > 0) {
           const int rs = (int)(b % kRemSlots);
+          t0 = PROF_NOW();
           while (ld_acquire_gpu_i32(RM.ready + rs) != (int)(b + 1)) __nanosleep(64);
+          PROF_ADD(p_wr, t0);
           acc = ldv_cg<T, int64_t>(reinterpret_cast<const int64_t*>(RM.part) + rs * 32 + lane);
           have = true;
         }
+        t0 = PROF_NOW();
         if (GFAR) {
           acc = fold_range<OP, T, ASSOC, int64_t>(acc, have, out + c, obg, C.jr, C.jf);
         } else {
@@ -343,9 +609,13 @@ __device__ __forceinline__ void sdp_finisher(const SdpShape& S, const int64_t* _
         far_part[fs * 32 + lane] = acc;
         __syncwarp();
         if (lane == 0) mbar_arrive(&far_full[fs]);
+        PROF_ADD(p_fold, t0);
       }
+      PROF_FLUSH(16, p_ww);
+      PROF_FLUSH(17, p_wr);
+      PROF_FLUSH(18, p_fold);
     }
-  } else if (warp == M + F + 1) {
+  } else if (role == M + F) {
     // ================================= writer ===============================
     for (int64_t b = 0; b < nb; ++b) {
       mbar_wait(&batch_done[b % kBatchBars], (unsigned)((b / kBatchBars) & 1));
@@ -392,13 +662,18 @@ __device__ __forceinline__ void sdp_producer(const SdpShape& S, const int64_t* _
   const int per = (jr + W - 1) / W;
   const int lo = min(jr, warp * per), hi = min(jr, lo + per);
   const int64_t nb = (S.n - S.a1 + 31) / 32;
+  PROF_DECL(p_wait);
+  PROF_DECL(p_fold);
   for (int64_t b = pid; b < nb; b += np) {
+    long long t0 = PROF_NOW();
     if (tid == 0) {
       const long long need = (long long)max(b + 1 - look, b + 1 - (int64_t)kRemSlots);
       while ((long long)ld_acquire_gpu(reinterpret_cast<const long long*>(RM.published)) < need)
         __nanosleep(128);
     }
     __syncthreads();
+    PROF_ADD(p_wait, t0);
+    t0 = PROF_NOW();
     const int64_t c = S.a1 + 32 * b + lane;
     if (lo < hi) {
       red[warp * 32 + lane] = fold_range<OP, T, true, int64_t, true>(T(0), false, out + c, obg, lo, hi);
@@ -415,6 +690,11 @@ __device__ __forceinline__ void sdp_producer(const SdpShape& S, const int64_t* _
       __syncwarp();
       if (lane == 0) st_release_gpu_i32(RM.ready + rs, (int)(b + 1));
     }
+    PROF_ADD(p_fold, t0);
+  }
+  if (warp == 0) {
+    PROF_FLUSH(24, p_wait);
+    PROF_FLUSH(25, p_fold);
   }
 }
 
@@ -444,7 +724,7 @@ __global__ void __launch_bounds__(1024, 1)
 // -----------------------------------------------------------------------------
 // Batched S-DP with a small a_1: one warp per instance runs every stage itself
 // -- offsets >= 32 straight from its private mirrored ring, offsets < 32
-// through chain_fold.  SMALL: a_1 < 32.
+// through chain_fold.  SMALL: a_1 < 64 (the first operand is assigned inside chain_fold).
 template <int OP, typename T, bool SMALL, bool ASSOC>
 __global__ void __launch_bounds__(256)
     sdp_batch_warp(const SdpShape S, int64_t batch, const int64_t* __restrict__ g_offsets,
@@ -477,25 +757,32 @@ __global__ void __launch_bounds__(256)
     o[i] = v;
   }
   __syncwarp();
-  int j32 = S.k;
-  uint32_t mask32 = 0;
-  for (int j = S.k - 1; j >= 0; --j) {
-    const int a = offs[j];
-    if (a >= 32) break;
-    j32 = j;
-    mask32 |= 1u << a;
-  }
-  const uint32_t bits = chain_bits(mask32, lane);
+  int jn = S.k;  // offsets[0, jn) >= 64 fold from the ring, the rest in chain_fold
+  while (jn > 0 && offs[jn - 1] < 64) --jn;
+  const ChainMasks cm = chain_masks(offs, S.k, lane);
+  constexpr bool kLA = !SMALL && ASSOC && !(OP == kModAdd && sizeof(T) == 8);
+  const LaMasks lm = la_masks(offs, S.k, lane);
+  T nxt = T(0);
   const int64_t nb = (n - a1 + 31) / 32;
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t c = a1 + 32 * b + lane;
     const uint32_t pos = ((uint32_t)c & (R - 1)) + R;
     T acc;
-    if (!SMALL) {
-      acc = fold_range<OP, T, ASSOC>(T(0), false, ring + pos, ob, 0, j32);
-      acc = chain_fold<OP, T, true>(acc, ring, pos, offs, j32, j32, S.k, bits, lane);
+    if (kLA) {
+      acc = fold_range<OP, T, ASSOC>(T(0), false, ring + pos, ob, 0, jn);
+      if (b == 0) {
+        bool h = true;
+        pre_steps<OP, T, true, ASSOC>(acc, h, ring + pos, cm.hi, cm.lo);
+      } else {
+        acc = SemiOp<OP, T>::apply(acc, nxt);
+      }
+      nxt = la_ring_group<OP, T>(ring + (((uint32_t)(c + 32) & (R - 1)) + R), lm.far);
+      LaSteps<OP, T, 1>::run(acc, nxt, lm);
+    } else if (!SMALL) {
+      acc = fold_range<OP, T, ASSOC>(T(0), false, ring + pos, ob, 0, jn);
+      acc = chain_fold<OP, T, true, ASSOC>(acc, ring, pos, cm);
     } else {
-      acc = chain_fold<OP, T, false>(T(0), ring, pos, offs, 0, 0, S.k, bits, lane);
+      acc = chain_fold<OP, T, false, ASSOC>(T(0), ring, pos, cm);
     }
     if (c < n) {
       ring[pos - R] = acc;
@@ -528,6 +815,30 @@ __global__ void sdp_chain_step_probe(int64_t batches, T seed, long long* cycles,
   }
   const long long t1 = clock64();
   if (lane == 0) *cycles = t1 - t0;
+  sink[lane] = acc;
+}
+
+// Isolated chain_fold timing with a real instance's masks (mode 0: full fold,
+// 1: shuffle chain only, 2: out-of-batch pre-steps only).  Cycles per batch.
+template <int OP, typename T>
+__global__ void sdp_chain_fold_probe(int64_t batches, uint32_t hi, uint32_t m32, int mode,
+                                     long long* cycles, T* sink) {
+  __shared__ T ring[256];
+  const int lane = threadIdx.x & 31;
+  for (int i = lane; i < 256; i += 32) ring[i] = (T)(i * 7 + 3);
+  __syncwarp();
+  ChainMasks m{hi, m32 & ~((2u << lane) - 1u), chain_bits(m32, lane)};
+  if (mode == 1) m.hi = m.lo = 0;
+  if (mode == 2) m.bits = 0;
+  T acc = (T)lane;
+  const long long t0 = clock64();
+  for (int64_t b = 0; b < batches; ++b) {
+    acc = chain_fold<OP, T, true, true>(acc, ring, 128 + lane, m);
+    ring[128 + lane] = acc;
+    __syncwarp();
+  }
+  const long long t1 = clock64();
+  if (lane == 0) *cycles = (t1 - t0) / batches;
   sink[lane] = acc;
 }
 

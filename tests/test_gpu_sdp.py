@@ -143,3 +143,20 @@ def test_multi_cta_shapes(gpu, oracle, ctas, warps, monkeypatch):
     monkeypatch.setenv("PIPEDP_SDP_REMOTE_WARPS", str(warps))
     offs, init = oracle.generate_sdp(60000, 1500, 8, False, 6000)
     _check(gpu, oracle, offs, init, 60000, "max")
+
+
+@pytest.mark.parametrize("op", OPS)
+def test_k1_large_a1_raw_copy(gpu, oracle, op):
+    # k = 1 with a_1 >= 64: the table is a raw periodic copy of init for every op
+    rng = np.random.default_rng(3)
+    init = rng.integers(-(2**62), 2**62, 100)
+    _check(gpu, oracle, [100], init, 1000, op)
+
+
+@pytest.mark.parametrize("op", OPS)
+def test_all_offsets_below_64_with_large_one(gpu, oracle, op):
+    # a_1 >= 64 but every other offset < 64: empty mid range, chain does the rest
+    offs = [200, 63, 40, 33, 32, 31, 17, 2, 1]
+    rng = np.random.default_rng(4)
+    init = rng.integers(0, 2**20, 200) if op != "saturating-add" else rng.integers(0, 5, 200)
+    _check(gpu, oracle, offs, init, 7000, op)
