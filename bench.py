@@ -1,0 +1,468 @@
+#!/usr/bin/env python
+"""bench.py -- pipedp-b200 benchmark (BASELINE.json metric: DP relaxations/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
+
+One process per GPU (torchrun for N > 1, NCCL only for the barrier and the
+max-over-ranks timing reduction; the data path has no collective).
+
+Workloads (BASELINE.json configs; inputs from the reference's own seeded
+generators, generate.cpp:21-60, restated bit-exactly in the C ABI):
+  c1   S-DP Fibonacci n=2^20, offsets {2,1}, saturating-add, init {1,1}
+  c2   S-DP n=2^24, k=1024, a_1=4096, min, seed 1           (DEFAULT, the headline)
+  c3   MCM n=1024, dims U[1,100], seed 1 (pipeline kernel; --mcm-kernel tournament for the paper's method)
+  c4   MCM n=8192, dims U[1,100], seed 1 (table in HBM)
+  c5a  65,536 x MCM n=64 (batch, sharded over ranks)
+  c5b  65,536 x S-DP n=2^16, k=64, min (batch, sharded over ranks)
+Single-instance workloads (c1-c4) cannot be split (every cell depends on its
+predecessors): at N > 1 every rank solves its own instance
+(seed 1 + rank), i.e. a batch of N independent instances, one per GPU -- weak
+scaling.  c5a/c5b shard a fixed batch of 65,536 instances -- strong scaling.
+
+A "step" is one solve of the workload on inputs already resident in HBM
+(`value`); `e2e` repeats it through the reference-facing C-ABI call with HOST
+buffers (H2D of offsets/init or dims and D2H of every table inside the timed
+region).  L2 (126 MB) is flushed by writing a 256 MiB buffer before every
+timed step.  The CPU baseline is the reference library itself
+(oracle/_ref, compiled from the reference sources) on the box's host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DP relaxations/sec (S-DP, MCM n=1024/8192) and % of roofline vs CPU ref"
+UNIT = "relaxations/s"
+
+WORKLOADS = {
+    "c1": "S-DP Fibonacci n=2^20 k=2 offsets{2,1} saturating-add init{1,1}",
+    "c2": "S-DP n=2^24 k=1024 a1=4096 min seed1",
+    "c3": "MCM n=1024 dims U[1,100] seed1 (+split table)",
+    "c4": "MCM n=8192 dims U[1,100] seed1 (+split table, table in HBM)",
+    "c5a": "batch 65536 x MCM n=64 dims U[1,100] (+split)",
+    "c5b": "batch 65536 x S-DP n=2^16 k=64 a1=128 min",
+}
+BATCH = {"c5a", "c5b"}
+
+
+def env_int(name, default):
+    v = os.environ.get(name)
+    return int(v) if v else default
+
+
+def load_json(path):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------- clocks ---
+class ClockSampler:
+    """nvidia-smi samples of SM clock and throttle reasons while running."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            f = [x.strip() for x in line.split(",")]
+            if len(f) == 6:
+                self.rows.append(f)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = sorted(float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit())
+        mx = max((float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()), default=None)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+# -------------------------------------------------------------- workloads ---
+class Single:
+    """One instance per rank (c1-c4), device-resident plan + buffers."""
+
+    def __init__(self, pd, torch, name, rank, dev, mcm_kernel):
+        self.pd, self.torch, self.name = pd, torch, name
+        seed = 1 + rank
+        self.seed = seed
+        self.dev = torch.device("cuda", dev)
+        if name in ("c1", "c2"):
+            if name == "c1":
+                self.inst = pd.SdpInstance(1 << 20, [2, 1], [1, 1], "saturating-add")
+            else:
+                self.inst = pd.generate_sdp(n=1 << 24, k=1024, op="min", seed=seed, a1_cap=4096)
+            i = self.inst
+            self.relax = (i.n - i.a1) * i.k
+            self.plan = pd.SdpPlan(1, i.n, i.k, i.a1, i.offsets, i.init, i.op, dev)
+            self.d_init = torch.tensor(list(map(int, i.init)), dtype=torch.int64, device=self.dev)
+            self.d_cells = torch.empty(i.n, dtype=torch.int64, device=self.dev)
+            self.out_bytes = i.n * 8
+            self.in_bytes = (i.k + i.a1) * 8
+            self.table_cells = i.n
+        else:
+            n = 1024 if name == "c3" else 8192
+            self.inst = pd.generate_mcm(n=n, seed=seed, dims_min=1, dims_max=100)
+            self.kernel = {"pipeline": pd.MCM_AUTO, "wavefront": pd.MCM_WAVEFRONT,
+                           "tournament": pd.MCM_TOURNAMENT}[mcm_kernel]
+            self.relax = (n ** 3 - n) // 6
+            self.plan = pd.McmPlan(1, n, self.inst.dims, self.kernel, dev)
+            size = pd.cell_count(n) + 1
+            self.d_cells = torch.empty(size, dtype=torch.int64, device=self.dev)
+            self.d_split = torch.empty(size, dtype=torch.int64, device=self.dev)
+            self.out_bytes = 2 * size * 8
+            self.in_bytes = (n + 1) * 8
+            self.table_cells = size
+
+    def execute(self, stream):
+        if self.name in ("c1", "c2"):
+            self.plan.execute(self.d_init.data_ptr(), self.d_cells.data_ptr(), stream.cuda_stream)
+        else:
+            self.plan.execute(self.d_cells.data_ptr(), self.d_split.data_ptr(), stream.cuda_stream)
+
+    def launches(self):
+        return max(1, self.plan.describe()[2])
+
+    def kernel_name(self):
+        return self.plan.describe()[0]
+
+    def value_bits(self):
+        return self.plan.describe()[1]
+
+    def e2e_step(self):
+        """The reference-facing call with host buffers (C ABI pipedp_*_solve)."""
+        pd = self.pd
+        if self.name in ("c1", "c2"):
+            t = pd.solve_sequential(self.inst)
+            return t.cells
+        t, split = pd.solve_mcm_with_split(self.inst, self.kernel)
+        return t.cells
+
+    def e2e_bytes(self):
+        return self.in_bytes, self.out_bytes
+
+    def digest(self):
+        return self.pd.table_digest(self.d_cells.cpu().numpy())
+
+
+class Batch:
+    def __init__(self, pd, torch, name, rank, world, dev):
+        from paper_2008_01938_b200 import batch as B
+        self.pd, self.torch, self.name = pd, torch, name
+        spec = B.McmBatchSpec() if name == "c5a" else B.SdpBatchSpec()
+        self.spec = spec
+        self.shard = B.BatchShard(spec, rank, world, dev)
+        self.relax = self.shard.relaxations()
+        n = spec.n
+        if name == "c5a":
+            self.out_bytes = 2 * self.shard.count * (pd.cell_count(n) + 1) * 8
+            self.in_bytes = self.shard.count * (n + 1) * 8
+        else:
+            self.out_bytes = self.shard.count * n * 8
+            self.in_bytes = self.shard.count * (spec.k + self.shard.a1) * 8
+
+    def execute(self, stream):
+        self.shard.execute(stream)
+
+    def launches(self):
+        return self.shard.launches_per_execute()
+
+    def kernel_name(self):
+        return self.shard.plan.describe()[0]
+
+    def value_bits(self):
+        return self.shard.plan.describe()[1]
+
+    def e2e_step(self):
+        import numpy as np
+        pd, s = self.pd, self.shard
+        L = pd.lib()
+        if self.name == "c5b":
+            cells = np.empty(s.count * self.spec.n, dtype=np.int64)
+            pd._check(L.pipedp_sdp_solve_batch(s.count, self.spec.n, self.spec.k, s.a1,
+                                               pd._p(s.h_offsets.reshape(-1)), pd._p(s.h_init.reshape(-1)),
+                                               0, pd._p(cells), s.device))
+            return cells
+        size = s.count * (pd.cell_count(self.spec.n) + 1)
+        cells = np.empty(size, dtype=np.int64)
+        split = np.empty(size, dtype=np.int64)
+        pd._check(L.pipedp_mcm_solve_batch(s.count, self.spec.n, pd._p(s.h_dims.reshape(-1)),
+                                           pd._p(cells), pd._p(split), s.device))
+        return cells
+
+    def e2e_bytes(self):
+        return self.in_bytes, self.out_bytes
+
+
+# ----------------------------------------------------------- CPU baselines ---
+def cpu_reference_sample(name, threads, steps=1):
+    """The reference library (oracle/_ref) on a bounded sample of the workload.
+    Returns (relax/s, cores, kind, sample description, seconds)."""
+    import numpy as np
+    from concurrent.futures import ThreadPoolExecutor
+    from oracle import pyoracle
+    ref = pyoracle.load_ref()
+    kind = "reference"
+    if ref is None:  # reference sources absent at build time: the C restatement
+        ref, kind = pyoracle.load_c(), "port"
+    jobs = []  # (callable, relaxations)
+    if name == "c1":
+        reps = 100
+        jobs = [(lambda: ref.sdp_solve([2, 1], [1, 1], 1 << 20, "saturating-add"), (2**20 - 2) * 2)] * reps
+        sample = f"{reps} x full c1 instance, solve_sequential (sdp.cpp:84)"
+        threads = 1
+    elif name == "c2":
+        offs, init = ref.generate_sdp(1 << 24, 1024, 1, False, 4096)
+        n = 1 << 23
+        jobs = [(lambda: ref.sdp_solve(offs, init, n, "min"), (n - 4096) * 1024)]
+        sample = "first 2^23 cells of the c2 instance (same offsets/init), solve_sequential (sdp.cpp:84), 1 thread"
+        threads = 1
+    elif name in ("c3", "c4"):
+        n = 1024 if name == "c3" else 1536
+        dims = ref.generate_mcm(n, 1, 1, 100)
+        jobs = [(lambda: ref.mcm_solve(dims), (n**3 - n) // 6)]
+        sample = (f"MCM n={n} seed 1 dims U[1,100], solve_mcm_sequential with split (mcm.cpp:85), 1 thread"
+                  + ("; n=8192 takes ~48 min, so n=1536 stands in" if name == "c4" else ""))
+        threads = 1
+    elif name == "c5a":
+        cnt = 4096
+        dims = [ref.generate_mcm(64, i, 1, 100) for i in range(cnt)]
+        jobs = [((lambda d=d: ref.mcm_solve(d)), (64**3 - 64) // 6) for d in dims]
+        sample = f"{cnt} of the 65,536 c5a instances, solve_mcm_sequential, {threads}-thread pool"
+    else:
+        cnt = 512
+        insts = [ref.generate_sdp(1 << 16, 64, i, False, 0) for i in range(cnt)]
+        jobs = [((lambda o=o, i=i: ref.sdp_solve(o, i, 1 << 16, "min")), ((1 << 16) - 128) * 64) for o, i in insts]
+        sample = f"{cnt} of the 65,536 c5b instances, solve_sequential, {threads}-thread pool"
+    relax = sum(r for _, r in jobs)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        if threads == 1:
+            for f, _ in jobs:
+                f()
+        else:
+            with ThreadPoolExecutor(threads) as ex:  # ctypes releases the GIL
+                list(ex.map(lambda j: j[0](), jobs))
+    dt = time.perf_counter() - t0
+    return relax * steps / dt, threads, kind, sample, dt
+
+
+def traffic_for(name):
+    """dram bytes per launch of the dominant kernel from the committed ncu
+    --set full summary (profiles/ncu_summary.json), or None."""
+    s = load_json(os.path.join(ROOT, "profiles", "ncu_summary.json")) or {}
+    e = s.get(name)
+    return e.get("dram_bytes_per_launch") if isinstance(e, dict) else None
+
+
+# --------------------------------------------------------------------- main ---
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--mcm-kernel", default="pipeline", choices=["pipeline", "wavefront", "tournament"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=None)
+    args = ap.parse_args()
+
+    world = env_int("WORLD_SIZE", 1)
+    rank = env_int("RANK", 0)
+    local = env_int("LOCAL_RANK", 0)
+    name = args.workload
+    single = name not in BATCH
+    config = {"workload": f"{name}: {WORKLOADS[name]}", "n_instances": world if single else 65536,
+              "parallelism": (f"replicas{world}" if single else f"shard{world}"),
+              "l2": "flushed (256 MiB write) before every timed step"}
+    if name in ("c3", "c4"):
+        config["mcm_kernel"] = args.mcm_kernel
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        import os as _os
+        cores = _os.cpu_count() or 1
+        thr = 1 if single else cores
+        cpu_reference_sample(name, thr, 1)  # warm-up sample
+        v, thr, kind, sample, dt = cpu_reference_sample(name, thr, max(1, args.steps))
+        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": dt * 1e3 / max(1, args.steps),
+                "higher_is_better": True, "scaling": "weak" if single else "strong",
+                "vs_baseline": None, "dtype": "int64", "data": "synthetic (reference generators)",
+                "config": config, "impl": "reference",
+                "cpu_baseline": {"value": v, "unit": UNIT, "cores": thr, "kind": kind, "sample": sample},
+                "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import paper_2008_01938_b200 as pd
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    W = Batch(pd, torch, name, rank, world, local) if not single else Single(pd, torch, name, rank, local,
+                                                                               args.mcm_kernel)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(max(args.warmup, 0)):
+        flush.zero_()
+        W.execute(stream)
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for e0, e1 in ev:
+            flush.zero_()
+            e0.record(stream)
+            W.execute(stream)
+            e1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    kernel_ms = sum(step_ms)
+    kernel_ms_max = max_over_ranks(kernel_ms)
+    relax_total = sum_over_ranks(float(W.relax))
+    value = relax_total * K / (kernel_ms_max / 1e3)
+
+    # parity spot check of the benchmarked output (rank 0, seed-1 instance)
+    parity = None
+    if rank == 0 and single:
+        golden = load_json(os.path.join(ROOT, "tests", "golden", "golden.json")) or {}
+        want = {"c1": golden.get("configs", {}).get("c1_saturating-add", {}).get("digest"),
+                "c2": golden.get("configs", {}).get("c2", {}).get("digest"),
+                "c3": "9e31907a82260f66", "c4": "cc41fd2d4975b51b"}.get(name)
+        got = f"{W.digest():016x}"
+        parity = {"cells_digest": got, "golden": want, "match": (got == want) if want else None}
+
+    # end to end through the reference-facing C ABI with host buffers
+    ek = args.e2e_steps if args.e2e_steps is not None else min(K, 3)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(ek):
+        W.e2e_step()
+    e2e_s = max_over_ranks(time.perf_counter() - t0)
+    h2d, d2h = W.e2e_bytes()
+    e2e = {"value": relax_total * ek / e2e_s if ek else None, "unit": UNIT,
+           "h2d_bytes_per_step": int(sum_over_ranks(h2d)), "d2h_bytes_per_step": int(sum_over_ranks(d2h)),
+           "steps": ek, "ms_per_step": e2e_s * 1e3 / max(ek, 1),
+           "call": "pipedp_sdp_solve / pipedp_mcm_solve (C ABI, host buffers)" if single
+           else "pipedp_sdp_solve_batch / pipedp_mcm_solve_batch (C ABI, host buffers)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
+    hbm_peak = peaks.get("hbm_gbs")
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (burst copy)" if hbm_peak else "fallback 6650 GB/s (B200_PROFILING.md)"
+    hbm_peak = hbm_peak or 6650.0
+    avg_ms = kernel_ms / K
+    alg_bytes = W.in_bytes + W.out_bytes
+    achieved = alg_bytes / (avg_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                "frac": achieved / hbm_peak, "traffic": traffic_for(name), "peak_source": peak_src,
+                "kernel": W.kernel_name(), "algorithmic_bytes_per_launch": alg_bytes,
+                "avg_launch_ms": avg_ms}
+    extra = {}
+    if name in ("c1", "c2"):
+        i = W.inst
+        bits = W.value_bits()
+        op_ns, op_cyc = pd.op_latency_ns(i.op, bits, local)
+        hand_ns, _ = pd.chain_step_ns(i.op, bits, local) if (i.op, bits) != ("saturating-add", 32) else (None, None)
+        steps = i.n - i.a1  # a_k = 1: one cell per step
+        floor_ms = steps * op_ns / 1e6
+        extra["chain_roofline"] = {
+            "definition": "(n - a_1) dependent steps x latency of one dependent (x) in a register chain",
+            "steps": steps, "t_op_ns": op_ns, "t_op_cycles": op_cyc, "floor_ms": floor_ms,
+            "achieved_ms": avg_ms, "frac": floor_ms / avg_ms,
+            "t_warp_handoff_ns": hand_ns, "value_bits": bits}
+    if name in ("c3", "c4"):
+        n = W.inst.n
+        extra["mcm_steps"] = {"cells": n * (n - 1) // 2, "ns_per_cell": avg_ms * 1e6 / (n * (n - 1) // 2),
+                              "diagonals": n - 1, "us_per_diagonal": avg_ms * 1e3 / (n - 1)}
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        v, thr, kind, sample, _ = cpu_reference_sample(name, 1 if single else cores, 1)
+        cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": kind, "sample": sample}
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+            "warmup": args.warmup, "ms_per_step": kernel_ms_max / K, "higher_is_better": True,
+            "scaling": "weak" if single else "strong", "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic (the reference's seeded generators, generate.cpp:21-60)",
+            "config": config, "e2e": e2e, "gpu_launches": W.launches() * K,
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
+            "kernel_value_bits": W.value_bits(), "parity": parity, "step_ms": step_ms, **extra}
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

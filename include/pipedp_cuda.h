@@ -79,6 +79,15 @@ int32_t pipedp_generate_sdp(int64_t n, int64_t k, int32_t op, uint64_t seed, int
 /* generate_mcm -- generate.cpp:49-60 (dims_out: n+1) */
 int32_t pipedp_generate_mcm(int64_t n, uint64_t seed, int64_t dims_min, int64_t dims_max,
                             int64_t* dims_out);
+/* Batched generators for the batch driver: instance i = generate_* with seed
+ * seed0 + i.  S-DP: offsets_out [count*k], init_out [count*a_1] (a_1 = a1_cap,
+ * 2k when a1_cap == 0, or k when consecutive; returned in *a1_out).
+ * MCM: dims_out [count*(n+1)]. */
+int32_t pipedp_generate_sdp_batch(int64_t n, int64_t k, uint64_t seed0, int64_t count,
+                                  int32_t consecutive, int64_t a1_cap, int64_t* offsets_out,
+                                  int64_t* init_out, int64_t* a1_out);
+int32_t pipedp_generate_mcm_batch(int64_t n, uint64_t seed0, int64_t count, int64_t dims_min,
+                                  int64_t dims_max, int64_t* dims_out);
 
 /* ---- S-DP, host buffers ---------------------------------------------------
  * Replaces the table computation of solve_sequential (sdp.cpp:84-89),
@@ -151,6 +160,11 @@ int32_t pipedp_digest_device(const int64_t* d_tables, int64_t count, int64_t nta
  * the S-DP chain warp for `op` at `value_bits`. */
 int32_t pipedp_chain_step_ns(int32_t op, int32_t value_bits, int32_t device, double* ns_out,
                              double* sm_clock_mhz_out);
+
+/* Hardware floor of the S-DP dependency chain: latency of one dependent (x)
+ * at `value_bits` in a single-thread register chain (ns and SM cycles). */
+int32_t pipedp_op_latency_ns(int32_t op, int32_t value_bits, int32_t device, double* ns_out,
+                             double* cycles_out);
 
 /* Role-level cycle counters of the profiling build (-DPIPEDP_PROFILE,
  * tools/build_profile.sh); returns PIPEDP_ERR_UNSUPPORTED otherwise. */

@@ -50,7 +50,8 @@ EXPORTS = (
     "pipedp_mcm_solve", "pipedp_mcm_pipeline", "pipedp_mcm_solve_batch",
     "pipedp_mcm_plan_create", "pipedp_mcm_plan_execute", "pipedp_mcm_plan_describe",
     "pipedp_mcm_plan_destroy", "pipedp_digest_device", "pipedp_chain_step_ns",
-    "pipedp_profile_read",
+    "pipedp_profile_read", "pipedp_generate_sdp_batch", "pipedp_generate_mcm_batch",
+    "pipedp_op_latency_ns",
 )
 
 
@@ -96,6 +97,10 @@ def lib():
     L.pipedp_generate_sdp.argtypes = [C.c_int64, C.c_int64, C.c_int32, C.c_uint64, C.c_int32,
                                       C.c_int64, _i64p, _i64p, C.c_int64, _i64p]
     L.pipedp_generate_mcm.argtypes = [C.c_int64, C.c_uint64, C.c_int64, C.c_int64, _i64p]
+    L.pipedp_generate_sdp_batch.argtypes = [C.c_int64, C.c_int64, C.c_uint64, C.c_int64, C.c_int32,
+                                            C.c_int64, _i64p, _i64p, _i64p]
+    L.pipedp_generate_mcm_batch.argtypes = [C.c_int64, C.c_uint64, C.c_int64, C.c_int64, C.c_int64,
+                                            _i64p]
     L.pipedp_sdp_solve.argtypes = [_i64p, C.c_int64, _i64p, C.c_int64, C.c_int64, C.c_int32,
                                    _i64p, _u8p]
     L.pipedp_sdp_solve_batch.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int64, _i64p, _i64p,
@@ -117,6 +122,8 @@ def lib():
     L.pipedp_mcm_plan_destroy.argtypes = [C.c_void_p]
     L.pipedp_digest_device.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
     L.pipedp_chain_step_ns.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double),
+                                       C.POINTER(C.c_double)]
+    L.pipedp_op_latency_ns.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]
     _lib = L
     return L
@@ -313,6 +320,18 @@ def generate_sdp(n=64, k=4, op="min", seed=0, consecutive=False, a1_cap=0) -> Sd
     return SdpInstance(n, offs, init[: a1.value].copy(), op)
 
 
+def generate_sdp_batch(n, k, seed0, count, consecutive=False, a1_cap=0):
+    """Instances generate_sdp(seed = seed0 + i), i < count, as SoA arrays
+    (offsets [count, k], init [count, a_1])."""
+    a1 = k if consecutive else (a1_cap if a1_cap > 0 else 2 * k)
+    offs = np.empty((count, k), dtype=np.int64)
+    init = np.empty((count, a1), dtype=np.int64)
+    got = C.c_int64()
+    _check(lib().pipedp_generate_sdp_batch(n, k, seed0, count, int(consecutive), a1_cap, _p(offs),
+                                           _p(init), C.byref(got)))
+    return offs, init
+
+
 # -------------------------------------------------------------------- MCM ----
 def cell_count(n: int) -> int:
     return n * (n + 1) // 2
@@ -410,6 +429,13 @@ def generate_mcm(n=8, seed=0, dims_min=1, dims_max=50) -> McmInstance:
     return McmInstance(dims)
 
 
+def generate_mcm_batch(n, seed0, count, dims_min=1, dims_max=100):
+    """Instances generate_mcm(seed = seed0 + i) as dims [count, n+1]."""
+    dims = np.empty((count, n + 1), dtype=np.int64)
+    _check(lib().pipedp_generate_mcm_batch(n, seed0, count, dims_min, dims_max, _p(dims)))
+    return dims
+
+
 # ----------------------------------------------------- device-resident plans --
 class SdpPlan:
     """Device-resident S-DP execution (C ABI pipedp_sdp_plan_*).  Host copies of
@@ -495,3 +521,10 @@ def chain_step_ns(op="min", value_bits=32, device=-1):
     ns, mhz = C.c_double(), C.c_double()
     _check(lib().pipedp_chain_step_ns(_op_index(op), value_bits, device, C.byref(ns), C.byref(mhz)))
     return ns.value, mhz.value
+
+
+def op_latency_ns(op="min", value_bits=32, device=-1):
+    """(ns, SM cycles) of one dependent (x) -- the dependency-chain floor per cell."""
+    ns, cyc = C.c_double(), C.c_double()
+    _check(lib().pipedp_op_latency_ns(_op_index(op), value_bits, device, C.byref(ns), C.byref(cyc)))
+    return ns.value, cyc.value

@@ -14,6 +14,7 @@
 #include <mutex>
 #include <random>
 #include <string>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
@@ -624,6 +625,50 @@ int32_t pipedp_generate_mcm(int64_t n, uint64_t seed, int64_t dims_min, int64_t 
   return validate_mcm(dims_out, n + 1);
 }
 
+// Batched generators (harness for the batch driver): instance i is exactly
+// generate_sdp / generate_mcm with seed0 + i; every S-DP instance has a_1 = cap
+// (or k when consecutive), so the outputs are dense SoA blocks.
+int32_t pipedp_generate_sdp_batch(int64_t n, int64_t k, uint64_t seed0, int64_t count,
+                                  int32_t consecutive, int64_t a1_cap, int64_t* offsets_out,
+                                  int64_t* init_out, int64_t* a1_out) {
+  if (count < 0 || k < 1) return fail(PIPEDP_E_INVALID_PARAMS, "bad batch shape");
+  const int64_t a1 = consecutive ? k : (a1_cap > 0 ? a1_cap : 2 * k);
+  if (a1_out) *a1_out = a1;
+  const int nt = (int)std::max<int64_t>(1, std::min<int64_t>(count / 64 + 1, 32));
+  std::vector<int32_t> rc(nt, PIPEDP_OK);
+  std::vector<std::string> err(nt);
+  auto work = [&](int t) {
+    for (int64_t i = t; i < count; i += nt) {
+      int64_t got = 0;
+      const int r = pipedp_generate_sdp(n, k, 0, seed0 + (uint64_t)i, consecutive, a1_cap,
+                                        offsets_out + i * k, init_out + i * a1, a1, &got);
+      if (r != PIPEDP_OK) {
+        rc[t] = r;
+        err[t] = g_last_error;
+        return;
+      }
+    }
+  };
+  std::vector<std::thread> th;
+  for (int t = 1; t < nt; ++t) th.emplace_back(work, t);
+  work(0);
+  for (auto& x : th) x.join();
+  for (int t = 0; t < nt; ++t)
+    if (rc[t] != PIPEDP_OK) {
+      g_last_error = err[t];
+      return rc[t];
+    }
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_generate_mcm_batch(int64_t n, uint64_t seed0, int64_t count, int64_t dims_min,
+                                  int64_t dims_max, int64_t* dims_out) {
+  if (count < 0) return fail(PIPEDP_E_INVALID_PARAMS, "bad batch shape");
+  for (int64_t i = 0; i < count; ++i)
+    TRY(pipedp_generate_mcm(n, seed0 + (uint64_t)i, dims_min, dims_max, dims_out + i * (n + 1)));
+  return PIPEDP_OK;
+}
+
 // ------------------------------------------------------------- S-DP ---
 int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
                                const int64_t* h_offsets, const int64_t* h_init, int32_t op,
@@ -1011,6 +1056,60 @@ int32_t pipedp_chain_step_ns(int32_t op, int32_t value_bits, int32_t device, dou
   const double steps = (double)batches * 32.0;
   if (ns_out) *ns_out = ms * 1e6 / steps;
   if (mhz_out) *mhz_out = (double)cyc / (ms * 1e3);
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_op_latency_ns(int32_t op, int32_t value_bits, int32_t device, double* ns_out,
+                             double* cycles_out) {
+  TRY(select_device(device));
+  Scope sc;
+  TRY(sc.init());
+  long long* d_cyc = nullptr;
+  int64_t* d_vals = nullptr;
+  int64_t* d_sink = nullptr;
+  TRY(sc.alloc(&d_cyc, 1));
+  TRY(sc.alloc(&d_vals, 16));
+  TRY(sc.alloc(&d_sink, 1));
+  // operands that keep every op "live": small positive values (no saturation,
+  // mod-add stays in range, min/max alternate)
+  const int64_t h64[9] = {17, 3, 29, 5, 11, 23, 7, 13, 19};
+  const int32_t h32[9] = {17, 3, 29, 5, 11, 23, 7, 13, 19};
+  if (value_bits == 32) CK(cudaMemcpy(d_vals, h32, sizeof h32, cudaMemcpyHostToDevice));
+  else CK(cudaMemcpy(d_vals, h64, sizeof h64, cudaMemcpyHostToDevice));
+  const int64_t iters = 1 << 16;
+  cudaEvent_t e0, e1;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  auto run = [&]() -> int {
+    CK(cudaEventRecord(e0, sc.stream));
+    int32_t* v32 = reinterpret_cast<int32_t*>(d_vals);
+    int32_t* s32 = reinterpret_cast<int32_t*>(d_sink);
+    switch (op * 100 + value_bits) {
+      case 32: op_latency_probe<kMin, int32_t><<<1, 1, 0, sc.stream>>>(iters, v32, d_cyc, s32); break;
+      case 64: op_latency_probe<kMin, int64_t><<<1, 1, 0, sc.stream>>>(iters, d_vals, d_cyc, d_sink); break;
+      case 132: op_latency_probe<kMax, int32_t><<<1, 1, 0, sc.stream>>>(iters, v32, d_cyc, s32); break;
+      case 164: op_latency_probe<kMax, int64_t><<<1, 1, 0, sc.stream>>>(iters, d_vals, d_cyc, d_sink); break;
+      case 264: op_latency_probe<kSatAdd, int64_t><<<1, 1, 0, sc.stream>>>(iters, d_vals, d_cyc, d_sink); break;
+      case 332: op_latency_probe<kModAdd, int32_t><<<1, 1, 0, sc.stream>>>(iters, v32, d_cyc, s32); break;
+      case 364: op_latency_probe<kModAdd, int64_t><<<1, 1, 0, sc.stream>>>(iters, d_vals, d_cyc, d_sink); break;
+      default: return fail(PIPEDP_E_INVALID_PARAMS, "no latency probe for op %d at %d bits", op, value_bits);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(e1, sc.stream));
+    CK(cudaEventSynchronize(e1));
+    return PIPEDP_OK;
+  };
+  TRY(run());
+  TRY(run());
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, e0, e1));
+  long long cyc = 0;
+  CK(cudaMemcpy(&cyc, d_cyc, sizeof cyc, cudaMemcpyDeviceToHost));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  const double ops = (double)iters * 8.0;
+  if (ns_out) *ns_out = ms * 1e6 / ops;
+  if (cycles_out) *cycles_out = (double)cyc / ops;
   return PIPEDP_OK;
 }
 

@@ -818,6 +818,38 @@ __global__ void sdp_chain_step_probe(int64_t batches, T seed, long long* cycles,
   sink[lane] = acc;
 }
 
+// Hardware floor of the dependency chain: one thread, a loop-carried chain of
+// dependent (x) (the empty asm pins x to a register after every op so the
+// compiler cannot reassociate the chain).  Whatever the schedule, cell i of
+// an instance with a_k = 1 needs at least one (x) that consumes cell i-1, so
+// (n - a_1) x this latency bounds every S-DP kernel from below.
+template <typename T>
+__device__ __forceinline__ void opaque(T& x);
+template <>
+__device__ __forceinline__ void opaque<int32_t>(int32_t& x) { asm volatile("" : "+r"(x)); }
+template <>
+__device__ __forceinline__ void opaque<int64_t>(int64_t& x) { asm volatile("" : "+l"(x)); }
+
+template <int OP, typename T>
+__global__ void op_latency_probe(int64_t iters, const T* vals, long long* cycles, T* sink) {
+  using O = SemiOp<OP, T>;
+  T v[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) v[j] = vals[j];
+  T x = vals[8];
+  const long long t0 = clock64();
+  for (int64_t it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      x = O::apply(x, v[j]);
+      opaque(x);
+    }
+  }
+  const long long t1 = clock64();
+  *cycles = t1 - t0;
+  *sink = x;
+}
+
 // Isolated chain_fold timing with a real instance's masks (mode 0: full fold,
 // 1: shuffle chain only, 2: out-of-batch pre-steps only).  Cycles per batch.
 template <int OP, typename T>
