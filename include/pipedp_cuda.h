@@ -134,6 +134,10 @@ int32_t pipedp_mcm_solve(const int64_t* dims, int64_t dims_len, int32_t kernel,
 int32_t pipedp_mcm_pipeline(const int64_t* dims, int64_t dims_len, int32_t mode,
                             int64_t* cells_out, uint8_t* filled_out, int64_t* steps_out,
                             int64_t* stall_iterations_out);
+/* solve_mcm_bruteforce (mcm.cpp:130-138): the reference's independent oracle
+ * (enumeration of every parenthesisation, n <= 12, else TooLargeForBruteForce),
+ * run on the device. */
+int32_t pipedp_mcm_bruteforce(const int64_t* dims, int64_t dims_len, int64_t* out);
 /* batch of independent MCM instances of equal n (dims [batch*(n+1)],
  * cells/split [batch*(cell_count(n)+1)]) */
 int32_t pipedp_mcm_solve_batch(int64_t batch, int64_t n, const int64_t* dims, int64_t* cells_out,

@@ -51,7 +51,7 @@ EXPORTS = (
     "pipedp_mcm_plan_create", "pipedp_mcm_plan_execute", "pipedp_mcm_plan_describe",
     "pipedp_mcm_plan_destroy", "pipedp_digest_device", "pipedp_chain_step_ns",
     "pipedp_profile_read", "pipedp_generate_sdp_batch", "pipedp_generate_mcm_batch",
-    "pipedp_op_latency_ns",
+    "pipedp_op_latency_ns", "pipedp_mcm_bruteforce",
 )
 
 
@@ -125,6 +125,7 @@ def lib():
                                        C.POINTER(C.c_double)]
     L.pipedp_op_latency_ns.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]
+    L.pipedp_mcm_bruteforce.argtypes = [_i64p, C.c_int64, _i64p]
     _lib = L
     return L
 
@@ -385,6 +386,15 @@ def solve_mcm_with_split(inst: McmInstance, kernel: int = MCM_AUTO):
 
 def solve_mcm_tournament(inst: McmInstance):
     return _mcm(inst, MCM_TOURNAMENT, True)
+
+
+def solve_mcm_bruteforce(inst: McmInstance) -> int:
+    """solve_mcm_bruteforce (mcm.cpp:130-138): enumeration over every
+    parenthesisation (n <= 12), on the device."""
+    d = _a64(inst.dims)
+    out = C.c_int64()
+    _check(lib().pipedp_mcm_bruteforce(_p(d), len(d), C.byref(out)))
+    return out.value
 
 
 def solve_mcm_pipeline(inst: McmInstance, mode: str = PAPER_LITERAL) -> McmPipelineResult:

@@ -946,6 +946,25 @@ int32_t pipedp_mcm_pipeline(const int64_t* dims, int64_t dims_len, int32_t mode,
   return PIPEDP_OK;
 }
 
+int32_t pipedp_mcm_bruteforce(const int64_t* dims, int64_t dims_len, int64_t* out) {
+  TRY(validate_mcm(dims, dims_len));
+  const int64_t n = dims_len - 1;
+  if (n > 12)
+    return fail(PIPEDP_E_TOO_LARGE_FOR_BRUTE, "n=%lld exceeds the enumeration limit of 12", (long long)n);
+  TRY(select_device(-1));
+  Scope sc;
+  TRY(sc.init());
+  int64_t *d_p = nullptr, *d_out = nullptr;
+  TRY(sc.alloc(&d_p, n + 1));
+  TRY(sc.alloc(&d_out, 1));
+  CK(cudaMemcpyAsync(d_p, dims, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, sc.stream));
+  mcm_bruteforce_kernel<<<1, 32, 0, sc.stream>>>(d_p, (int)n, d_out);
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(out, d_out, sizeof(int64_t), cudaMemcpyDeviceToHost, sc.stream));
+  CK(cudaStreamSynchronize(sc.stream));
+  return PIPEDP_OK;
+}
+
 // ------------------------------------------------------------ utilities ---
 }  // extern "C"
 

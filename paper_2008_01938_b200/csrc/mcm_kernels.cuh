@@ -386,3 +386,25 @@ __global__ void __launch_bounds__(1024, 1)
 }
 
 }  // namespace pipedp_dev
+
+namespace pipedp_dev {
+
+// -----------------------------------------------------------------------------
+// solve_mcm_bruteforce (mcm.cpp:112-138): the reference's independent oracle,
+// minimum over every full parenthesisation by direct recursion on splits
+// (exponential on purpose, n <= 12, never touches a table).  One thread.
+__device__ int64_t mcm_enumerate(const int64_t* __restrict__ p, int r, int c) {
+  if (r == c) return 0;
+  int64_t best = INT64_MAX;
+  for (int s = r; s < c; ++s) {
+    const int64_t cost = mcm_enumerate(p, r, s) + mcm_enumerate(p, s + 1, c) + p[r - 1] * p[s] * p[c];
+    best = cost < best ? cost : best;
+  }
+  return best;
+}
+
+__global__ void mcm_bruteforce_kernel(const int64_t* __restrict__ p, int n, int64_t* out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) *out = mcm_enumerate(p, 1, n);
+}
+
+}  // namespace pipedp_dev

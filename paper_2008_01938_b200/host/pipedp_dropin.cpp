@@ -275,6 +275,12 @@ SolutionTable solve_mcm_sequential(const McmInstance& inst, std::vector<std::int
   return mcm_solve(inst, split, PIPEDP_MCM_AUTO);
 }
 
+std::int64_t solve_mcm_bruteforce(const McmInstance& inst) {  // mcm.cpp:130-138
+  std::int64_t out = 0;
+  check(pipedp_mcm_bruteforce(inst.dims.data(), static_cast<std::int64_t>(inst.dims.size()), &out));
+  return out;
+}
+
 SolutionTable solve_mcm_tournament(const McmInstance& inst, std::vector<std::int64_t>* split) {
   return mcm_solve(inst, split, PIPEDP_MCM_TOURNAMENT);
 }
