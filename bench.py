@@ -142,7 +142,7 @@ class Single:
             n = 1024 if name == "c3" else 8192
             self.inst = pd.generate_mcm(n=n, seed=seed, dims_min=1, dims_max=100)
             self.kernel = {"pipeline": pd.MCM_AUTO, "wavefront": pd.MCM_WAVEFRONT,
-                           "tournament": pd.MCM_TOURNAMENT}[mcm_kernel]
+                           "tournament": pd.MCM_TOURNAMENT, "tiled": pd.MCM_TILED}[mcm_kernel]
             self.relax = (n ** 3 - n) // 6
             self.plan = pd.McmPlan(1, n, self.inst.dims, self.kernel, dev)
             size = pd.cell_count(n) + 1
@@ -301,7 +301,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mcm-kernel", default="pipeline", choices=["pipeline", "wavefront", "tournament"])
+    ap.add_argument("--mcm-kernel", default="pipeline", choices=["pipeline", "tiled", "wavefront", "tournament"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()

@@ -51,10 +51,11 @@ enum { PIPEDP_OP_MIN = 0, PIPEDP_OP_MAX = 1, PIPEDP_OP_SATURATING_ADD = 2, PIPED
 
 /* MCM kernels */
 enum {
-  PIPEDP_MCM_AUTO = 0,       /* shared-memory CTA for small n, HBM wavefront otherwise */
+  PIPEDP_MCM_AUTO = 0,       /* shared-memory CTA for small n / batches, tiled pipeline otherwise */
   PIPEDP_MCM_WAVEFRONT = 1,  /* multi-SM dataflow pipeline, table in HBM */
   PIPEDP_MCM_SMEM = 2,       /* one CTA, table in shared memory (small n) */
-  PIPEDP_MCM_TOURNAMENT = 3  /* the paper's O(n^2 log n) comparison kernel */
+  PIPEDP_MCM_TOURNAMENT = 3, /* the paper's O(n^2 log n) comparison kernel */
+  PIPEDP_MCM_TILED = 4       /* blocked pipeline: 64x64 tiles, TMA-staged, split-K far terms */
 };
 
 /* McmMode (mcm_pipeline.hpp:88) */

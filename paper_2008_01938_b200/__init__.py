@@ -38,7 +38,7 @@ ERRC = [
 ]
 OPS = ("min", "max", "saturating-add", "modular-add")  # OpKind order, semigroup.hpp:13
 
-MCM_AUTO, MCM_WAVEFRONT, MCM_SMEM, MCM_TOURNAMENT = 0, 1, 2, 3
+MCM_AUTO, MCM_WAVEFRONT, MCM_SMEM, MCM_TOURNAMENT, MCM_TILED = 0, 1, 2, 3, 4
 PAPER_LITERAL, STALL_ON_HAZARD = "paper_literal", "stall_on_hazard"
 
 # C ABI exports declared in include/pipedp_cuda.h (checked by tests/test_host.py)

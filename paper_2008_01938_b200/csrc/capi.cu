@@ -20,6 +20,7 @@
 
 #include "../../include/pipedp_cuda.h"
 #include "mcm_kernels.cuh"
+#include "mcm_tiled.cuh"
 #include "sdp_kernels.cuh"
 
 using namespace pipedp_dev;
@@ -445,7 +446,14 @@ int plan_mcm(int64_t batch, int64_t n, const int64_t* dims, int kernel, McmDispa
     const bool fits = need <= kSmemBudget;
     kernel = (fits && (batch > 1 || n <= 160)) ? PIPEDP_MCM_SMEM : PIPEDP_MCM_WAVEFRONT;
     if (!fits && batch > 1) kernel = PIPEDP_MCM_WAVEFRONT;
+    if (kernel == PIPEDP_MCM_WAVEFRONT && batch == 1 && d->bits == 32 &&
+        env_int("PIPEDP_MCM_TILED", 1) != 0)
+      kernel = PIPEDP_MCM_TILED;
   }
+  if (kernel == PIPEDP_MCM_TILED && batch > 1)
+    return fail(PIPEDP_E_INVALID_PARAMS, "the tiled kernel solves one instance at a time");
+  if (kernel == PIPEDP_MCM_TILED && (n + kT - 1) / kT >= 65535)
+    return fail(PIPEDP_ERR_UNSUPPORTED, "n=%lld too large for the tiled MCM kernel", (long long)n);
   if (kernel == PIPEDP_MCM_SMEM && d->smem64 > 227 * 1024 && d->smem32 > 227 * 1024)
     return fail(PIPEDP_ERR_UNSUPPORTED, "n=%lld too large for the shared-memory MCM kernel",
                 (long long)n);
@@ -454,7 +462,7 @@ int plan_mcm(int64_t batch, int64_t n, const int64_t* dims, int kernel, McmDispa
                 (long long)n);
   if ((kernel == PIPEDP_MCM_TOURNAMENT) && batch > 1)
     return fail(PIPEDP_E_INVALID_PARAMS, "the tournament kernel solves one instance at a time");
-  if (kernel < PIPEDP_MCM_AUTO || kernel > PIPEDP_MCM_TOURNAMENT)
+  if (kernel < PIPEDP_MCM_AUTO || kernel > PIPEDP_MCM_TILED)
     return fail(PIPEDP_E_INVALID_PARAMS, "unknown MCM kernel %d", kernel);
   d->kernel = kernel;
   d->threads = n <= 64 ? 128 : (n <= 256 ? 256 : 512);
@@ -478,6 +486,15 @@ struct pipedp_mcm_plan {
   int64_t total_chunks;
   int launches;
   int last_bits;
+  // tiled kernel
+  int32_t* d_pp;                 // dims, zero padded to N*T + 2
+  uint32_t* d_tiles;
+  unsigned long long* d_keys;
+  int* d_tile_flags;             // tile_done | far_count
+  unsigned long long* d_tasks;
+  int64_t ntasks;
+  int32_t N;
+  int tiled_grid;
 };
 
 namespace {
@@ -505,6 +522,43 @@ int mcm_wave_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split
   }
   CK(cudaGetLastError());
   return PIPEDP_OK;
+}
+
+int mcm_tiled_launch(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t st) {
+  const int64_t n = P->n, N = P->N, ntiles = N * (N + 1) / 2;
+  CK(cudaMemsetAsync(P->d_keys, 0xFF, sizeof(unsigned long long) * ntiles * kTC, st));
+  CK(cudaMemsetAsync(P->d_tile_flags, 0, sizeof(int) * 2 * ntiles, st));
+  CK(cudaMemsetAsync(P->d_next, 0, sizeof(unsigned long long), st));
+  CK(cudaMemsetAsync(cells, 0, sizeof(int64_t) * (n + 1), st));
+  CK(cudaMemsetAsync(split, 0, sizeof(int64_t) * (n + 1), st));
+  McmTiled S{n, (int32_t)N, P->ntasks, P->d_pp, P->d_tiles, P->d_keys, P->d_tile_flags,
+             P->d_tile_flags + ntiles, P->d_tasks, P->d_next, cells, split, P->d_overflow};
+  CK(cudaFuncSetAttribute(mcm_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)kTiledSmemBytes));
+  mcm_tiled_kernel<<<(unsigned)P->tiled_grid, kTiledThreads, kTiledSmemBytes, st>>>(S);
+  CK(cudaGetLastError());
+  return PIPEDP_OK;
+}
+
+// Task list of the tiled kernel, ordered by readiness (see mcm_tiled.cuh):
+// position 2*Delta for the diagonal/near task of tile (I, I+Delta), position
+// 2*max(K-I, J-K)+1 for far task (I, J, K).
+std::vector<unsigned long long> mcm_tiled_tasks(int N) {
+  std::vector<std::vector<unsigned long long>> buckets((size_t)2 * N + 1);
+  for (int I = 0; I < N; ++I) buckets[0].push_back(tiled_task(kTaskDiag, I, I, 0));
+  for (int D = 1; D < N; ++D)
+    for (int I = 0; I + D < N; ++I) buckets[(size_t)2 * D].push_back(tiled_task(kTaskNear, I, I + D, 0));
+  for (int D = 2; D < N; ++D)
+    for (int I = 0; I + D < N; ++I) {
+      const int J = I + D;
+      for (int K = I + 1; K < J; ++K) {
+        const int L = std::max(K - I, J - K);
+        buckets[(size_t)2 * L + 1].push_back(tiled_task(kTaskFar, I, J, K));
+      }
+    }
+  std::vector<unsigned long long> out;
+  for (auto& b : buckets) out.insert(out.end(), b.begin(), b.end());
+  return out;
 }
 
 int mcm_smem_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split, cudaStream_t st) {
@@ -537,6 +591,7 @@ int mcm_execute(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t
   for (;;) {
     CK(cudaMemsetAsync(P->d_overflow, 0, sizeof(int), st));
     if (P->d.kernel == PIPEDP_MCM_SMEM) TRY(mcm_smem_launch(P, bits, cells, split, st));
+    else if (P->d.kernel == PIPEDP_MCM_TILED && bits == 32) TRY(mcm_tiled_launch(P, cells, split, st));
     else TRY(mcm_wave_launch(P, bits, cells, split, st));
     ++P->launches;
     P->last_bits = bits;
@@ -809,7 +864,32 @@ int32_t pipedp_mcm_plan_create(int64_t batch, int64_t n, const int64_t* h_dims, 
   if (e == cudaSuccess) e = cudaMemcpy(P->d_dims, h_dims, sizeof(int64_t) * p32.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&P->d_overflow, sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&P->h_overflow, sizeof(int));
-  if (e == cudaSuccess && d.kernel == PIPEDP_MCM_WAVEFRONT) {
+  if (e == cudaSuccess && d.kernel == PIPEDP_MCM_TILED) {
+    const int64_t N = (n + kT - 1) / kT, ntiles = N * (N + 1) / 2;
+    P->N = (int32_t)N;
+    std::vector<int32_t> pp((size_t)(N * kT + 2), 0);
+    for (int64_t i = 0; i <= n; ++i) pp[(size_t)i] = (int32_t)h_dims[i];
+    const std::vector<unsigned long long> tasks = mcm_tiled_tasks((int)N);
+    P->ntasks = (int64_t)tasks.size();
+    e = cudaMalloc(&P->d_pp, sizeof(int32_t) * pp.size());
+    if (e == cudaSuccess) e = cudaMemcpy(P->d_pp, pp.data(), sizeof(int32_t) * pp.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_tiles, sizeof(uint32_t) * ntiles * kTC);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_keys, sizeof(unsigned long long) * ntiles * kTC);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_tile_flags, sizeof(int) * 2 * ntiles);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_tasks, sizeof(unsigned long long) * tasks.size());
+    if (e == cudaSuccess)
+      e = cudaMemcpy(P->d_tasks, tasks.data(), sizeof(unsigned long long) * tasks.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(mcm_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)kTiledSmemBytes);
+    int per_sm = 0;
+    if (e == cudaSuccess)
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mcm_tiled_kernel, kTiledThreads, kTiledSmemBytes);
+    // persistent grid: every CTA resident (tasks wait on earlier tasks only)
+    P->tiled_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(per_sm, 1) * sm_count(), P->ntasks));
+    if (e == cudaSuccess && per_sm < 1) e = cudaErrorInvalidConfiguration;
+  }
+  // the wavefront resources also back the tiled kernel's exact int64 rerun
+  if (e == cudaSuccess && (d.kernel == PIPEDP_MCM_WAVEFRONT || d.kernel == PIPEDP_MCM_TILED)) {
     std::vector<int64_t> base((size_t)n + 1, 0);
     int64_t total = 0;
     for (int64_t D = 1; D < n; ++D) {
@@ -839,8 +919,9 @@ int32_t pipedp_mcm_plan_execute(pipedp_mcm_plan_t P, int64_t* d_cells, int64_t* 
 int32_t pipedp_mcm_plan_describe(pipedp_mcm_plan_t P, char* name, size_t cap, int32_t* bits,
                                  int32_t* launches) {
   if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
-  const char* nm = P->d.kernel == PIPEDP_MCM_SMEM ? "mcm_smem_cta"
+  const char* nm = P->d.kernel == PIPEDP_MCM_SMEM         ? "mcm_smem_cta"
                    : P->d.kernel == PIPEDP_MCM_TOURNAMENT ? "mcm_tournament"
+                   : (P->d.kernel == PIPEDP_MCM_TILED && P->last_bits != 64) ? "mcm_tiled_kernel"
                                                           : "mcm_wavefront";
   if (name && cap) snprintf(name, cap, "%s", nm);
   if (bits) *bits = P->last_bits ? P->last_bits : P->d.bits;
@@ -858,6 +939,11 @@ int32_t pipedp_mcm_plan_destroy(pipedp_mcm_plan_t P) {
   cudaFree(P->d_done);
   cudaFree(P->d_next);
   cudaFree(P->d_overflow);
+  cudaFree(P->d_pp);
+  cudaFree(P->d_tiles);
+  cudaFree(P->d_keys);
+  cudaFree(P->d_tile_flags);
+  cudaFree(P->d_tasks);
   if (P->h_overflow) cudaFreeHost(P->h_overflow);
   delete P;
   return PIPEDP_OK;

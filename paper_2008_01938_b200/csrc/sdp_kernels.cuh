@@ -351,6 +351,104 @@ struct LaSteps<OP, T, 32> {
   }
 };
 
+// ---- idempotent closure (min / max) ------------------------------------------
+// For an idempotent, associative, commutative (x) the in-batch recurrence
+//   x_l = b_l (x) (x)_{d in S, d <= l} x_{l-d}      (b_l: every out-of-batch term)
+// unrolls to x_l = (x)_{t in T_l} b_t with T_l = {t <= l : l - t in S*}, S* the
+// additive closure of the offset set (a path t -> l of in-batch steps exists
+// iff l - t is a sum of offsets; folding a value twice changes nothing).  The
+// next batch's terms from this batch, (x)_{d in S, l < d <= l+32} x_{l+32-d},
+// unroll the same way to (x)_{t in V_l} b_t.  Both are reductions over b that
+// do NOT depend on each other lane's result, so the batch's 31 dependent
+// shuffle steps become independent shuffles.  When 1 in S, S* covers
+// everything: T_l = [0, l] (x = inclusive prefix-(x) of b, a 5-step scan) and
+// x is monotone along the batch, so the next-batch fold is x at the single
+// lane src_l = l + 32 - min{d in S : d > l}.
+struct IdemMasks {
+  uint32_t T;   // in-batch sources of x_l
+  uint32_t V;   // sources of the next batch's fold
+  int32_t src;  // scan form: lane whose x is the next-batch fold (-1: none)
+  bool scan;    // 1 in S (warp-uniform)
+};
+
+__device__ __forceinline__ IdemMasks idem_masks(const int32_t* offs, int k, int lane) {
+  uint64_t s64 = 0;
+  for (int j = k - 1; j >= 0; --j) {
+    const int a = offs[j];
+    if (a >= 64) break;
+    s64 |= 1ull << a;
+  }
+  const uint32_t s32 = (uint32_t)s64;
+  uint32_t reach = 1;  // bit m: m in S* (m < 32)
+  for (int m = 1; m < 32; ++m) {
+    const uint32_t cand = s32 & ((2u << m) - 1u);  // offsets d <= m
+    uint32_t hit = 0;
+    for (int d = 1; d <= m; ++d) hit |= ((cand >> d) & (reach >> (m - d))) & 1u;
+    reach |= hit << m;
+  }
+  auto tmask = [&](int l) {  // T_l
+    uint32_t t = 0;
+    for (int u = 0; u <= l; ++u) t |= ((reach >> (l - u)) & 1u) << u;
+    return t;
+  };
+  IdemMasks m;
+  m.scan = (s64 & 2ull) != 0;
+  m.T = tmask(lane);
+  m.V = 0;
+  m.src = -1;
+  for (int t = 31; t >= 0; --t) {  // U_l = {t : l + 32 - t in S}
+    const int d = lane + 32 - t;
+    if ((s64 >> d) & 1ull) {
+      m.V |= tmask(t);
+      if (m.src < 0) m.src = t;  // largest t = smallest d
+    }
+  }
+  return m;
+}
+
+// General form: broadcast b_t, t = 0..31 (independent shuffles), fold into x
+// when t in T_l and into the next-batch accumulator when t in V_l.
+template <int OP, typename T, int TT>
+struct IdemBcast {
+  __device__ __forceinline__ static void run(const T& b, T& x, T& nx, uint32_t mt, uint32_t mv) {
+    using O = SemiOp<OP, T>;
+    const T v = shfl_idx(b, TT);
+    if (bit_at<32 - TT>(mt)) x = O::apply(x, v);  // bit TT
+    if (bit_at<32 - TT>(mv)) nx = O::apply(nx, v);
+    IdemBcast<OP, T, TT + 1>::run(b, x, nx, mt, mv);
+  }
+};
+template <int OP, typename T>
+struct IdemBcast<OP, T, 32> {
+  __device__ __forceinline__ static void run(const T&, T&, T&, uint32_t, uint32_t) {}
+};
+
+// acc: in b, out x.  nxt: out, the next batch's fold of this batch's cells.
+template <int OP, typename T>
+__device__ __forceinline__ void idem_closure(T& acc, T& nxt, const IdemMasks& m) {
+  using O = SemiOp<OP, T>;
+  const T id = SemiId<OP, T>::value();
+  if (m.scan) {
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {
+      const T v = __shfl_up_sync(0xffffffffu, acc, s);  // lanes < s get their own value: idempotent
+      acc = O::apply(acc, v);
+    }
+    const T v = shfl_idx(acc, m.src < 0 ? 0 : m.src);
+    nxt = m.src < 0 ? id : v;
+  } else {
+    T x = id, nx = id;
+    IdemBcast<OP, T, 0>::run(acc, x, nx, m.T, m.V);
+    acc = x;
+    nxt = nx;
+  }
+}
+
+template <int OP>
+struct IsIdem {
+  static constexpr bool value = OP == kMin || OP == kMax;
+};
+
 // Ring group of offsets d in [l+33, 63] below p (cells two batches back),
 // identity for absent slots, tree-reduced.  The identity select is arithmetic
 // (sign-extended mask bit + LOP3): 31 live predicates exhaust the 7 predicate
@@ -482,6 +580,7 @@ __device__ __forceinline__ void sdp_finisher(const SdpShape& S, const int64_t* _
     const ChainMasks cm = chain_masks(offs, S.k, lane);
     constexpr bool kLA = !SMALL && ASSOC && !(OP == kModAdd && sizeof(T) == 8);
     const LaMasks lm = la_masks(offs, S.k, lane);
+    const IdemMasks im = idem_masks(offs, S.k, lane);
     T nxt = T(0);  // look-ahead accumulator of the next batch (kLA)
     if (kLA) {
       // seed nxt for batch 0: offsets d in [l+1, l+32] over the preset cells,
@@ -510,8 +609,12 @@ __device__ __forceinline__ void sdp_finisher(const SdpShape& S, const int64_t* _
         if (kLA) {
           // mid(b) already holds the offsets >= l+33; nxt the ones in [l+1, l+32]
           acc = SemiOp<OP, T>::apply(acc, nxt);
-          nxt = SemiId<OP, T>::value();
-          LaSteps<OP, T, 1>::run(acc, nxt, lm);
+          if (IsIdem<OP>::value) {
+            idem_closure<OP, T>(acc, nxt, im);
+          } else {
+            nxt = SemiId<OP, T>::value();
+            LaSteps<OP, T, 1>::run(acc, nxt, lm);
+          }
         } else {
           acc = chain_fold<OP, T, true, ASSOC>(acc, ring, pos, cm);
         }
@@ -762,6 +865,7 @@ __global__ void __launch_bounds__(256)
   const ChainMasks cm = chain_masks(offs, S.k, lane);
   constexpr bool kLA = !SMALL && ASSOC && !(OP == kModAdd && sizeof(T) == 8);
   const LaMasks lm = la_masks(offs, S.k, lane);
+  const IdemMasks im = idem_masks(offs, S.k, lane);
   T nxt = T(0);
   const int64_t nb = (n - a1 + 31) / 32;
   for (int64_t b = 0; b < nb; ++b) {
@@ -776,8 +880,14 @@ __global__ void __launch_bounds__(256)
       } else {
         acc = SemiOp<OP, T>::apply(acc, nxt);
       }
-      nxt = la_ring_group<OP, T>(ring + (((uint32_t)(c + 32) & (R - 1)) + R), lm.far);
-      LaSteps<OP, T, 1>::run(acc, nxt, lm);
+      const T nr = la_ring_group<OP, T>(ring + (((uint32_t)(c + 32) & (R - 1)) + R), lm.far);
+      if (IsIdem<OP>::value) {
+        idem_closure<OP, T>(acc, nxt, im);
+        nxt = SemiOp<OP, T>::apply(nxt, nr);
+      } else {
+        nxt = nr;
+        LaSteps<OP, T, 1>::run(acc, nxt, lm);
+      }
     } else if (!SMALL) {
       acc = fold_range<OP, T, ASSOC>(T(0), false, ring + pos, ob, 0, jn);
       acc = chain_fold<OP, T, true, ASSOC>(acc, ring, pos, cm);

@@ -23,13 +23,13 @@ def test_spec_apex_kats(gpu):
         assert t.cells[-1] == apex and split[-1] == sp
 
 
-@pytest.mark.parametrize("kernel", [0, 1, 2, 3])
+@pytest.mark.parametrize("kernel", [0, 1, 2, 3, 4])
 @pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 7, 16, 33, 64, 100])
 def test_small(gpu, oracle, kernel, n):
     _check(gpu, oracle, oracle.generate_mcm(n, n, 1, 100), kernel)
 
 
-@pytest.mark.parametrize("kernel", [0, 1, 3])
+@pytest.mark.parametrize("kernel", [0, 1, 3, 4])
 @pytest.mark.parametrize("n", [129, 200, 257, 511])
 def test_medium(gpu, oracle, kernel, n):
     _check(gpu, oracle, oracle.generate_mcm(n, 3, 1, 100), kernel)
@@ -40,6 +40,21 @@ def test_ties_first_min(gpu, oracle):
     for n in (5, 40, 300):
         _check(gpu, oracle, [7] * (n + 1), 0)
         _check(gpu, oracle, [7] * (n + 1), 1)
+    for n in (65, 200, 300):
+        _check(gpu, oracle, [7] * (n + 1), 4)
+        _check(gpu, oracle, [1] * (n + 1), 4)
+
+
+@pytest.mark.parametrize("n", [2, 3, 63, 64, 65, 127, 128, 130, 191, 192, 320, 700])
+def test_tiled_shapes(gpu, oracle, n):
+    # tile edge 64: exact multiples, one-past and ragged last tiles, 1..11 tiles per side
+    _check(gpu, oracle, oracle.generate_mcm(n, 17 + n, 1, 100), 4)
+
+
+def test_tiled_wide_dims_and_overflow(gpu, oracle):
+    _check(gpu, oracle, oracle.generate_mcm(260, 5, 1, 1290), 4)    # 32-bit, large values
+    _check(gpu, oracle, oracle.generate_mcm(300, 9, 1000, 1290), 4)  # reaches 2^30 -> exact int64 rerun
+    _check(gpu, oracle, oracle.generate_mcm(200, 2, 1, 100000), 4)   # max_dim^3 >= 2^31 -> int64 path
 
 
 def test_int32_overflow_falls_back_to_int64(gpu, oracle):
@@ -56,11 +71,21 @@ def test_wide_dims_int64(gpu, oracle):
     _check(gpu, oracle, dims[:80], 2)
 
 
-def test_config3_n1024(gpu, oracle):
+@pytest.mark.parametrize("kernel", [0, 1, 4])
+def test_config3_n1024(gpu, oracle, kernel):
     dims = oracle.generate_mcm(1024, 1, 1, 100)
-    t, split = gpu.solve_mcm_with_split(gpu.McmInstance(dims))
+    t, split = gpu.solve_mcm_with_split(gpu.McmInstance(dims), kernel)
     assert gpu.digest_hex(gpu.table_digest(t.cells)) == "9e31907a82260f66"
     assert gpu.digest_hex(gpu.table_digest(split)) == "42bfd8baf652c2f3"
+
+
+def test_config4_n8192_digest(gpu):
+    # BASELINE config 4: digests from SURVEY 8c (the reference took 48 min on one core)
+    dims = gpu.generate_mcm(n=8192, seed=1, dims_min=1, dims_max=100).dims
+    t, split = gpu.solve_mcm_with_split(gpu.McmInstance(dims))
+    assert gpu.digest_hex(gpu.table_digest(t.cells)) == "cc41fd2d4975b51b"
+    assert gpu.digest_hex(gpu.table_digest(split)) == "f9e2c86f904b28e1"
+    assert t.cells[-1] == 21215156
 
 
 @pytest.mark.parametrize("mode", ["paper_literal", "stall_on_hazard"])
