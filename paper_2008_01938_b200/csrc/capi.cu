@@ -22,6 +22,7 @@
 #include "mcm_kernels.cuh"
 #include "mcm_tiled.cuh"
 #include "sdp_kernels.cuh"
+#include "sdp_v2.cuh"
 
 using namespace pipedp_dev;
 
@@ -197,6 +198,8 @@ struct SdpDispatch {
   int grid_extra;  // producer CTAs (remote)
   size_t smem;
   int wpb;  // warp kernel: warps per block
+  bool v2;   // offset-partitioned single-instance pipeline (sdp_v2.cuh)
+  SdpV2Shape s2;
 };
 
 // value width and associativity from the init values (see common.cuh)
@@ -234,6 +237,75 @@ int sm_count() {
 size_t sdp_cta_smem(int64_t R, int64_t kpad, size_t vb) {
   return 2 * R * vb + 3 * kpad * 4 + (size_t)(kMidSlots + kFarSlots) * 32 * vb +
          (size_t)(2 * kBatchBars + kMidSlots + kFarSlots) * 8 + 64;
+}
+
+size_t sdp_v2_smem(int64_t R, int64_t kpad, size_t vb, int NW, int NC) {
+  return 2 * R * vb + kpad * 4 + (size_t)kMidSlots * 32 * vb + (size_t)kNearSlots * NW * 32 * vb +
+         (size_t)kFetchSlots * 32 * vb + (size_t)NC * 32 * 32 * 4 +
+         (size_t)(2 * kBatchBars + kMidSlots + kNearSlots + kFetchSlots) * 8 + 64;
+}
+
+// sdp_v2 plan (one instance): offsets >= a_rem to remote producers (when there
+// are enough of them), [64, a_rem) to register-resident near warps, < 64 to the
+// chain / combiners.  Returns false when the instance does not fit the layout.
+bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispatch* d) {
+  const size_t vb = d->bits / 8;
+  SdpV2Shape& s = d->s2;
+  s.n = n;
+  s.k = (int32_t)k;
+  s.a1 = (int32_t)a1;
+  const int64_t kpad = (k + 3) & ~3ll;
+  const int64_t nb = (n - a1 + 31) / 32;
+  int a_rem = std::max(128, env_int("PIPEDP_SDP2_AREM", 768));
+  int64_t jr = 0, jn = 0;
+  for (int64_t j = 0; j < k; ++j) {
+    jr += offs[j] >= a_rem;
+    jn += offs[j] >= 64;
+  }
+  bool remote = jr >= 64 && nb >= 256 && env_int("PIPEDP_SDP_MULTI", 1) != 0;
+  if (!remote) {
+    a_rem = 1 << 30;
+    jr = 0;
+  }
+  const int64_t cover = remote ? a_rem : a1;
+  const int64_t R = 1ll << ceil_log2((uint64_t)(cover + 512));
+  const int64_t count = jn - jr;
+  const int NW = (int)((count + kNearMax - 1) / kNearMax);
+  const int NC = std::max(1, std::min(8, env_int("PIPEDP_SDP2_COMB", 4)));
+  int NG = std::max(1, env_int("PIPEDP_SDP2_NEAR_GROUP", 2));
+  if (NW > kNearWarps) return false;
+  while (NG > 1 && sdp2_warps(NW, NG, NC, true) > 32) --NG;
+  if (sdp2_warps(NW, NG, NC, true) > 32) return false;
+  s.ring_log2 = ceil_log2((uint64_t)R);
+  s.a_rem = a_rem;
+  s.near_warps = NW;
+  s.comb_warps = NC;
+  s.near_group = NG;
+  for (int j = 0; j <= NW; ++j) s.near_lo[j] = (int32_t)(jr + (NW ? count * j / NW : 0));
+  const size_t smem = sdp_v2_smem(R, kpad, vb, NW, NC);
+  if (smem > kSmemBudget) return false;
+  d->v2 = true;
+  d->remote = remote;
+  d->small = false;
+  d->gfar = false;
+  d->warp_kernel = false;
+  d->smem = smem;
+  d->threads = 32 * sdp2_warps(NW, NG, NC, remote);
+  d->grid_extra = 0;
+  SdpShape& ps = d->shape;  // the producers' view
+  ps.n = n;
+  ps.k = (int32_t)k;
+  ps.a1 = (int32_t)a1;
+  ps.a_remote = a_rem;
+  ps.remote_warps = 0;
+  if (remote) {
+    ps.remote_warps = env_int("PIPEDP_SDP_REMOTE_WARPS", 16);
+    d->grid_extra = std::min(sm_count() - 1, env_int("PIPEDP_SDP_REMOTE_CTAS", 64));
+    d->threads = std::max(d->threads, 32 * ps.remote_warps);
+    const size_t psmem = (size_t)2 * kpad * 4 + (size_t)ps.remote_warps * 32 * 8 + 64;
+    d->smem = std::max(d->smem, psmem);
+  }
+  return true;
 }
 
 int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* offsets,
@@ -283,6 +355,10 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
     d->smem = sdp_cta_smem(1ll << s.ring_log2, kpad, vb);
     return PIPEDP_OK;
   }
+  d->v2 = false;
+  if (batch == 1 && d->assoc && !(op == PIPEDP_OP_MODULAR_ADD && d->bits == 64) &&
+      env_int("PIPEDP_SDP_V2", 1) != 0 && plan_sdp_v2(n, k, a1, offsets, d))
+    return PIPEDP_OK;
   // offset counts per stage (max over the batch sizes the stages)
   int64_t jf_max = 0, jr_max = 0;
   for (int64_t b = 0; b < batch; ++b) {
@@ -364,9 +440,29 @@ int launch_warp(const SdpDispatch& d, int64_t batch, const int64_t* offs, const 
   return PIPEDP_OK;
 }
 
+template <int OP, typename T>
+int launch_v2(const SdpDispatch& d, const int64_t* offs, const int64_t* init, int64_t* out,
+              const SdpRemote& rm, cudaStream_t st) {
+  if (!d.remote) {
+    auto kern = sdp_v2_cta<OP, T>;
+    CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem));
+    kern<<<1, d.threads, d.smem, st>>>(d.s2, offs, init, out);
+    CK(cudaGetLastError());
+    return PIPEDP_OK;
+  }
+  auto kern = sdp_v2_multi<OP, T>;
+  CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)d.smem));
+  SdpV2Shape s2 = d.s2;
+  SdpShape ps = d.shape;
+  void* args[] = {(void*)&s2, (void*)&ps, (void*)&offs, (void*)&init, (void*)&out, (void*)&rm};
+  CK(cudaLaunchCooperativeKernel((void*)kern, dim3(1 + d.grid_extra), dim3(d.threads), args, d.smem, st));
+  return PIPEDP_OK;
+}
+
 template <int OP, typename T, bool ASSOC>
 int launch_sdp_t(const SdpDispatch& d, int64_t batch, const int64_t* offs, const int64_t* init,
                  int64_t* out, const SdpRemote& rm, cudaStream_t st) {
+  if (ASSOC && d.v2 && !(OP == kModAdd && sizeof(T) == 8)) return launch_v2<OP, T>(d, offs, init, out, rm, st);
   if (d.warp_kernel) {
     return d.small ? launch_warp<OP, T, true, ASSOC>(d, batch, offs, init, out, st)
                    : launch_warp<OP, T, false, ASSOC>(d, batch, offs, init, out, st);
@@ -396,6 +492,7 @@ int launch_sdp(const SdpDispatch& d, int64_t batch, const int64_t* offs, const i
 }
 
 const char* sdp_kernel_name(const SdpDispatch& d) {
+  if (d.v2) return d.remote ? "sdp_v2_multi" : "sdp_v2_cta";
   if (d.warp_kernel) return "sdp_batch_warp";
   if (d.small) return "sdp_pipeline_cta[chain]";
   if (d.remote) return "sdp_pipeline_multi";

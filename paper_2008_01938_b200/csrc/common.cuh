@@ -138,6 +138,35 @@ __device__ __forceinline__ void st_release_gpu_i32(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Polling without per-iteration L1 invalidation: an ld.acquire.gpu compiles to
+// LDG.STRONG.GPU + CCTL.IVALL, and a CTA spinning on it invalidates its SM's L1
+// every iteration -- which stalls the LSU pipe that a co-resident CTA's shared
+// memory traffic uses.  Poll with relaxed loads, then one acquire fence.
+__device__ __forceinline__ int ld_relaxed_gpu_i32(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long ld_relaxed_gpu(const long long* p) {
+  long long v;
+  asm volatile("ld.relaxed.gpu.global.b64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+// spin until *p == want / >= want (acquire on exit)
+__device__ __forceinline__ void spin_eq_gpu(const int* p, int want, unsigned ns) {
+  while (ld_relaxed_gpu_i32(p) != want) __nanosleep(ns);
+  fence_acquire_gpu();
+}
+__device__ __forceinline__ void spin_ge_gpu(const int* p, int want, unsigned ns) {
+  while (ld_relaxed_gpu_i32(p) < want) __nanosleep(ns);
+  fence_acquire_gpu();
+}
+__device__ __forceinline__ void spin_ge_gpu64(const long long* p, long long want, unsigned ns) {
+  while (ld_relaxed_gpu(p) < want) __nanosleep(ns);
+  fence_acquire_gpu();
+}
+
 // ---- mbarrier (hardware-suspended waits; no issue slots burnt polling) ----
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
   return (unsigned)__cvta_generic_to_shared(p);

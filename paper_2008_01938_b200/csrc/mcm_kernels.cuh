@@ -193,9 +193,7 @@ __global__ void __launch_bounds__(256)
       const int cpw1 = 32 / mcm_wave_group(D - 1);
       const int64_t b1 = __ldg(W.chunk_base + D - 1);
       const int64_t q1 = (r_lo - 1) / cpw1, q2 = r_hi / cpw1;
-      for (int64_t qq = q1; qq <= q2; ++qq) {
-        while (ld_acquire_gpu_i32(W.done + b1 + qq) == 0) __nanosleep(32);
-      }
+      for (int64_t qq = q1; qq <= q2; ++qq) spin_ge_gpu(W.done + b1 + qq, 1, 32);
     }
     const int64_t r = r_lo + lane / G;
     const bool live = r <= r_hi;

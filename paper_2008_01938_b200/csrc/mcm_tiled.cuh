@@ -89,12 +89,18 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 __device__ __forceinline__ void fence_proxy_async_shared() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
-__device__ __forceinline__ void spin_until_set(const int* flag) {
-  while (ld_acquire_gpu_i32(flag) == 0) __nanosleep(64);
-}
-__device__ __forceinline__ void spin_until_count(const int* ctr, int want) {
-  while (ld_acquire_gpu_i32(ctr) < want) __nanosleep(64);
-}
+__device__ __forceinline__ void spin_until_set(const int* flag) { spin_ge_gpu(flag, 1, 64); }
+__device__ __forceinline__ void spin_until_count(const int* ctr, int want) { spin_ge_gpu(ctr, want, 64); }
+
+#ifdef PIPEDP_PROFILE
+__shared__ long long s_prof_ready;
+__shared__ long long s_prof_mark;   // near: end of init
+__shared__ long long s_prof_mark2;  // near/diag: end of the wavefront
+#define PROF_READY() \
+  if (threadIdx.x == 0) s_prof_ready = clock64()
+#else
+#define PROF_READY()
+#endif
 
 struct TBest {
   uint32_t v;
@@ -116,9 +122,51 @@ __device__ __forceinline__ TBest tb_reduce4(TBest b) {  // over lanes l, l^1, l^
   return b;
 }
 
+// Lexicographic (value, k) reduction over aligned groups of 2^lg lanes (lg <= 5);
+// fully unrolled with warp-uniform guards (no data-dependent loop trip count).
+__device__ __forceinline__ TBest tb_reduce(TBest b, int lg) {
+#pragma unroll
+  for (int i = 0; i < 5; ++i) {
+    if (i < lg) {
+      const uint32_t ov = __shfl_xor_sync(0xffffffffu, b.v, 1 << i);
+      const uint32_t ok = __shfl_xor_sync(0xffffffffu, b.k, 1 << i);
+      tb_take(b, ov, ok);
+    }
+  }
+  return b;
+}
+
+// log2 of the lanes per cell for a step with `count` live cells: the largest
+// G = 2^lg with count * G <= 256, at most 32 (the reduction stays in a warp).
+__device__ __forceinline__ int lanes_log2(int count) {
+  const int cl = 32 - __clz(count - 1);  // ceil(log2(count)), count >= 1
+  const int lg = 8 - cl;
+  return lg > 5 ? 5 : lg;
+}
+
+// Fold terms kl = k0, k0 + G, ... < k1 of one cell, k ascending (strict '<'
+// keeps the first minimum), two independent accumulators for ILP.
+//   cost = L[lrow + kl * ls] + Rm[rrow + kl * rs] + prc * pk[kl]
+template <typename F>
+__device__ __forceinline__ TBest fold_terms(int k0, int k1, int G, uint32_t kbase, F term) {
+  TBest b0{0xFFFFFFFFu, 0xFFFFFFFFu}, b1{0xFFFFFFFFu, 0xFFFFFFFFu};
+  int kl = k0;
+  for (; kl + G < k1; kl += 2 * G) {
+    const uint32_t c0 = term(kl), c1 = term(kl + G);
+    if (c0 < b0.v) { b0.v = c0; b0.k = kbase + kl; }
+    if (c1 < b1.v) { b1.v = c1; b1.k = kbase + kl + G; }
+  }
+  if (kl < k1) {
+    const uint32_t c0 = term(kl);
+    if (c0 < b0.v) { b0.v = c0; b0.k = kbase + kl; }
+  }
+  tb_take(b0, b1.v, b1.k);
+  return b0;
+}
+
 // Shared-memory carve-up (bytes), one layout for every task kind.
 struct TiledSmem {
-  uint32_t* A;      // far: tile (I, K) [T][T];  near: tile (I, I) [T][T]
+  uint32_t* A;      // far: tile (I, K) [T][T];  near: tile (I, I) [T][kXP]
   uint32_t* B;      // far: rows k+1 [T][T];     near: tile (J, J) [T][kXP]
   uint32_t* X;      // near/diag: this tile's values [T][kXP]
   uint32_t* KX;     // near/diag: this tile's split k [T][kXP]
@@ -130,7 +178,7 @@ struct TiledSmem {
 __device__ __forceinline__ TiledSmem tiled_smem(unsigned char* base) {
   TiledSmem s;
   s.A = reinterpret_cast<uint32_t*>(base);
-  s.B = s.A + kTC;
+  s.B = s.A + kT * kXP;
   s.X = s.B + kT * kXP;
   s.KX = s.X + kT * kXP;
   s.R0 = s.KX + kT * kXP;
@@ -139,7 +187,7 @@ __device__ __forceinline__ TiledSmem tiled_smem(unsigned char* base) {
   return s;
 }
 constexpr size_t kTiledSmemBytes =
-    (size_t)(kTC + 3 * kT * kXP + kT) * 4 + 4 * (kT + 4) * 4 + 16;
+    (size_t)(4 * kT * kXP + kT) * 4 + 4 * (kT + 4) * 4 + 16;
 
 // ---- far task: tile (I, J), split points k in tile K ------------------------------
 __device__ __forceinline__ void tiled_far(const McmTiled& S, const TiledSmem& sm, int I, int J, int K,
@@ -169,6 +217,7 @@ __device__ __forceinline__ void tiled_far(const McmTiled& S, const TiledSmem& sm
   __syncthreads();
   mbar_wait(sm.bar, phase);
   phase ^= 1u;
+  PROF_READY();
   const int ty = tid >> 4, tx = tid & 15;
   uint32_t u[4][4], best[4][4], bk[4][4];
 #pragma unroll
@@ -253,6 +302,7 @@ __device__ __forceinline__ void tiled_finish(const McmTiled& S, const TiledSmem&
 // ---- diagonal tile: MCM on the T x T triangle --------------------------------------
 __device__ __forceinline__ void tiled_diag(const McmTiled& S, const TiledSmem& sm, int I) {
   const int tid = threadIdx.x;
+  PROF_READY();
   int32_t* pI = sm.P;  // pI[x] = p[IT + x], x = 0..T
   if (tid <= kT) pI[tid] = S.p[(int64_t)I * kT + tid];
   for (int e = tid; e < kT; e += kTiledThreads) {
@@ -260,19 +310,20 @@ __device__ __forceinline__ void tiled_diag(const McmTiled& S, const TiledSmem& s
     sm.KX[e * kXP + e] = 0;
   }
   __syncthreads();
-  const int cell = tid >> 2, q = tid & 3;
   const uint32_t kb = (uint32_t)I * kT + 1;
   for (int dl = 1; dl < kT; ++dl) {
-    const int rl = cell, cl = cell + dl;
+    const int lg = lanes_log2(kT - dl), G = 1 << lg;
+    const int rl = tid >> lg, q = tid & (G - 1), cl = rl + dl;
     TBest b{0xFFFFFFFFu, 0xFFFFFFFFu};
     if (cl < kT) {
       const uint32_t prc = (uint32_t)pI[rl] * (uint32_t)pI[cl + 1];
-      for (int kl = rl + q; kl < cl; kl += 4) {
-        const uint32_t cost = sm.X[rl * kXP + kl] + sm.X[(kl + 1) * kXP + cl] + prc * (uint32_t)pI[kl + 1];
-        tb_take(b, cost, kb + kl);
-      }
+      const uint32_t* xr = sm.X + rl * kXP;
+      const uint32_t* xc = sm.X + kXP + cl;
+      b = fold_terms(rl + q, cl, G, kb, [&](int kl) {
+        return xr[kl] + xc[kl * kXP] + prc * (uint32_t)pI[kl + 1];
+      });
     }
-    b = tb_reduce4(b);
+    b = tb_reduce(b, lg);
     if (cl < kT && q == 0) {
       sm.X[rl * kXP + cl] = b.v;
       sm.KX[rl * kXP + cl] = b.k;
@@ -299,12 +350,16 @@ __device__ __forceinline__ void tiled_near(const McmTiled& S, const TiledSmem& s
   if (tid < 32) {  // tile (I, I) contiguous; tile (J, J) row by row into the padded pitch
     if (tid == 0) {
       mbar_expect_tx(sm.bar, (uint32_t)(kTC * 4 * 2 + kT * 4));
-      bulk_g2s(sm.A, S.tiles + tiled_index(I, I, N) * kTC, kTC * 4, sm.bar);
       bulk_g2s(sm.R0, S.tiles + tiled_index(I + 1, J, N) * kTC, kT * 4, sm.bar);
     }
     __syncwarp();
-    const uint32_t* src = S.tiles + tiled_index(J, J, N) * kTC;
-    for (int row = tid; row < kT; row += 32) bulk_g2s(sm.B + row * kXP, src + row * kT, kT * 4, sm.bar);
+    // tiles (I, I) and (J, J) row by row into the padded pitch (column reads stay conflict-light)
+    const uint32_t* srcI = S.tiles + tiled_index(I, I, N) * kTC;
+    const uint32_t* srcJ = S.tiles + tiled_index(J, J, N) * kTC;
+    for (int row = tid; row < kT; row += 32) {
+      bulk_g2s(sm.A + row * kXP, srcI + row * kT, kT * 4, sm.bar);
+      bulk_g2s(sm.B + row * kXP, srcJ + row * kT, kT * 4, sm.bar);
+    }
   }
   int32_t* pr = sm.P;                 // p[r-1], r in tile I
   int32_t* pc = sm.P + (kT + 4);      // p[c],   c in tile J
@@ -319,6 +374,7 @@ __device__ __forceinline__ void tiled_near(const McmTiled& S, const TiledSmem& s
   __syncthreads();
   mbar_wait(sm.bar, phase);
   phase ^= 1u;
+  PROF_READY();
   // init: far partial (Delta >= 2) (x) the k0 = (I+1)T term
   const unsigned long long* key = S.keys + tiled_index(I, J, N) * kTC;
   const uint32_t k0 = (uint32_t)(I + 1) * kT;
@@ -330,18 +386,22 @@ __device__ __forceinline__ void tiled_near(const McmTiled& S, const TiledSmem& s
       b.v = (uint32_t)(kv >> 32);
       b.k = (uint32_t)kv;
     }
-    const uint32_t cost = sm.A[rl * kT + (kT - 1)] + sm.R0[ul] + (uint32_t)pr[rl] * (uint32_t)pkI[kT - 1] * (uint32_t)pc[ul];
+    const uint32_t cost = sm.A[rl * kXP + (kT - 1)] + sm.R0[ul] + (uint32_t)pr[rl] * (uint32_t)pkI[kT - 1] * (uint32_t)pc[ul];
     tb_take(b, cost, k0);
     sm.X[rl * kXP + ul] = b.v;
     sm.KX[rl * kXP + ul] = b.k;
   }
   __syncthreads();
+#ifdef PIPEDP_PROFILE
+  if (tid == 0) s_prof_mark = clock64();
+#endif
   // pipeline over the tile's anti-diagonals: cell (rl, ul) at step (T-1-rl) + ul
-  const int ci = tid >> 2, q = tid & 3;
   const uint32_t kI = (uint32_t)I * kT + 1, kJ = (uint32_t)J * kT + 1;
   for (int s = 0; s <= 2 * (kT - 1); ++s) {
     const int ulo = s > kT - 1 ? s - (kT - 1) : 0;
     const int uhi = s < kT - 1 ? s : kT - 1;
+    const int lg = lanes_log2(uhi - ulo + 1), G = 1 << lg;
+    const int ci = tid >> lg, q = tid & (G - 1);
     const int ul = ulo + ci;
     const bool live = ul <= uhi;
     TBest b{0xFFFFFFFFu, 0xFFFFFFFFu};
@@ -350,17 +410,20 @@ __device__ __forceinline__ void tiled_near(const McmTiled& S, const TiledSmem& s
       rl = (kT - 1) - s + ul;
       const uint32_t prc = (uint32_t)pr[rl] * (uint32_t)pc[ul];
       // k in tile I: left (r, k) from tile (I, I), right (k+1, c) from rows below
-      for (int kl = rl + q; kl < kT - 1; kl += 4) {
-        const uint32_t cost = sm.A[rl * kT + kl] + sm.X[(kl + 1) * kXP + ul] + prc * (uint32_t)pkI[kl];
-        tb_take(b, cost, kI + kl);
-      }
+      const uint32_t* ar = sm.A + rl * kXP;
+      const uint32_t* xc = sm.X + kXP + ul;
+      b = fold_terms(rl + q, kT - 1, G, kI, [&](int kl) {
+        return ar[kl] + xc[kl * kXP] + prc * (uint32_t)pkI[kl];
+      });
       // k in tile J: left (r, k) from columns to the left, right (k+1, c) from tile (J, J)
-      for (int kl = q; kl < ul; kl += 4) {
-        const uint32_t cost = sm.X[rl * kXP + kl] + sm.B[(kl + 1) * kXP + ul] + prc * (uint32_t)pkJ[kl];
-        tb_take(b, cost, kJ + kl);
-      }
+      const uint32_t* xr = sm.X + rl * kXP;
+      const uint32_t* bc = sm.B + kXP + ul;
+      const TBest b2 = fold_terms(q, ul, G, kJ, [&](int kl) {
+        return xr[kl] + bc[kl * kXP] + prc * (uint32_t)pkJ[kl];
+      });
+      tb_take(b, b2.v, b2.k);
     }
-    b = tb_reduce4(b);
+    b = tb_reduce(b, lg);
     if (live && q == 0) {
       TBest cur{sm.X[rl * kXP + ul], sm.KX[rl * kXP + ul]};
       tb_take(cur, b.v, b.k);
@@ -368,6 +431,12 @@ __device__ __forceinline__ void tiled_near(const McmTiled& S, const TiledSmem& s
       sm.KX[rl * kXP + ul] = cur.k;
     }
     __syncthreads();
+#ifdef PIPEDP_PROFILE
+    if (tid == 0 && (s == 15 || s == 31 || s == 63 || s == 95 || s == 126)) {
+      const int slot = s == 15 ? 0 : s == 31 ? 1 : s == 63 ? 2 : s == 95 ? 3 : 4;
+      atomicAdd(&g_prof[48 + slot], (unsigned long long)(clock64() - s_prof_mark));
+    }
+#endif
   }
 }
 
@@ -389,14 +458,41 @@ __global__ void __launch_bounds__(kTiledThreads, 2) mcm_tiled_kernel(const McmTi
     const unsigned long long t = S.tasks[idx];
     const int kind = (int)(t >> 48), I = (int)((t >> 32) & 0xFFFF), J = (int)((t >> 16) & 0xFFFF),
               K = (int)(t & 0xFFFF);
+    const long long p_t0 = PROF_NOW();
+#ifdef PIPEDP_PROFILE
+    if (threadIdx.x == 0 && idx == 0) {
+      unsigned long long g0;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g0));
+      g_prof[63] = g0;
+    }
+#endif
     if (kind == kTaskFar) {
       tiled_far(S, sm, I, J, K, phase);
     } else {
       if (kind == kTaskDiag) tiled_diag(S, sm, I);
       else tiled_near(S, sm, I, J, phase);
+#ifdef PIPEDP_PROFILE
+      if (threadIdx.x == 0) s_prof_mark2 = clock64();
+#endif
       tiled_finish(S, sm, I, J);
     }
     __syncthreads();
+#ifdef PIPEDP_PROFILE
+    if (threadIdx.x == 0) {  // per kind: task cycles, wait cycles, count; per level: last finish
+      const long long p_t1 = clock64();
+      atomicAdd(&g_prof[32 + 4 * kind], (unsigned long long)(p_t1 - p_t0));
+      atomicAdd(&g_prof[33 + 4 * kind], (unsigned long long)(s_prof_ready - p_t0));
+      atomicAdd(&g_prof[34 + 4 * kind], 1ull);
+      if (kind == kTaskNear) {
+        atomicAdd(&g_prof[44], (unsigned long long)(s_prof_mark - s_prof_ready));   // init
+        atomicAdd(&g_prof[45], (unsigned long long)(s_prof_mark2 - s_prof_mark));   // wavefront
+        atomicAdd(&g_prof[46], (unsigned long long)(p_t1 - s_prof_mark2));          // finish
+      }
+      unsigned long long gt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+      if (kind != kTaskFar && J - I < 64) atomicMax(&g_prof[64 + J - I], gt);
+    }
+#endif
   }
 }
 

@@ -696,7 +696,7 @@ __device__ __forceinline__ void sdp_finisher(const SdpShape& S, const int64_t* _
         if (REMOTE && C.jr > 0) {
           const int rs = (int)(b % kRemSlots);
           t0 = PROF_NOW();
-          while (ld_acquire_gpu_i32(RM.ready + rs) != (int)(b + 1)) __nanosleep(64);
+          spin_eq_gpu(RM.ready + rs, (int)(b + 1), 64);
           PROF_ADD(p_wr, t0);
           acc = ldv_cg<T, int64_t>(reinterpret_cast<const int64_t*>(RM.part) + rs * 32 + lane);
           have = true;
@@ -771,8 +771,7 @@ __device__ __forceinline__ void sdp_producer(const SdpShape& S, const int64_t* _
     long long t0 = PROF_NOW();
     if (tid == 0) {
       const long long need = (long long)max(b + 1 - look, b + 1 - (int64_t)kRemSlots);
-      while ((long long)ld_acquire_gpu(reinterpret_cast<const long long*>(RM.published)) < need)
-        __nanosleep(128);
+      spin_ge_gpu64(reinterpret_cast<const long long*>(RM.published), need, 128);
     }
     __syncthreads();
     PROF_ADD(p_wait, t0);

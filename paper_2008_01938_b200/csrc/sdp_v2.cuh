@@ -1,0 +1,328 @@
+// sdp_v2.cuh -- single-instance S-DP pipeline, offset-partitioned stages
+// (sm_100a).  Used for associative (x) with an identity (min, max, 32-bit
+// modular-add, saturating-add without mixed signs); sdp_kernels.cuh keeps the
+// strict-order and HBM-ring variants.
+//
+// Reference semantics: sdp.cpp:48-60 (fill_table), sdp_pipeline.hpp:24-46.
+// Regrouping only (never a different set of operands): every cell folds the
+// same k operands as the reference; ASSOC lets the fold be split into partial
+// folds that are combined later.
+//
+// Finisher CTA (one per instance), cells in batches of 32 (one per lane):
+//   warp 0            chain: folds mid(b) (x) nxt and resolves the in-batch
+//                     dependency (idempotent closure for min/max, the 32-step
+//                     shuffle hand-off otherwise); owns SM sub-partition 0
+//   near warps j      each owns a contiguous range of offsets in [64, a_rem),
+//                     held in REGISTERS as ring byte offsets; every near warp
+//                     folds its range for EVERY batch as soon as the batches
+//                     it reads are final (lookahead = its smallest offset / 32)
+//   combiner warps    batch b -> warp b % NC: near partials (x) remote partial
+//                     (x) ring group d in [l+33, 63] (per-lane register list)
+//                     -> mid(b) for the chain
+//   writer warp       streams finished batches to HBM (coalesced int64) and,
+//                     with remote producers, publishes the finished prefix
+// Remote producer CTAs (sdp_producer, multi-CTA cooperative launch) fold the
+// offsets >= a_rem from the HBM table (long lookahead, gpu-scope flags).
+#pragma once
+
+#include "sdp_kernels.cuh"
+
+namespace pipedp_dev {
+
+constexpr int kNearMax = 32;   // offsets per near warp (registers)
+constexpr int kNearSlots = 16; // near -> combiner partial slots
+constexpr int kNearWarps = 20; // max near warps
+constexpr int kFetchSlots = 16; // fetcher -> combiner remote partial slots
+
+struct SdpV2Shape {
+  int64_t n;
+  int32_t k;
+  int32_t a1;
+  int32_t ring_log2;
+  int32_t a_rem;       // offsets >= a_rem come from remote producers (1 << 30: none)
+  int32_t near_warps;  // NW
+  int32_t comb_warps;  // NC
+  int32_t near_group;  // NG warps per offset range (batch b -> warp b % NG)
+  int32_t near_lo[kNearWarps + 1];  // near warp j owns offset indices [near_lo[j], near_lo[j+1])
+};
+
+__host__ __device__ __forceinline__ int sdp2_warps(int NW, int NG, int NC, bool remote) {
+  // chain + NC + NW*NG + writer (+ fetcher) roles, skipping warp ids = 0 mod 4 (SMSP 0 is the chain's)
+  return sdp_warps_for_roles(NC + NW * NG + 1 + (remote ? 1 : 0));
+}
+
+template <int OP, typename T, bool REMOTE>
+__device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64_t* __restrict__ offsets,
+                                                const int64_t* __restrict__ init, int64_t* out,
+                                                const SdpRemote& RM) {
+  using O = SemiOp<OP, T>;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const uint32_t R = 1u << S.ring_log2;
+  const int kpad = (S.k + 3) & ~3;
+  const int NW = S.near_warps, NC = S.comb_warps, NG = S.near_group;
+  T* ring = reinterpret_cast<T*>(smem);                       // 2R, mirrored
+  int32_t* offs = reinterpret_cast<int32_t*>(ring + 2 * R);   // raw a_j
+  T* mid_part = reinterpret_cast<T*>(offs + kpad);            // [kMidSlots][32]
+  T* near_part = mid_part + kMidSlots * 32;                   // [kNearSlots][NW][32]
+  T* rem_part = near_part + (size_t)kNearSlots * NW * 32;                  // [kFetchSlots][32]
+  int32_t* rg_scratch = reinterpret_cast<int32_t*>(rem_part + kFetchSlots * 32);  // [NC][32][32]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(rg_scratch + (size_t)NC * 32 * 32);
+  uint64_t* batch_done = bars;                   // [kBatchBars] chain -> all
+  uint64_t* written = batch_done + kBatchBars;  // [kBatchBars] writer -> chain
+  uint64_t* mid_full = written + kBatchBars;    // [kMidSlots] combiner -> chain
+  uint64_t* near_full = mid_full + kMidSlots;   // [kNearSlots] near warps -> combiner (count NW)
+  uint64_t* rem_full = near_full + kNearSlots;  // [kFetchSlots] fetcher -> combiner
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t a1 = S.a1, n = S.n;
+  for (int j = tid; j < S.k; j += blockDim.x) offs[j] = (int32_t)offsets[j];
+  const int64_t ring_from = a1 > (int64_t)R ? a1 - (int64_t)R : 0;
+  for (int64_t i = tid; i < a1; i += blockDim.x) {
+    const int64_t v = init[i];
+    if (i >= ring_from) {
+      const uint32_t p = (uint32_t)i & (R - 1);
+      ring[p] = (T)v;
+      ring[p + R] = (T)v;
+    }
+    out[i] = v;
+  }
+  if (tid == 0) {
+    for (int s = 0; s < 2 * kBatchBars + kMidSlots; ++s) mbar_init(&bars[s], 1);
+    for (int s = 0; s < kNearSlots; ++s) mbar_init(&near_full[s], (unsigned)(NW > 0 ? NW : 1));
+    for (int s = 0; s < kFetchSlots; ++s) mbar_init(&rem_full[s], 1);
+  }
+  __syncthreads();
+  const int64_t nb = (n - a1 + 31) / 32;
+  const int role = sdp_role_of_warp(warp);  // chain, idle SMSP-0 warps: -1
+  const T id = SemiId<OP, T>::value();
+
+  if (warp == 0) {
+    // ================================= chain ================================
+    const LaMasks lm = la_masks(offs, S.k, lane);
+    const IdemMasks im = idem_masks(offs, S.k, lane);
+    // nxt for batch 0: offsets d in [l+1, l+32] over the preset cells
+    T nxt = id;
+    {
+      const uint32_t pos0 = ((uint32_t)(a1 + lane) & (R - 1)) + R;
+      for (int d = lane + 32; d >= lane + 1; --d)
+        if ((lm.nbits >> (d - lane - 1)) & 1u) nxt = O::apply(nxt, ring[pos0 - d]);
+    }
+    PROF_DECL(p_wait);
+    PROF_DECL(p_fold);
+    const long long p_start = PROF_NOW();
+    for (int64_t b = 0; b < nb; ++b) {
+      if ((b & 15) == 0 && b >= 32) {
+        // writer lag <= 48 batches: the ring slots about to be overwritten
+        // (R/32 >= 64 batches back) are in HBM, and the writer never trails the
+        // 64-entry barrier rings by a full cycle
+        wait_batches(written, b - 32);
+      }
+      const int64_t c = a1 + 32 * b + lane;
+      const uint32_t pos = ((uint32_t)c & (R - 1)) + R;
+      const int slot = (int)(b % kMidSlots);
+      long long t0 = PROF_NOW();
+      mbar_wait(&mid_full[slot], (unsigned)((b / kMidSlots) & 1));
+      PROF_ADD(p_wait, t0);
+      t0 = PROF_NOW();
+      T acc = O::apply(mid_part[slot * 32 + lane], nxt);
+      if (IsIdem<OP>::value) {
+        idem_closure<OP, T>(acc, nxt, im);
+      } else {
+        nxt = id;
+        LaSteps<OP, T, 1>::run(acc, nxt, lm);
+      }
+      if (c < n) {
+        ring[pos - R] = acc;
+        ring[pos] = acc;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&batch_done[b % kBatchBars]);
+      PROF_ADD(p_fold, t0);
+    }
+    PROF_DECL(p_all);
+    PROF_ADD(p_all, p_start);
+    PROF_FLUSH(0, p_wait);
+    PROF_FLUSH(1, p_fold);
+    PROF_FLUSH(2, p_all);
+    PROF_FLUSH(3, nb);
+  } else if (role < 0) {
+    // idle: SMSP 0 belongs to the chain warp
+  } else if (role < NC) {
+    // =============================== combiner ===============================
+    // ring group: offsets d in [l+33, 63], a per-lane register list (compacted
+    // through this warp's shared scratch so the list indices stay static)
+    int32_t* scr = rg_scratch + (size_t)role * 32 * 32;
+    int nrg = 0;
+    {
+      const LaMasks lm = la_masks(offs, S.k, lane);
+      for (int d = 63; d >= lane + 33; --d)
+        if ((lm.far >> (d - 32)) & 1u) scr[(nrg++) * 32 + lane] = d * (int32_t)sizeof(T);
+    }
+    __syncwarp();
+    int32_t rg[31];
+#pragma unroll
+    for (int i = 0; i < 31; ++i) rg[i] = i < nrg ? scr[i * 32 + lane] : 0;  // 0: own slot, masked below
+    int mrg = nrg;  // warp-uniform loop bound
+#pragma unroll
+    for (int sh = 16; sh >= 1; sh >>= 1) mrg = max(mrg, __shfl_xor_sync(0xffffffffu, mrg, sh));
+    PROF_DECL(p_w1);
+    PROF_DECL(p_w2);
+    PROF_DECL(p_w3);
+    PROF_DECL(p_work);
+    for (int64_t b = role; b < nb; b += NC) {
+      long long t0 = PROF_NOW();
+      wait_batches(batch_done, b - 1);  // ring group reads batch b-2
+      PROF_ADD(p_w1, t0);
+      t0 = PROF_NOW();
+      const int64_t c = a1 + 32 * b + lane;
+      const char* base = reinterpret_cast<const char*>(ring + (((uint32_t)c & (R - 1)) + R));
+      T a0 = id, a1v = id;
+#pragma unroll
+      for (int i = 0; i < 31; i += 2) {
+        if (i < mrg) {  // uniform
+          const T v0 = *reinterpret_cast<const T*>(base - rg[i]);
+          const T v1 = *reinterpret_cast<const T*>(base - rg[i + 1 < 31 ? i + 1 : i]);
+          a0 = O::apply(a0, i < nrg ? v0 : id);
+          a1v = O::apply(a1v, i + 1 < nrg ? v1 : id);
+        }
+      }
+      T acc = O::apply(a0, a1v);
+      if (NW > 0) {
+        const int ns = (int)(b % kNearSlots);
+        PROF_ADD(p_work, t0);
+        t0 = PROF_NOW();
+        mbar_wait(&near_full[ns], (unsigned)((b / kNearSlots) & 1));
+        PROF_ADD(p_w2, t0);
+        t0 = PROF_NOW();
+        for (int j = 0; j < NW; ++j) acc = O::apply(acc, near_part[((size_t)ns * NW + j) * 32 + lane]);
+      }
+      if (REMOTE) {  // staged into shared memory by the fetcher warp
+        const int fs = (int)(b % kFetchSlots);
+        PROF_ADD(p_work, t0);
+        t0 = PROF_NOW();
+        mbar_wait(&rem_full[fs], (unsigned)((b / kFetchSlots) & 1));
+        PROF_ADD(p_w3, t0);
+        t0 = PROF_NOW();
+        acc = O::apply(acc, rem_part[fs * 32 + lane]);
+      }
+      const int slot = (int)(b % kMidSlots);
+      mid_part[slot * 32 + lane] = acc;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mid_full[slot]);
+      PROF_ADD(p_work, t0);
+    }
+    PROF_FLUSH(8, p_w1);
+    PROF_FLUSH(9, p_w2);
+    PROF_FLUSH(10, p_w3);
+    PROF_FLUSH(11, p_work);
+  } else if (role < NC + NW * NG) {
+    // ================================= near =================================
+    const int j = (role - NC) / NG, g = (role - NC) % NG;
+    const int j0 = S.near_lo[j], j1 = S.near_lo[j + 1];
+    const int cnt = j1 - j0;  // <= kNearMax, warp-uniform
+    int32_t ob[kNearMax];  // padded with a valid offset; padded slots fold the identity
+#pragma unroll
+    for (int i = 0; i < kNearMax; ++i) ob[i] = offs[j0 + (i < cnt ? i : 0)] * (int32_t)sizeof(T);
+    const int amin = cnt > 0 ? offs[j1 - 1] : (1 << 30);
+    const int64_t look = (amin - 31 + 31) / 32;  // ceil((amin - 31) / 32): batches behind
+    PROF_DECL(p_nw);
+    PROF_DECL(p_nf);
+    for (int64_t b = g; b < nb; b += NG) {
+      int64_t need = b + 1 - look;                              // operands final
+      need = max(need, b + 1 - (int64_t)kNearSlots + 1);        // slot consumed by the combiner
+      long long t0 = PROF_NOW();
+      wait_batches(batch_done, need);
+      PROF_ADD(p_nw, t0);
+      t0 = PROF_NOW();
+      const int64_t c = a1 + 32 * b + lane;
+      const char* base = reinterpret_cast<const char*>(ring + (((uint32_t)c & (R - 1)) + R));
+      T a0 = id, a1v = id, a2 = id, a3 = id;
+#pragma unroll
+      for (int i = 0; i < kNearMax; i += 4) {
+        T v0 = *reinterpret_cast<const T*>(base - ob[i]);
+        T v1 = *reinterpret_cast<const T*>(base - ob[i + 1]);
+        T v2 = *reinterpret_cast<const T*>(base - ob[i + 2]);
+        T v3 = *reinterpret_cast<const T*>(base - ob[i + 3]);
+        if (!IsIdem<OP>::value) {  // duplicates are harmless only for idempotent ops
+          v0 = i < cnt ? v0 : id;
+          v1 = i + 1 < cnt ? v1 : id;
+          v2 = i + 2 < cnt ? v2 : id;
+          v3 = i + 3 < cnt ? v3 : id;
+        }
+        a0 = O::apply(a0, v0);
+        a1v = O::apply(a1v, v1);
+        a2 = O::apply(a2, v2);
+        a3 = O::apply(a3, v3);
+      }
+      const int ns = (int)(b % kNearSlots);
+      near_part[((size_t)ns * NW + j) * 32 + lane] = O::apply(O::apply(a0, a1v), O::apply(a2, a3));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&near_full[ns]);
+      PROF_ADD(p_nf, t0);
+    }
+    PROF_FLUSH(16 + (j == 0 ? 0 : 2), p_nw);
+    PROF_FLUSH(17 + (j == 0 ? 0 : 2), p_nf);
+    (void)g;
+  } else if (REMOTE && role == NC + NW * NG + 1) {
+    // ================================ fetcher ===============================
+    // copies the remote producers' partials into shared slots ahead of the
+    // combiners, so no global-memory latency sits on the combine path
+    // eight batches per round: lane i < 8 polls batch b0+i, then every lane
+    // loads its cell of all eight partials (eight independent L2 reads)
+    for (int64_t b0 = 0; b0 < nb; b0 += 8) {
+      if (b0 >= kFetchSlots) wait_batches(batch_done, b0 + 8 - kFetchSlots);  // slots consumed
+      if (lane < 8 && b0 + lane < nb)
+        spin_eq_gpu(RM.ready + (int)((b0 + lane) % kRemSlots), (int)(b0 + lane + 1), 32);
+      __syncwarp();
+      fence_acquire_gpu();
+      T v[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        v[i] = b0 + i < nb ? ldv_cg<T, int64_t>(reinterpret_cast<const int64_t*>(RM.part) +
+                                                (int)((b0 + i) % kRemSlots) * 32 + lane)
+                           : T(0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) rem_part[(int)((b0 + i) % kFetchSlots) * 32 + lane] = v[i];
+      __syncwarp();
+      if (lane < 8 && b0 + lane < nb) mbar_arrive(&rem_full[(int)((b0 + lane) % kFetchSlots)]);
+    }
+  } else if (role == NC + NW * NG) {
+    // ================================= writer ===============================
+    for (int64_t b = 0; b < nb; ++b) {
+      mbar_wait(&batch_done[b % kBatchBars], (unsigned)((b / kBatchBars) & 1));
+      const int64_t c = a1 + 32 * b + lane;
+      if (c < n) out[c] = (int64_t)ring[(uint32_t)c & (R - 1)];
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&written[b % kBatchBars]);
+      if (REMOTE && ((b + 1) % kPubEvery == 0 || b + 1 == nb)) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) st_release_gpu(reinterpret_cast<long long*>(RM.published), (long long)(b + 1));
+      }
+    }
+  }
+}
+
+template <int OP, typename T>
+__global__ void __launch_bounds__(1024, 1)
+    sdp_v2_cta(const __grid_constant__ SdpV2Shape S, const int64_t* __restrict__ g_offsets, const int64_t* __restrict__ g_init,
+               int64_t* __restrict__ g_out) {
+  const int64_t inst = blockIdx.x;
+  sdp_v2_finisher<OP, T, false>(S, g_offsets + inst * S.k, g_init + inst * S.a1, g_out + inst * S.n,
+                                SdpRemote{});
+}
+
+// Block 0: finisher; blocks 1..: remote producers (cooperative launch).
+template <int OP, typename T>
+__global__ void __launch_bounds__(1024, 1)
+    sdp_v2_multi(const __grid_constant__ SdpV2Shape S, const SdpShape PS, const int64_t* __restrict__ g_offsets,
+                 const int64_t* __restrict__ g_init, int64_t* g_out, const SdpRemote RM) {
+  if (blockIdx.x == 0) {
+    sdp_v2_finisher<OP, T, true>(S, g_offsets, g_init, g_out, RM);
+  } else {
+    if (threadIdx.x >= 32 * PS.remote_warps) return;
+    sdp_producer<OP, T>(PS, g_offsets, g_out, RM, blockIdx.x - 1, gridDim.x - 1);
+  }
+}
+
+}  // namespace pipedp_dev
