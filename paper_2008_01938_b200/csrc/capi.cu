@@ -23,6 +23,7 @@
 #include "mcm_tiled.cuh"
 #include "sdp_kernels.cuh"
 #include "sdp_v2.cuh"
+#include "host_io.hpp"
 
 using namespace pipedp_dev;
 
@@ -241,7 +242,7 @@ size_t sdp_cta_smem(int64_t R, int64_t kpad, size_t vb) {
 
 size_t sdp_v2_smem(int64_t R, int64_t kpad, size_t vb, int NW, int NC) {
   return 2 * R * vb + kpad * 4 + (size_t)kMidSlots * 32 * vb + (size_t)kNearSlots * NW * 32 * vb +
-         (size_t)kFetchSlots * 32 * vb + (size_t)NC * 32 * 32 * 4 +
+         (size_t)kFetchSlots * 32 * vb + (size_t)kPreMax * 32 * 4 +
          (size_t)(2 * kBatchBars + kMidSlots + kNearSlots + kFetchSlots) * 8 + 64;
 }
 
@@ -257,10 +258,18 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   const int64_t kpad = (k + 3) & ~3ll;
   const int64_t nb = (n - a1 + 31) / 32;
   int a_rem = std::max(128, env_int("PIPEDP_SDP2_AREM", 768));
+  // chain-local range [l+33, a_chain): at most kPreMax offsets for lane 0
+  int a_chain = 64;
+  for (int cand = 64; cand <= 256; cand += 32) {
+    int64_t cnt = 0;
+    for (int64_t j = 0; j < k; ++j) cnt += offs[j] >= 33 && offs[j] < cand;
+    if (cnt <= kPreMax) a_chain = cand;
+  }
+  a_chain = std::min(a_chain, std::max(64, env_int("PIPEDP_SDP2_ACHAIN", 1 << 20)));
   int64_t jr = 0, jn = 0;
   for (int64_t j = 0; j < k; ++j) {
     jr += offs[j] >= a_rem;
-    jn += offs[j] >= 64;
+    jn += offs[j] >= a_chain;
   }
   bool remote = jr >= 64 && nb >= 256 && env_int("PIPEDP_SDP_MULTI", 1) != 0;
   if (!remote) {
@@ -274,10 +283,11 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   const int NC = std::max(1, std::min(8, env_int("PIPEDP_SDP2_COMB", 4)));
   int NG = std::max(1, env_int("PIPEDP_SDP2_NEAR_GROUP", 2));
   if (NW > kNearWarps) return false;
-  while (NG > 1 && sdp2_warps(NW, NG, NC, true) > 32) --NG;
-  if (sdp2_warps(NW, NG, NC, true) > 32) return false;
+  while (NG > 1 && sdp2_warps(NW, NG, NC, true) > 24) --NG;
+  if (sdp2_warps(NW, NG, NC, true) > 24) return false;
   s.ring_log2 = ceil_log2((uint64_t)R);
   s.a_rem = a_rem;
+  s.a_chain = a_chain;
   s.near_warps = NW;
   s.comb_warps = NC;
   s.near_group = NG;
@@ -299,7 +309,7 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   ps.a_remote = a_rem;
   ps.remote_warps = 0;
   if (remote) {
-    ps.remote_warps = env_int("PIPEDP_SDP_REMOTE_WARPS", 16);
+    ps.remote_warps = std::min(24, env_int("PIPEDP_SDP_REMOTE_WARPS", 16));
     d->grid_extra = std::min(sm_count() - 1, env_int("PIPEDP_SDP_REMOTE_CTAS", 64));
     d->threads = std::max(d->threads, 32 * ps.remote_warps);
     const size_t psmem = (size_t)2 * kpad * 4 + (size_t)ps.remote_warps * 32 * 8 + 64;
@@ -515,7 +525,8 @@ struct pipedp_sdp_plan {
 namespace {
 
 struct McmDispatch {
-  int kernel;  // PIPEDP_MCM_WAVEFRONT / SMEM / TOURNAMENT
+  int kernel;  // PIPEDP_MCM_WAVEFRONT / SMEM / TOURNAMENT / TILED
+  int tile;    // tiled kernel: tile edge (32 or 64)
   int bits;    // 32 or 64 (first attempt)
   int threads;
   size_t smem32, smem64;
@@ -549,7 +560,8 @@ int plan_mcm(int64_t batch, int64_t n, const int64_t* dims, int kernel, McmDispa
   }
   if (kernel == PIPEDP_MCM_TILED && batch > 1)
     return fail(PIPEDP_E_INVALID_PARAMS, "the tiled kernel solves one instance at a time");
-  if (kernel == PIPEDP_MCM_TILED && (n + kT - 1) / kT >= 65535)
+  d->tile = (n <= env_int("PIPEDP_MCM_T32_MAXN", 2048)) ? 32 : 64;
+  if (kernel == PIPEDP_MCM_TILED && (n + d->tile - 1) / d->tile >= 65535)
     return fail(PIPEDP_ERR_UNSUPPORTED, "n=%lld too large for the tiled MCM kernel", (long long)n);
   if (kernel == PIPEDP_MCM_SMEM && d->smem64 > 227 * 1024 && d->smem32 > 227 * 1024)
     return fail(PIPEDP_ERR_UNSUPPORTED, "n=%lld too large for the shared-memory MCM kernel",
@@ -623,16 +635,23 @@ int mcm_wave_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split
 
 int mcm_tiled_launch(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t st) {
   const int64_t n = P->n, N = P->N, ntiles = N * (N + 1) / 2;
-  CK(cudaMemsetAsync(P->d_keys, 0xFF, sizeof(unsigned long long) * ntiles * kTC, st));
+  const int64_t TC = (int64_t)P->d.tile * P->d.tile;
+  CK(cudaMemsetAsync(P->d_keys, 0xFF, sizeof(unsigned long long) * ntiles * TC, st));
   CK(cudaMemsetAsync(P->d_tile_flags, 0, sizeof(int) * 2 * ntiles, st));
   CK(cudaMemsetAsync(P->d_next, 0, sizeof(unsigned long long), st));
   CK(cudaMemsetAsync(cells, 0, sizeof(int64_t) * (n + 1), st));
   CK(cudaMemsetAsync(split, 0, sizeof(int64_t) * (n + 1), st));
   McmTiled S{n, (int32_t)N, P->ntasks, P->d_pp, P->d_tiles, P->d_keys, P->d_tile_flags,
              P->d_tile_flags + ntiles, P->d_tasks, P->d_next, cells, split, P->d_overflow};
-  CK(cudaFuncSetAttribute(mcm_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)kTiledSmemBytes));
-  mcm_tiled_kernel<<<(unsigned)P->tiled_grid, kTiledThreads, kTiledSmemBytes, st>>>(S);
+  if (P->d.tile == 32) {
+    CK(cudaFuncSetAttribute(t32::mcm_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)t32::kTiledSmemBytes));
+    t32::mcm_tiled_kernel<<<(unsigned)P->tiled_grid, kTiledThreads, t32::kTiledSmemBytes, st>>>(S);
+  } else {
+    CK(cudaFuncSetAttribute(t64::mcm_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)t64::kTiledSmemBytes));
+    t64::mcm_tiled_kernel<<<(unsigned)P->tiled_grid, kTiledThreads, t64::kTiledSmemBytes, st>>>(S);
+  }
   CK(cudaGetLastError());
   return PIPEDP_OK;
 }
@@ -895,6 +914,8 @@ int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t P) {
   return PIPEDP_OK;
 }
 
+// Host-buffer solves: cached device buffers + staged, double-buffered copies
+// (host_io.hpp); the tables themselves come only from the kernels.
 static int32_t sdp_solve_host(int64_t batch, int64_t n, int64_t k, int64_t a1,
                               const int64_t* offsets, const int64_t* init, int32_t op,
                               int64_t* cells_out, int32_t device) {
@@ -904,16 +925,14 @@ static int32_t sdp_solve_host(int64_t batch, int64_t n, int64_t k, int64_t a1,
     pipedp_sdp_plan_t p;
     ~Guard() { pipedp_sdp_plan_destroy(p); }
   } guard{P};
-  Scope sc;
-  TRY(sc.init());
-  int64_t *d_init = nullptr, *d_cells = nullptr;
-  TRY(sc.alloc(&d_init, batch * a1));
-  TRY(sc.alloc(&d_cells, batch * n));
-  CK(cudaMemcpyAsync(d_init, init, sizeof(int64_t) * batch * a1, cudaMemcpyHostToDevice, sc.stream));
-  TRY(pipedp_sdp_plan_execute(P, d_init, d_cells, sc.stream));
-  CK(cudaMemcpyAsync(cells_out, d_cells, sizeof(int64_t) * batch * n, cudaMemcpyDeviceToHost,
-                     sc.stream));
-  CK(cudaStreamSynchronize(sc.stream));
+  pipedp_host::Workspace* W = nullptr;
+  CK(pipedp_host::workspace(P->device, &W));
+  void *d_init = nullptr, *d_cells = nullptr;
+  CK(W->buffer(0, sizeof(int64_t) * batch * a1, &d_init));
+  CK(W->buffer(1, sizeof(int64_t) * batch * n, &d_cells));
+  CK(W->h2d(d_init, init, sizeof(int64_t) * batch * a1));
+  TRY(pipedp_sdp_plan_execute(P, (const int64_t*)d_init, (int64_t*)d_cells, W->stream));
+  CK(W->d2h(cells_out, d_cells, sizeof(int64_t) * batch * n));
   return PIPEDP_OK;
 }
 
@@ -962,31 +981,34 @@ int32_t pipedp_mcm_plan_create(int64_t batch, int64_t n, const int64_t* h_dims, 
   if (e == cudaSuccess) e = cudaMalloc(&P->d_overflow, sizeof(int));
   if (e == cudaSuccess) e = cudaMallocHost(&P->h_overflow, sizeof(int));
   if (e == cudaSuccess && d.kernel == PIPEDP_MCM_TILED) {
-    const int64_t N = (n + kT - 1) / kT, ntiles = N * (N + 1) / 2;
+    const int64_t T = d.tile, TC = T * T;
+    const int64_t N = (n + T - 1) / T, ntiles = N * (N + 1) / 2;
     P->N = (int32_t)N;
-    std::vector<int32_t> pp((size_t)(N * kT + 2), 0);
+    std::vector<int32_t> pp((size_t)(N * T + 2), 0);
     for (int64_t i = 0; i <= n; ++i) pp[(size_t)i] = (int32_t)h_dims[i];
     const std::vector<unsigned long long> tasks = mcm_tiled_tasks((int)N);
     P->ntasks = (int64_t)tasks.size();
     e = cudaMalloc(&P->d_pp, sizeof(int32_t) * pp.size());
     if (e == cudaSuccess) e = cudaMemcpy(P->d_pp, pp.data(), sizeof(int32_t) * pp.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaMalloc(&P->d_tiles, sizeof(uint32_t) * ntiles * kTC);
-    if (e == cudaSuccess) e = cudaMalloc(&P->d_keys, sizeof(unsigned long long) * ntiles * kTC);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_tiles, sizeof(uint32_t) * ntiles * TC);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_keys, sizeof(unsigned long long) * ntiles * TC);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_tile_flags, sizeof(int) * 2 * ntiles);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_tasks, sizeof(unsigned long long) * tasks.size());
     if (e == cudaSuccess)
       e = cudaMemcpy(P->d_tasks, tasks.data(), sizeof(unsigned long long) * tasks.size(), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess) e = cudaFuncSetAttribute(mcm_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   (int)kTiledSmemBytes);
+    const void* kern = T == 32 ? (const void*)t32::mcm_tiled_kernel : (const void*)t64::mcm_tiled_kernel;
+    const size_t ksmem = T == 32 ? t32::kTiledSmemBytes : t64::kTiledSmemBytes;
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ksmem);
     int per_sm = 0;
-    if (e == cudaSuccess)
-      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, mcm_tiled_kernel, kTiledThreads, kTiledSmemBytes);
+    if (e == cudaSuccess) e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTiledThreads, ksmem);
     // persistent grid: every CTA resident (tasks wait on earlier tasks only)
     P->tiled_grid = (int)std::max<int64_t>(1, std::min<int64_t>((int64_t)std::max(per_sm, 1) * sm_count(), P->ntasks));
     if (e == cudaSuccess && per_sm < 1) e = cudaErrorInvalidConfiguration;
   }
   // the wavefront resources also back the tiled kernel's exact int64 rerun
-  if (e == cudaSuccess && (d.kernel == PIPEDP_MCM_WAVEFRONT || d.kernel == PIPEDP_MCM_TILED)) {
+  const bool smem_may_fall_back = d.kernel == PIPEDP_MCM_SMEM && d.bits == 32 && d.smem64 > 227 * 1024;
+  if (e == cudaSuccess &&
+      (d.kernel == PIPEDP_MCM_WAVEFRONT || d.kernel == PIPEDP_MCM_TILED || smem_may_fall_back)) {
     std::vector<int64_t> base((size_t)n + 1, 0);
     int64_t total = 0;
     for (int64_t D = 1; D < n; ++D) {
@@ -1018,7 +1040,8 @@ int32_t pipedp_mcm_plan_describe(pipedp_mcm_plan_t P, char* name, size_t cap, in
   if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
   const char* nm = P->d.kernel == PIPEDP_MCM_SMEM         ? "mcm_smem_cta"
                    : P->d.kernel == PIPEDP_MCM_TOURNAMENT ? "mcm_tournament"
-                   : (P->d.kernel == PIPEDP_MCM_TILED && P->last_bits != 64) ? "mcm_tiled_kernel"
+                   : (P->d.kernel == PIPEDP_MCM_TILED && P->last_bits != 64)
+                       ? (P->d.tile == 32 ? "mcm_tiled_kernel<32>" : "mcm_tiled_kernel<64>")
                                                           : "mcm_wavefront";
   if (name && cap) snprintf(name, cap, "%s", nm);
   if (bits) *bits = P->last_bits ? P->last_bits : P->d.bits;
@@ -1046,25 +1069,65 @@ int32_t pipedp_mcm_plan_destroy(pipedp_mcm_plan_t P) {
   return PIPEDP_OK;
 }
 
+// Re-upload a new batch of dims into an existing plan of the same shape and
+// dispatch (the scratch tables are reused; only the dims-derived arrays change).
+static int mcm_plan_reload(pipedp_mcm_plan_t P, const int64_t* h_dims, const McmDispatch& d) {
+  const int64_t cnt = P->batch * (P->n + 1);
+  std::vector<int32_t> p32((size_t)cnt);
+  for (int64_t i = 0; i < cnt; ++i) p32[(size_t)i] = (int32_t)h_dims[i];
+  CK(cudaSetDevice(P->device));
+  CK(cudaMemcpy(P->d_p, p32.data(), sizeof(int32_t) * cnt, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(P->d_dims, h_dims, sizeof(int64_t) * cnt, cudaMemcpyHostToDevice));
+  if (P->d_pp) {  // tiled: first n+1 entries (the zero padding is unchanged)
+    CK(cudaMemcpy(P->d_pp, p32.data(), sizeof(int32_t) * (P->n + 1), cudaMemcpyHostToDevice));
+  }
+  P->d = d;
+  P->launches = 0;
+  P->last_bits = 0;
+  return PIPEDP_OK;
+}
+
 static int32_t mcm_solve_host(int64_t batch, int64_t n, const int64_t* dims, int32_t kernel,
                               int64_t* cells_out, int64_t* split_out, int32_t device) {
+  // The last plan of this thread is kept: a caller solving instance after
+  // instance of one shape (the reference's bench/verify loops) reuses its
+  // device tables instead of reallocating hundreds of MiB per call.
+  struct Cached {
+    pipedp_mcm_plan_t plan = nullptr;
+    int64_t batch = 0, n = 0;
+    int32_t kernel = -1, device = -2;
+    ~Cached() { pipedp_mcm_plan_destroy(plan); }
+  };
+  thread_local Cached cache;
+  for (int64_t b = 0; b < batch; ++b) TRY(validate_mcm(dims + b * (n + 1), n + 1));
+  McmDispatch d{};
+  TRY(plan_mcm(batch, n, dims, kernel, &d));
+  int dev = device;
+  if (dev < 0) CK(cudaGetDevice(&dev));
   pipedp_mcm_plan_t P = nullptr;
-  TRY(pipedp_mcm_plan_create(batch, n, dims, kernel, device, &P));
-  struct Guard {
-    pipedp_mcm_plan_t p;
-    ~Guard() { pipedp_mcm_plan_destroy(p); }
-  } guard{P};
+  if (cache.plan && cache.batch == batch && cache.n == n && cache.kernel == kernel && cache.device == dev &&
+      cache.plan->d.tile == d.tile && cache.plan->d.bits == d.bits) {
+    P = cache.plan;
+    TRY(mcm_plan_reload(P, dims, d));
+  } else {
+    pipedp_mcm_plan_destroy(cache.plan);
+    cache.plan = nullptr;
+    TRY(pipedp_mcm_plan_create(batch, n, dims, kernel, device, &P));
+    cache.plan = P;
+    cache.batch = batch;
+    cache.n = n;
+    cache.kernel = kernel;
+    cache.device = dev;
+  }
   const int64_t size = batch * (n * (n + 1) / 2 + 1);
-  Scope sc;
-  TRY(sc.init());
-  int64_t *d_cells = nullptr, *d_split = nullptr;
-  TRY(sc.alloc(&d_cells, size));
-  TRY(sc.alloc(&d_split, size));
-  TRY(pipedp_mcm_plan_execute(P, d_cells, d_split, sc.stream));
-  CK(cudaMemcpyAsync(cells_out, d_cells, sizeof(int64_t) * size, cudaMemcpyDeviceToHost, sc.stream));
-  if (split_out)
-    CK(cudaMemcpyAsync(split_out, d_split, sizeof(int64_t) * size, cudaMemcpyDeviceToHost, sc.stream));
-  CK(cudaStreamSynchronize(sc.stream));
+  pipedp_host::Workspace* W = nullptr;
+  CK(pipedp_host::workspace(P->device, &W));
+  void *d_cells = nullptr, *d_split = nullptr;
+  CK(W->buffer(1, sizeof(int64_t) * size, &d_cells));
+  CK(W->buffer(2, sizeof(int64_t) * size, &d_split));
+  TRY(pipedp_mcm_plan_execute(P, (int64_t*)d_cells, (int64_t*)d_split, W->stream));
+  CK(W->d2h(cells_out, d_cells, sizeof(int64_t) * size));
+  if (split_out) CK(W->d2h(split_out, d_split, sizeof(int64_t) * size));
   return PIPEDP_OK;
 }
 

@@ -1,0 +1,209 @@
+// host_io.hpp -- host <-> device transfer runtime of the C ABI's host-buffer
+// entry points (pipedp_*_solve*).
+//
+// The reference's API takes and returns std::vector (pageable host memory).  A
+// plain cudaMemcpy into pageable memory goes through the driver's own bounce
+// buffer at a few GB/s; tables here are up to tens of GiB (config 5b: 32 GiB),
+// so the transfer path is its own small runtime:
+//   * a per-thread, per-device cache of device buffers (grow-only) so repeated
+//     calls do not pay cudaMalloc/cudaFree;
+//   * pinned staging buffers (two 64 MiB chunks per thread/device): DMA of chunk
+//     i+1 overlaps the host-side copy of chunk i;
+//   * the host-side copy of a chunk is split over a persistent worker pool, so
+//     the pageable side (first-touch faults included) runs at memory bandwidth.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+namespace pipedp_host {
+
+// Persistent pool for parallel host memcpy (never runs any DP arithmetic).
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool* pool = new CopyPool();  // never destroyed: its detached workers outlive main
+    return *pool;
+  }
+  int size() const { return (int)workers_.size() + 1; }
+  // run fn(i) for i in [0, n) on the pool and the caller; returns when all done
+  void parallel_for(int n, const std::function<void(int)>& fn) {
+    if (n <= 1 || workers_.empty()) {
+      for (int i = 0; i < n; ++i) fn(i);
+      return;
+    }
+    std::unique_lock<std::mutex> call(call_mu_);  // one parallel_for at a time
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      fn_ = &fn;
+      n_ = n;
+      next_ = 0;
+      pending_ = n;
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> g(mu_);
+    done_cv_.wait(g, [&] { return pending_ == 0; });
+    fn_ = nullptr;
+  }
+
+ private:
+  CopyPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int nt = (int)std::min(16u, hw) - 1;
+    for (int i = 0; i < nt; ++i) workers_.emplace_back([this] { loop(); });
+    for (auto& t : workers_) t.detach();
+  }
+  void work() {
+    for (;;) {
+      int i;
+      const std::function<void(int)>* f;
+      {
+        std::lock_guard<std::mutex> g(mu_);
+        if (!fn_ || next_ >= n_) return;
+        i = next_++;
+        f = fn_;
+      }
+      (*f)(i);
+      std::lock_guard<std::mutex> g(mu_);
+      if (--pending_ == 0) done_cv_.notify_all();
+    }
+  }
+  void loop() {
+    unsigned long long seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return gen_ != seen; });
+        seen = gen_;
+      }
+      work();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex call_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* fn_ = nullptr;
+  int n_ = 0, next_ = 0, pending_ = 0;
+  unsigned long long gen_ = 0;
+};
+
+inline void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kPiece = 4u << 20;
+  const int pieces = (int)std::min<size_t>((bytes + kPiece - 1) / kPiece, (size_t)CopyPool::get().size() * 2);
+  if (pieces <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t per = (bytes + pieces - 1) / pieces;
+  CopyPool::get().parallel_for(pieces, [&](int i) {
+    const size_t lo = (size_t)i * per, hi = std::min(bytes, lo + per);
+    if (lo < hi) std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, hi - lo);
+  });
+}
+
+// Per-thread, per-device transfer workspace.
+struct Workspace {
+  static constexpr size_t kChunk = 64u << 20;
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  void* pinned[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  struct Buf {
+    void* p = nullptr;
+    size_t cap = 0;
+  };
+  Buf bufs[4];
+
+  cudaError_t init(int dev) {
+    device = dev;
+    cudaError_t e = cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking);
+    for (int i = 0; i < 2 && e == cudaSuccess; ++i) {
+      e = cudaHostAlloc(&pinned[i], kChunk, cudaHostAllocDefault);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    }
+    return e;
+  }
+  // device buffer `slot` with at least `bytes` (contents not preserved)
+  cudaError_t buffer(int slot, size_t bytes, void** out) {
+    Buf& b = bufs[slot];
+    if (b.cap < bytes) {
+      if (b.p) cudaFree(b.p);
+      b.p = nullptr;
+      b.cap = 0;
+      cudaError_t e = cudaMalloc(&b.p, std::max<size_t>(bytes, 256));
+      if (e != cudaSuccess) return e;
+      b.cap = std::max<size_t>(bytes, 256);
+    }
+    *out = b.p;
+    return cudaSuccess;
+  }
+  // pageable host -> device, staged and double-buffered; asynchronous w.r.t.
+  // the device work queued after it on `stream` (returns once the host side is read)
+  cudaError_t h2d(void* dst, const void* src, size_t bytes) {
+    size_t off = 0;
+    int i = 0;
+    while (off < bytes) {
+      const size_t len = std::min(kChunk, bytes - off);
+      const int s = i & 1;
+      cudaError_t e = cudaEventSynchronize(ev[s]);  // buffer s free again
+      if (e != cudaSuccess) return e;
+      parallel_memcpy(pinned[s], static_cast<const char*>(src) + off, len);
+      e = cudaMemcpyAsync(static_cast<char*>(dst) + off, pinned[s], len, cudaMemcpyHostToDevice, stream);
+      if (e == cudaSuccess) e = cudaEventRecord(ev[s], stream);
+      if (e != cudaSuccess) return e;
+      off += len;
+      ++i;
+    }
+    return cudaSuccess;
+  }
+  // device -> pageable host after the work queued on `stream`; synchronous
+  cudaError_t d2h(void* dst, const void* src, size_t bytes) {
+    const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+    auto issue = [&](size_t c) {
+      const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+      cudaError_t e = cudaMemcpyAsync(pinned[c & 1], static_cast<const char*>(src) + off, len,
+                                      cudaMemcpyDeviceToHost, stream);
+      return e == cudaSuccess ? cudaEventRecord(ev[c & 1], stream) : e;
+    };
+    if (nchunks == 0) return cudaStreamSynchronize(stream);
+    cudaError_t e = issue(0);
+    for (size_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+      if (c + 1 < nchunks) e = issue(c + 1);  // overlaps the host copy of chunk c
+      if (e == cudaSuccess) e = cudaEventSynchronize(ev[c & 1]);
+      if (e != cudaSuccess) break;
+      const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+      parallel_memcpy(static_cast<char*>(dst) + off, pinned[c & 1], len);
+    }
+    return e;
+  }
+};
+
+// The calling thread's workspace for `device` (created on first use).
+inline cudaError_t workspace(int device, Workspace** out) {
+  thread_local std::vector<Workspace*> spaces;
+  for (Workspace* w : spaces)
+    if (w->device == device) {
+      *out = w;
+      return cudaSuccess;
+    }
+  auto* w = new Workspace();
+  cudaError_t e = w->init(device);
+  if (e != cudaSuccess) {
+    delete w;  // partial resources are reclaimed at process exit
+    return e;
+  }
+  spaces.push_back(w);
+  *out = w;
+  return cudaSuccess;
+}
+
+}  // namespace pipedp_host

@@ -12,12 +12,13 @@
 //   warp 0            chain: folds mid(b) (x) nxt and resolves the in-batch
 //                     dependency (idempotent closure for min/max, the 32-step
 //                     shuffle hand-off otherwise); owns SM sub-partition 0
-//   near warps j      each owns a contiguous range of offsets in [64, a_rem),
+//   chain warp also   folds offsets d in [l+33, a_chain) of batch b+1 while
+//                     resolving batch b (they only read batches <= b-1)
+//   near warps j      each owns a contiguous range of offsets in [a_chain, a_rem),
 //                     held in REGISTERS as ring byte offsets; every near warp
 //                     folds its range for EVERY batch as soon as the batches
 //                     it reads are final (lookahead = its smallest offset / 32)
 //   combiner warps    batch b -> warp b % NC: near partials (x) remote partial
-//                     (x) ring group d in [l+33, 63] (per-lane register list)
 //                     -> mid(b) for the chain
 //   writer warp       streams finished batches to HBM (coalesced int64) and,
 //                     with remote producers, publishes the finished prefix
@@ -33,6 +34,7 @@ constexpr int kNearMax = 32;   // offsets per near warp (registers)
 constexpr int kNearSlots = 16; // near -> combiner partial slots
 constexpr int kNearWarps = 20; // max near warps
 constexpr int kFetchSlots = 16; // fetcher -> combiner remote partial slots
+constexpr int kPreMax = 32;     // chain-folded offsets per lane (registers)
 
 struct SdpV2Shape {
   int64_t n;
@@ -40,6 +42,7 @@ struct SdpV2Shape {
   int32_t a1;
   int32_t ring_log2;
   int32_t a_rem;       // offsets >= a_rem come from remote producers (1 << 30: none)
+  int32_t a_chain;     // offsets in [l+33, a_chain) are folded by the chain warp itself
   int32_t near_warps;  // NW
   int32_t comb_warps;  // NC
   int32_t near_group;  // NG warps per offset range (batch b -> warp b % NG)
@@ -65,8 +68,8 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
   T* mid_part = reinterpret_cast<T*>(offs + kpad);            // [kMidSlots][32]
   T* near_part = mid_part + kMidSlots * 32;                   // [kNearSlots][NW][32]
   T* rem_part = near_part + (size_t)kNearSlots * NW * 32;                  // [kFetchSlots][32]
-  int32_t* rg_scratch = reinterpret_cast<int32_t*>(rem_part + kFetchSlots * 32);  // [NC][32][32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(rg_scratch + (size_t)NC * 32 * 32);
+  int32_t* pre_scratch = reinterpret_cast<int32_t*>(rem_part + kFetchSlots * 32);  // [kPreMax][32]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(pre_scratch + (size_t)kPreMax * 32);
   uint64_t* batch_done = bars;                   // [kBatchBars] chain -> all
   uint64_t* written = batch_done + kBatchBars;  // [kBatchBars] writer -> chain
   uint64_t* mid_full = written + kBatchBars;    // [kMidSlots] combiner -> chain
@@ -107,6 +110,43 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
       for (int d = lane + 32; d >= lane + 1; --d)
         if ((lm.nbits >> (d - lane - 1)) & 1u) nxt = O::apply(nxt, ring[pos0 - d]);
     }
+    // offsets d in [l+33, a_chain): folded here, one batch ahead, interleaved
+    // with the closure (they read batches <= b-1 only) -- no hand-off latency
+    // on the dependency distance these offsets leave
+    int32_t pre[kPreMax];
+    int npre = 0;
+    {
+      int32_t* scr = pre_scratch;  // [kPreMax][32]
+      for (int j = S.k - 1; j >= 0; --j) {
+        const int d = offs[j];
+        if (d >= S.a_chain) break;
+        if (d >= lane + 33 && npre < kPreMax) scr[(npre++) * 32 + lane] = d * (int32_t)sizeof(T);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < kPreMax; ++i) pre[i] = i < npre ? scr[i * 32 + lane] : (npre ? scr[lane] : 0);
+    }
+    int mpre = npre;
+#pragma unroll
+    for (int sh = 16; sh >= 1; sh >>= 1) mpre = max(mpre, __shfl_xor_sync(0xffffffffu, mpre, sh));
+    auto pre_fold = [&](const char* base) {  // (x) of ring[base - pre[i]], i < npre
+      T p0 = id, p1 = id;
+#pragma unroll
+      for (int i = 0; i < kPreMax; i += 2) {
+        if (i < mpre) {  // warp-uniform
+          T v0 = *reinterpret_cast<const T*>(base - pre[i]);
+          T v1 = *reinterpret_cast<const T*>(base - pre[i + 1]);
+          if (!IsIdem<OP>::value || npre == 0) {  // padding folds the identity
+            v0 = i < npre ? v0 : id;
+            v1 = i + 1 < npre ? v1 : id;
+          }
+          p0 = O::apply(p0, v0);
+          p1 = O::apply(p1, v1);
+        }
+      }
+      return O::apply(p0, p1);
+    };
+    T pre_cur = pre_fold(reinterpret_cast<const char*>(ring + (((uint32_t)(a1 + lane) & (R - 1)) + R)));
     PROF_DECL(p_wait);
     PROF_DECL(p_fold);
     const long long p_start = PROF_NOW();
@@ -124,13 +164,17 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
       mbar_wait(&mid_full[slot], (unsigned)((b / kMidSlots) & 1));
       PROF_ADD(p_wait, t0);
       t0 = PROF_NOW();
-      T acc = O::apply(mid_part[slot * 32 + lane], nxt);
+      T acc = O::apply(O::apply(mid_part[slot * 32 + lane], pre_cur), nxt);
+      // batch b+1's chain-local offsets: independent of this batch's closure
+      const T pre_next =
+          pre_fold(reinterpret_cast<const char*>(ring + (((uint32_t)(c + 32) & (R - 1)) + R)));
       if (IsIdem<OP>::value) {
         idem_closure<OP, T>(acc, nxt, im);
       } else {
         nxt = id;
         LaSteps<OP, T, 1>::run(acc, nxt, lm);
       }
+      pre_cur = pre_next;
       if (c < n) {
         ring[pos - R] = acc;
         ring[pos] = acc;
@@ -149,44 +193,19 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
     // idle: SMSP 0 belongs to the chain warp
   } else if (role < NC) {
     // =============================== combiner ===============================
-    // ring group: offsets d in [l+33, 63], a per-lane register list (compacted
-    // through this warp's shared scratch so the list indices stay static)
-    int32_t* scr = rg_scratch + (size_t)role * 32 * 32;
-    int nrg = 0;
-    {
-      const LaMasks lm = la_masks(offs, S.k, lane);
-      for (int d = 63; d >= lane + 33; --d)
-        if ((lm.far >> (d - 32)) & 1u) scr[(nrg++) * 32 + lane] = d * (int32_t)sizeof(T);
-    }
-    __syncwarp();
-    int32_t rg[31];
-#pragma unroll
-    for (int i = 0; i < 31; ++i) rg[i] = i < nrg ? scr[i * 32 + lane] : 0;  // 0: own slot, masked below
-    int mrg = nrg;  // warp-uniform loop bound
-#pragma unroll
-    for (int sh = 16; sh >= 1; sh >>= 1) mrg = max(mrg, __shfl_xor_sync(0xffffffffu, mrg, sh));
     PROF_DECL(p_w1);
     PROF_DECL(p_w2);
     PROF_DECL(p_w3);
     PROF_DECL(p_work);
     for (int64_t b = role; b < nb; b += NC) {
       long long t0 = PROF_NOW();
-      wait_batches(batch_done, b - 1);  // ring group reads batch b-2
+      // mid slot b % kMidSlots was last used by batch b - kMidSlots: the chain
+      // must have consumed it (this also keeps every waiter within half a
+      // barrier ring of the chain)
+      wait_batches(batch_done, b + 1 - kMidSlots / 2);
       PROF_ADD(p_w1, t0);
       t0 = PROF_NOW();
-      const int64_t c = a1 + 32 * b + lane;
-      const char* base = reinterpret_cast<const char*>(ring + (((uint32_t)c & (R - 1)) + R));
-      T a0 = id, a1v = id;
-#pragma unroll
-      for (int i = 0; i < 31; i += 2) {
-        if (i < mrg) {  // uniform
-          const T v0 = *reinterpret_cast<const T*>(base - rg[i]);
-          const T v1 = *reinterpret_cast<const T*>(base - rg[i + 1 < 31 ? i + 1 : i]);
-          a0 = O::apply(a0, i < nrg ? v0 : id);
-          a1v = O::apply(a1v, i + 1 < nrg ? v1 : id);
-        }
-      }
-      T acc = O::apply(a0, a1v);
+      T acc = id;
       if (NW > 0) {
         const int ns = (int)(b % kNearSlots);
         PROF_ADD(p_work, t0);
@@ -304,7 +323,7 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
 }
 
 template <int OP, typename T>
-__global__ void __launch_bounds__(1024, 1)
+__global__ void __launch_bounds__(768, 1)
     sdp_v2_cta(const __grid_constant__ SdpV2Shape S, const int64_t* __restrict__ g_offsets, const int64_t* __restrict__ g_init,
                int64_t* __restrict__ g_out) {
   const int64_t inst = blockIdx.x;
@@ -314,7 +333,7 @@ __global__ void __launch_bounds__(1024, 1)
 
 // Block 0: finisher; blocks 1..: remote producers (cooperative launch).
 template <int OP, typename T>
-__global__ void __launch_bounds__(1024, 1)
+__global__ void __launch_bounds__(768, 1)
     sdp_v2_multi(const __grid_constant__ SdpV2Shape S, const SdpShape PS, const int64_t* __restrict__ g_offsets,
                  const int64_t* __restrict__ g_init, int64_t* g_out, const SdpRemote RM) {
   if (blockIdx.x == 0) {

@@ -45,9 +45,11 @@ def test_ties_first_min(gpu, oracle):
         _check(gpu, oracle, [1] * (n + 1), 4)
 
 
-@pytest.mark.parametrize("n", [2, 3, 63, 64, 65, 127, 128, 130, 191, 192, 320, 700])
-def test_tiled_shapes(gpu, oracle, n):
-    # tile edge 64: exact multiples, one-past and ragged last tiles, 1..11 tiles per side
+@pytest.mark.parametrize("t32_maxn", ["0", "100000"])  # tile edge 64 / 32
+@pytest.mark.parametrize("n", [2, 3, 31, 32, 33, 63, 64, 65, 127, 128, 130, 191, 192, 320, 700])
+def test_tiled_shapes(gpu, oracle, n, t32_maxn, monkeypatch):
+    # exact multiples of the tile edge, one-past and ragged last tiles, 1..22 tiles per side
+    monkeypatch.setenv("PIPEDP_MCM_T32_MAXN", t32_maxn)
     _check(gpu, oracle, oracle.generate_mcm(n, 17 + n, 1, 100), 4)
 
 
@@ -72,7 +74,9 @@ def test_wide_dims_int64(gpu, oracle):
 
 
 @pytest.mark.parametrize("kernel", [0, 1, 4])
-def test_config3_n1024(gpu, oracle, kernel):
+@pytest.mark.parametrize("t32_maxn", ["0", "100000"])
+def test_config3_n1024(gpu, oracle, kernel, t32_maxn, monkeypatch):
+    monkeypatch.setenv("PIPEDP_MCM_T32_MAXN", t32_maxn)
     dims = oracle.generate_mcm(1024, 1, 1, 100)
     t, split = gpu.solve_mcm_with_split(gpu.McmInstance(dims), kernel)
     assert gpu.digest_hex(gpu.table_digest(t.cells)) == "9e31907a82260f66"

@@ -21,7 +21,7 @@ __global__ void __launch_bounds__(kTiledThreads, 2) near_bench(long long* cyc, u
   for (int s = 0; s <= 2 * (kT - 1); ++s) {
     const int ulo = s > kT - 1 ? s - (kT - 1) : 0;
     const int uhi = s < kT - 1 ? s : kT - 1;
-    const int lg = lanes_log2(uhi - ulo + 1), G = 1 << lg;
+    const int lg = step_lanes_log2(uhi - ulo + 1, s), G = 1 << lg;
     const int ci = tid >> lg, q = tid & (G - 1);
     const int ul = ulo + ci;
     const bool live = ul <= uhi;
@@ -33,14 +33,28 @@ __global__ void __launch_bounds__(kTiledThreads, 2) near_bench(long long* cyc, u
         const uint32_t prc = (uint32_t)pr[rl] * (uint32_t)pc[ul];
         const uint32_t* ar = sm.A + rl * kXP;
         const uint32_t* xc = sm.X + kXP + ul;
-        b = fold_terms(rl + q, kT - 1, G, kI, [&](int kl) { return ar[kl] + xc[kl * kXP] + prc * (uint32_t)pkI[kl]; });
         const uint32_t* xr = sm.X + rl * kXP;
         const uint32_t* bc = sm.B + kXP + ul;
-        const TBest b2 = fold_terms(q, ul, G, kJ, [&](int kl) { return xr[kl] + bc[kl * kXP] + prc * (uint32_t)pkJ[kl]; });
-        tb_take(b, b2.v, b2.k);
+        if (MODE <= 2) {
+          b = fold_terms(rl + q, kT - 1, G, kI, [&](int kl) { return ar[kl] + xc[kl * kXP] + prc * (uint32_t)pkI[kl]; });
+          const TBest b2 = fold_terms(q, ul, G, kJ, [&](int kl) { return xr[kl] + bc[kl * kXP] + prc * (uint32_t)pkJ[kl]; });
+          tb_take(b, b2.v, b2.k);
+        } else if (MODE == 3) {  // row loads only
+          b = fold_terms(rl + q, kT - 1, G, kI, [&](int kl) { return ar[kl] + prc * (uint32_t)kl; });
+          const TBest b2 = fold_terms(q, ul, G, kJ, [&](int kl) { return xr[kl] + prc * (uint32_t)kl; });
+          tb_take(b, b2.v, b2.k);
+        } else if (MODE == 4) {  // column loads only
+          b = fold_terms(rl + q, kT - 1, G, kI, [&](int kl) { return xc[kl * kXP] + prc * (uint32_t)kl; });
+          const TBest b2 = fold_terms(q, ul, G, kJ, [&](int kl) { return bc[kl * kXP] + prc * (uint32_t)kl; });
+          tb_take(b, b2.v, b2.k);
+        } else {  // no loads
+          b = fold_terms(rl + q, kT - 1, G, kI, [&](int kl) { return prc * (uint32_t)kl + (uint32_t)ul; });
+          const TBest b2 = fold_terms(q, ul, G, kJ, [&](int kl) { return prc * (uint32_t)kl + (uint32_t)rl; });
+          tb_take(b, b2.v, b2.k);
+        }
       }
     }
-    if (MODE >= 2) b = tb_reduce(b, lg);
+    if (MODE == 2) b = tb_reduce(b, lg);
     if (live && q == 0) {
       TBest cur{sm.X[rl * kXP + ul], sm.KX[rl * kXP + ul]};
       tb_take(cur, b.v, b.k);
@@ -48,23 +62,29 @@ __global__ void __launch_bounds__(kTiledThreads, 2) near_bench(long long* cyc, u
       sm.KX[rl * kXP + ul] = cur.k;
     }
     __syncthreads();
+    if (tid == 0) cyc[2 + s] = clock64() - t0;
     if (tid == 0 && (s == 15 || s == 126)) cyc[s == 15 ? 0 : 1] = clock64() - t0;
   }
   sink[tid] = sm.X[tid];
 }
 
 int main() {
-  long long* cyc; uint32_t* sink; cudaMalloc(&cyc, 16); cudaMalloc(&sink, 4096);
-  long long h[2];
+  long long* cyc; uint32_t* sink; cudaMalloc(&cyc, 8 * 160); cudaMalloc(&sink, 4096);
+  long long h[160];
   auto run = [&](auto kern, const char* nm) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTiledSmemBytes);
     kern<<<1, kTiledThreads, kTiledSmemBytes>>>(cyc, sink); kern<<<1, kTiledThreads, kTiledSmemBytes>>>(cyc, sink);
     cudaError_t e = cudaDeviceSynchronize();
-    cudaMemcpy(h, cyc, 16, cudaMemcpyDeviceToHost);
-    printf("%-28s %s first16 %lld  all127 %lld cyc (%.0f/step)\n", nm, cudaGetErrorString(e), h[0], h[1], h[1] / 127.0);
+    cudaMemcpy(h, cyc, 8 * 160, cudaMemcpyDeviceToHost);
+    printf("%-28s %s first16 %lld  all127 %lld cyc (%.0f/step)\n   per-step:", nm, cudaGetErrorString(e), h[0], h[1], h[1] / 127.0);
+    for (int s = 0; s < 127; s += 8) printf(" %d:%lld", s, h[2 + s] - (s ? h[1 + s] : 0));
+    printf("\n");
   };
   run(near_bench<0>, "steps+write only");
   run(near_bench<1>, "+terms");
   run(near_bench<2>, "+reduce (full)");
+  run(near_bench<3>, "row loads only");
+  run(near_bench<4>, "column loads only");
+  run(near_bench<5>, "no loads");
   return 0;
 }
