@@ -242,7 +242,7 @@ size_t sdp_cta_smem(int64_t R, int64_t kpad, size_t vb) {
 
 size_t sdp_v2_smem(int64_t R, int64_t kpad, size_t vb, int NW, int NC) {
   return 2 * R * vb + kpad * 4 + (size_t)kMidSlots * 32 * vb + (size_t)kNearSlots * NW * 32 * vb +
-         (size_t)kFetchSlots * 32 * vb + (size_t)kPreMax * 32 * 4 +
+         (size_t)kFetchSlots * 32 * vb + (size_t)kPreMax * 32 * 4 + 16 +
          (size_t)(2 * kBatchBars + kMidSlots + kNearSlots + kFetchSlots) * 8 + 64;
 }
 
@@ -259,13 +259,27 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   const int64_t nb = (n - a1 + 31) / 32;
   int a_rem = std::max(128, env_int("PIPEDP_SDP2_AREM", 768));
   // chain-local range [l+33, a_chain): at most kPreMax offsets for lane 0
+  // chain-local range: [l+33, 64) per lane (<= 31 offsets) plus the
+  // lane-independent [64, a_chain) with at most kPreUMax offsets
   int a_chain = 64;
-  for (int cand = 64; cand <= 256; cand += 32) {
+  for (int cand = 96; cand <= 256; cand += 32) {
     int64_t cnt = 0;
-    for (int64_t j = 0; j < k; ++j) cnt += offs[j] >= 33 && offs[j] < cand;
-    if (cnt <= kPreMax) a_chain = cand;
+    for (int64_t j = 0; j < k; ++j) cnt += offs[j] >= 64 && offs[j] < cand;
+    if (cnt <= kPreUMax) a_chain = cand;
   }
   a_chain = std::min(a_chain, std::max(64, env_int("PIPEDP_SDP2_ACHAIN", 1 << 20)));
+  // dominance form (sdp_v2.cuh): min/max with offset 1 take [l+33, 128) from
+  // the chain's own shuffles once batch 3 is reached (the first batches fold
+  // the same range from the ring, so [64, 128) must fit the register list)
+  bool has1 = false;
+  int64_t n64_128 = 0;
+  for (int64_t j = 0; j < k; ++j) {
+    has1 = has1 || offs[j] == 1;
+    n64_128 += offs[j] >= 64 && offs[j] < 128;
+  }
+  if ((d->op == PIPEDP_OP_MIN || d->op == PIPEDP_OP_MAX) && has1 && n64_128 <= kPreUMax &&
+      env_int("PIPEDP_SDP2_DOM", 1) != 0)
+    a_chain = 128;
   int64_t jr = 0, jn = 0;
   for (int64_t j = 0; j < k; ++j) {
     jr += offs[j] >= a_rem;
@@ -280,17 +294,44 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   const int64_t R = 1ll << ceil_log2((uint64_t)(cover + 512));
   const int64_t count = jn - jr;
   const int NW = (int)((count + kNearMax - 1) / kNearMax);
-  const int NC = std::max(1, std::min(8, env_int("PIPEDP_SDP2_COMB", 4)));
-  int NG = std::max(1, env_int("PIPEDP_SDP2_NEAR_GROUP", 2));
   if (NW > kNearWarps) return false;
-  while (NG > 1 && sdp2_warps(NW, NG, NC, true) > 24) --NG;
-  if (sdp2_warps(NW, NG, NC, true) > 24) return false;
+  // roles: as many combiners / near groups / fetchers as the 24-warp CTA holds
+  int NC = 0, NG = 0, NF = 0;
+  bool fit = false;
+  // preference: enough fetchers (a fetcher serialises poll + L2 read per
+  // batch), then near groups, then combiners (cheap per batch)
+  const int nf_max = std::max(1, env_int("PIPEDP_SDP2_FETCH", 4));
+  const int ng_max = std::max(1, env_int("PIPEDP_SDP2_NEAR_GROUP", 2));
+  const int nc_min = std::max(1, env_int("PIPEDP_SDP2_COMB", 2));
+  for (int nf = nf_max; nf >= 1 && !fit; nf = nf > 1 ? nf / 2 : 0) {
+    for (int ng = ng_max; ng >= 1 && !fit; --ng) {
+      for (int nc = nc_min; nc >= 1 && !fit; --nc) {
+        const int f = remote ? nf : 0;
+        if (sdp2_warps(NW, ng, nc, f) <= kMaxWarpsV2) {
+          NC = nc;
+          NG = ng;
+          NF = f;
+          fit = true;
+        }
+      }
+    }
+  }
+  if (!fit) return false;
   s.ring_log2 = ceil_log2((uint64_t)R);
   s.a_rem = a_rem;
   s.a_chain = a_chain;
+  s.pub_every = std::max(1, env_int("PIPEDP_SDP2_PUB", 4));
+  s.n_pre_u = 0;
+  for (int64_t j = k - 1; j >= 0; --j) {
+    if (offs[j] < 64) continue;
+    if (offs[j] >= a_chain) break;
+    s.pre_u[s.n_pre_u++] = -(int32_t)(offs[j] * (int64_t)vb);
+  }
+  for (int i = s.n_pre_u; i < kPreUMax; ++i) s.pre_u[i] = 0;
   s.near_warps = NW;
   s.comb_warps = NC;
   s.near_group = NG;
+  s.fetchers = std::max(1, NF);
   for (int j = 0; j <= NW; ++j) s.near_lo[j] = (int32_t)(jr + (NW ? count * j / NW : 0));
   const size_t smem = sdp_v2_smem(R, kpad, vb, NW, NC);
   if (smem > kSmemBudget) return false;
@@ -300,7 +341,7 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   d->gfar = false;
   d->warp_kernel = false;
   d->smem = smem;
-  d->threads = 32 * sdp2_warps(NW, NG, NC, remote);
+  d->threads = 32 * sdp2_warps(NW, NG, NC, remote ? NF : 0);
   d->grid_extra = 0;
   SdpShape& ps = d->shape;  // the producers' view
   ps.n = n;

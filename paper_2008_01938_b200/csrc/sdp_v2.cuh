@@ -34,7 +34,9 @@ constexpr int kNearMax = 32;   // offsets per near warp (registers)
 constexpr int kNearSlots = 16; // near -> combiner partial slots
 constexpr int kNearWarps = 20; // max near warps
 constexpr int kFetchSlots = 16; // fetcher -> combiner remote partial slots
-constexpr int kPreMax = 32;     // chain-folded offsets per lane (registers)
+constexpr int kMaxWarpsV2 = 24; // 768 threads: the chain warp's register budget
+constexpr int kPreMax = 32;     // chain-folded offsets per lane in [l+33, 63] (<= 31)
+constexpr int kPreUMax = 32;    // chain-folded lane-independent offsets in [64, a_chain)
 
 struct SdpV2Shape {
   int64_t n;
@@ -43,15 +45,20 @@ struct SdpV2Shape {
   int32_t ring_log2;
   int32_t a_rem;       // offsets >= a_rem come from remote producers (1 << 30: none)
   int32_t a_chain;     // offsets in [l+33, a_chain) are folded by the chain warp itself
+  int32_t pub_every;   // writer publishes the finished prefix every pub_every batches
+  int32_t fetchers;    // fetcher warps (remote mode): batch b -> fetcher b % fetchers
   int32_t near_warps;  // NW
   int32_t comb_warps;  // NC
   int32_t near_group;  // NG warps per offset range (batch b -> warp b % NG)
   int32_t near_lo[kNearWarps + 1];  // near warp j owns offset indices [near_lo[j], near_lo[j+1])
+  int32_t n_pre_u;                    // chain-folded offsets in [64, a_chain), lane-independent:
+  int32_t pre_u[kPreUMax];            //   as negative ring byte offsets (uniform-register operands)
 };
 
-__host__ __device__ __forceinline__ int sdp2_warps(int NW, int NG, int NC, bool remote) {
-  // chain + NC + NW*NG + writer (+ fetcher) roles, skipping warp ids = 0 mod 4 (SMSP 0 is the chain's)
-  return sdp_warps_for_roles(NC + NW * NG + 1 + (remote ? 1 : 0));
+__host__ __device__ __forceinline__ int sdp2_warps(int NW, int NG, int NC, int NF) {
+  // chain + NC + NW*NG + writer + NF fetchers, skipping
+  // warp ids = 0 mod 4 (SMSP 0 is the chain's)
+  return sdp_warps_for_roles(NC + NW * NG + 1 + NF);
 }
 
 template <int OP, typename T, bool REMOTE>
@@ -69,7 +76,8 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
   T* near_part = mid_part + kMidSlots * 32;                   // [kNearSlots][NW][32]
   T* rem_part = near_part + (size_t)kNearSlots * NW * 32;                  // [kFetchSlots][32]
   int32_t* pre_scratch = reinterpret_cast<int32_t*>(rem_part + kFetchSlots * 32);  // [kPreMax][32]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(pre_scratch + (size_t)kPreMax * 32);
+  int* written_count = reinterpret_cast<int*>(pre_scratch + (size_t)kPreMax * 32);  // [4] (16 B)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(written_count + 4);
   uint64_t* batch_done = bars;                   // [kBatchBars] chain -> all
   uint64_t* written = batch_done + kBatchBars;  // [kBatchBars] writer -> chain
   uint64_t* mid_full = written + kBatchBars;    // [kMidSlots] combiner -> chain
@@ -90,6 +98,7 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
     out[i] = v;
   }
   if (tid == 0) {
+    *written_count = 0;
     for (int s = 0; s < 2 * kBatchBars + kMidSlots; ++s) mbar_init(&bars[s], 1);
     for (int s = 0; s < kNearSlots; ++s) mbar_init(&near_full[s], (unsigned)(NW > 0 ? NW : 1));
     for (int s = 0; s < kFetchSlots; ++s) mbar_init(&rem_full[s], 1);
@@ -113,40 +122,83 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
     // offsets d in [l+33, a_chain): folded here, one batch ahead, interleaved
     // with the closure (they read batches <= b-1 only) -- no hand-off latency
     // on the dependency distance these offsets leave
-    int32_t pre[kPreMax];
+    // per-lane byte-offset list in shared memory ([i][lane]: conflict-free)
+    int32_t* pre = pre_scratch;
     int npre = 0;
-    {
-      int32_t* scr = pre_scratch;  // [kPreMax][32]
-      for (int j = S.k - 1; j >= 0; --j) {
-        const int d = offs[j];
-        if (d >= S.a_chain) break;
-        if (d >= lane + 33 && npre < kPreMax) scr[(npre++) * 32 + lane] = d * (int32_t)sizeof(T);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int i = 0; i < kPreMax; ++i) pre[i] = i < npre ? scr[i * 32 + lane] : (npre ? scr[lane] : 0);
+    for (int j = S.k - 1; j >= 0; --j) {
+      const int d = offs[j];
+      if (d >= 64) break;
+      if (d >= lane + 33 && npre < kPreMax) pre[(npre++) * 32 + lane] = d * (int32_t)sizeof(T);
     }
+    for (int i = npre; i < kPreMax; ++i) pre[i * 32 + lane] = 0;  // own slot; masked below
+    __syncwarp();
     int mpre = npre;
 #pragma unroll
     for (int sh = 16; sh >= 1; sh >>= 1) mpre = max(mpre, __shfl_xor_sync(0xffffffffu, mpre, sh));
-    auto pre_fold = [&](const char* base) {  // (x) of ring[base - pre[i]], i < npre
-      T p0 = id, p1 = id;
+    // the pre-fold is split in a load phase (issued before the closure, so its
+    // shared-memory latency overlaps the closure's shuffles) and a tree phase
+    // the pre-fold runs 8 offsets per step (all loads issued before any use,
+    // branch-free: the padded list entries point at the lane's own slot and are
+    // masked to the identity), split in a load phase issued before the closure
+    // (its latency overlaps the closure's shuffles) and a combine phase after it
+    auto pre_load = [&](const char* base, T* v) {  // v[8]: partial folds
 #pragma unroll
-      for (int i = 0; i < kPreMax; i += 2) {
-        if (i < mpre) {  // warp-uniform
-          T v0 = *reinterpret_cast<const T*>(base - pre[i]);
-          T v1 = *reinterpret_cast<const T*>(base - pre[i + 1]);
-          if (!IsIdem<OP>::value || npre == 0) {  // padding folds the identity
-            v0 = i < npre ? v0 : id;
-            v1 = i + 1 < npre ? v1 : id;
-          }
-          p0 = O::apply(p0, v0);
-          p1 = O::apply(p1, v1);
+      for (int j = 0; j < 8; ++j) v[j] = id;
+      // lane-independent offsets: immediate-free uniform operands, one load each
+#pragma unroll
+      for (int i0 = 0; i0 < kPreUMax; i0 += 8) {
+        if (i0 < S.n_pre_u) {
+          T x[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) x[j] = *reinterpret_cast<const T*>(base + S.pre_u[i0 + j]);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) v[j] = O::apply(v[j], i0 + j < S.n_pre_u ? x[j] : id);
         }
       }
-      return O::apply(p0, p1);
+      // lane-dependent offsets [l+33, 63]
+      for (int i0 = 0; i0 < mpre; i0 += 8) {  // warp-uniform trip count <= 4
+        int32_t o[8];
+        T x[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = pre[(i0 + j) * 32 + lane];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) x[j] = *reinterpret_cast<const T*>(base - o[j]);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = O::apply(v[j], i0 + j < npre ? x[j] : id);
+      }
+    };
+    auto pre_tree = [&](T* v) {
+#pragma unroll
+      for (int w = 4; w >= 1; w >>= 1) {
+#pragma unroll
+        for (int i = 0; i < w; ++i) v[i] = O::apply(v[i], v[i + w]);
+      }
+      return v[0];
+    };
+    auto pre_fold = [&](const char* base) {
+      T v[8];
+      pre_load(base, v);
+      return pre_tree(v);
     };
     T pre_cur = pre_fold(reinterpret_cast<const char*>(ring + (((uint32_t)(a1 + lane) & (R - 1)) + R)));
+    // Dominance form (idempotent (x) with offset 1, a_chain = 128): x of a
+    // finished batch is the prefix-(x) of its b vector (see idem_closure), so
+    // the terms a later batch takes from it, offsets d in a 32-wide range,
+    // fold to x at the single position of the smallest such d.  srcK: that
+    // position for the range landing K batches back (d in [l+32(K-1)+1,
+    // min(l+32K, 127)]), -1 when the range holds no offset.
+    const bool dom = IsIdem<OP>::value && im.scan && S.a_chain == 128;
+    int src2 = -1, src3 = -1, src4 = -1;
+    if (dom) {
+      for (int j = S.k - 1; j >= 0; --j) {  // ascending d
+        const int d = offs[j];
+        if (d > 127) break;
+        if (src2 < 0 && d >= lane + 33 && d <= lane + 64) src2 = lane + 64 - d;
+        if (src3 < 0 && d >= lane + 65 && d <= lane + 96) src3 = lane + 96 - d;
+        if (src4 < 0 && d >= lane + 97 && d <= lane + 128) src4 = lane + 128 - d;
+      }
+    }
+    T xm1 = id, xm2 = id, xm3 = id;  // x of batches b, b-1, b-2 after iteration b
     PROF_DECL(p_wait);
     PROF_DECL(p_fold);
     const long long p_start = PROF_NOW();
@@ -165,16 +217,29 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
       PROF_ADD(p_wait, t0);
       t0 = PROF_NOW();
       T acc = O::apply(O::apply(mid_part[slot * 32 + lane], pre_cur), nxt);
-      // batch b+1's chain-local offsets: independent of this batch's closure
-      const T pre_next =
-          pre_fold(reinterpret_cast<const char*>(ring + (((uint32_t)(c + 32) & (R - 1)) + R)));
-      if (IsIdem<OP>::value) {
+      if (dom && b >= 3) {
+        // batch b+1's chain-local offsets from x of batches b-1, b-2, b-3 by
+        // the closure's prefix structure: one shuffle per batch range
         idem_closure<OP, T>(acc, nxt, im);
+        const T v2 = shfl_idx(xm1, src2 < 0 ? 0 : src2);
+        const T v3 = shfl_idx(xm2, src3 < 0 ? 0 : src3);
+        const T v4 = shfl_idx(xm3, src4 < 0 ? 0 : src4);
+        pre_cur = O::apply(O::apply(src2 < 0 ? id : v2, src3 < 0 ? id : v3), src4 < 0 ? id : v4);
       } else {
-        nxt = id;
-        LaSteps<OP, T, 1>::run(acc, nxt, lm);
+        // batch b+1's chain-local offsets: independent of this batch's closure
+        T pv[8];
+        pre_load(reinterpret_cast<const char*>(ring + (((uint32_t)(c + 32) & (R - 1)) + R)), pv);
+        if (IsIdem<OP>::value) {
+          idem_closure<OP, T>(acc, nxt, im);
+        } else {
+          nxt = id;
+          LaSteps<OP, T, 1>::run(acc, nxt, lm);
+        }
+        pre_cur = pre_tree(pv);
       }
-      pre_cur = pre_next;
+      xm3 = xm2;
+      xm2 = xm1;
+      xm1 = acc;
       if (c < n) {
         ring[pos - R] = acc;
         ring[pos] = acc;
@@ -282,43 +347,49 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
     PROF_FLUSH(16 + (j == 0 ? 0 : 2), p_nw);
     PROF_FLUSH(17 + (j == 0 ? 0 : 2), p_nf);
     (void)g;
-  } else if (REMOTE && role == NC + NW * NG + 1) {
-    // ================================ fetcher ===============================
-    // copies the remote producers' partials into shared slots ahead of the
-    // combiners, so no global-memory latency sits on the combine path
-    // eight batches per round: lane i < 8 polls batch b0+i, then every lane
-    // loads its cell of all eight partials (eight independent L2 reads)
-    for (int64_t b0 = 0; b0 < nb; b0 += 8) {
-      if (b0 >= kFetchSlots) wait_batches(batch_done, b0 + 8 - kFetchSlots);  // slots consumed
-      if (lane < 8 && b0 + lane < nb)
-        spin_eq_gpu(RM.ready + (int)((b0 + lane) % kRemSlots), (int)(b0 + lane + 1), 32);
+  } else if (REMOTE && role > NC + NW * NG && role <= NC + NW * NG + S.fetchers) {
+    // ================================ fetchers ==============================
+    // copy the remote producers' partials into shared slots ahead of the
+    // combiners (batch b -> fetcher b % kFetchers), so no global-memory
+    // latency sits on the combine path
+    const int f = role - (NC + NW * NG + 1);
+    for (int64_t b = f; b < nb; b += S.fetchers) {
+      const int fs = (int)(b % kFetchSlots);
+      wait_batches(batch_done, b + 1 - kFetchSlots);  // slot consumed by the combiner
+      if (lane == 0) spin_eq_gpu(RM.ready + (int)(b % kRemSlots), (int)(b + 1), 32);
       __syncwarp();
       fence_acquire_gpu();
-      T v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i)
-        v[i] = b0 + i < nb ? ldv_cg<T, int64_t>(reinterpret_cast<const int64_t*>(RM.part) +
-                                                (int)((b0 + i) % kRemSlots) * 32 + lane)
-                           : T(0);
-#pragma unroll
-      for (int i = 0; i < 8; ++i) rem_part[(int)((b0 + i) % kFetchSlots) * 32 + lane] = v[i];
+      rem_part[fs * 32 + lane] =
+          ldv_cg<T, int64_t>(reinterpret_cast<const int64_t*>(RM.part) + (int)(b % kRemSlots) * 32 + lane);
       __syncwarp();
-      if (lane < 8 && b0 + lane < nb) mbar_arrive(&rem_full[(int)((b0 + lane) % kFetchSlots)]);
+      if (lane == 0) mbar_arrive(&rem_full[fs]);
     }
   } else if (role == NC + NW * NG) {
     // ================================= writer ===============================
+    PROF_DECL(p_ww);
+    PROF_DECL(p_wp);
     for (int64_t b = 0; b < nb; ++b) {
+      long long t0 = PROF_NOW();
       mbar_wait(&batch_done[b % kBatchBars], (unsigned)((b / kBatchBars) & 1));
+      PROF_ADD(p_ww, t0);
       const int64_t c = a1 + 32 * b + lane;
       if (c < n) out[c] = (int64_t)ring[(uint32_t)c & (R - 1)];
       __syncwarp();
       if (lane == 0) mbar_arrive(&written[b % kBatchBars]);
-      if (REMOTE && ((b + 1) % kPubEvery == 0 || b + 1 == nb)) {
-        __threadfence();
+      if (REMOTE && ((b + 1) % S.pub_every == 0 || b + 1 == nb)) {
+        t0 = PROF_NOW();
         __syncwarp();
-        if (lane == 0) st_release_gpu(reinterpret_cast<long long*>(RM.published), (long long)(b + 1));
+        if (lane == 0) {  // one gpu-scope release per publish (not one fence per lane)
+          __threadfence();
+          st_release_gpu(reinterpret_cast<long long*>(RM.published), (long long)(b + 1));
+        }
+        __syncwarp();
+        PROF_ADD(p_wp, t0);
       }
     }
+    PROF_FLUSH(28, p_ww);
+    PROF_FLUSH(29, p_wp);
+    PROF_FLUSH(29, p_wp);
   }
 }
 

@@ -1,3 +1,3 @@
-timeout 300 python -m pytest tests/test_gpu_mcm.py tests/test_gpu_batch.py tests/test_dropin.py -x -q > gpurun_out/pytest_m.txt 2>&1; tail -3 gpurun_out/pytest_m.txt
-for w in c2 c3 c4 c5a c5b; do timeout 200 python bench.py --workload $w --no-cpu-baseline --steps 3 > gpurun_out/bench_$w.json 2>&1; python -c "
-import json; d=json.loads(open('gpurun_out/bench_$w.json').read().strip().splitlines()[-1]); print('$w', d['roofline']['kernel'], round(d['ms_per_step'],3), '%.3e'%d['value'], 'e2e ms', round(d['e2e']['ms_per_step'],2), '%.3e'%d['e2e']['value'], d['parity'])" || tail -5 gpurun_out/bench_$w.json; done
+timeout 300 python -m pytest tests/test_gpu_sdp.py tests/test_gpu_batch.py -x -q > gpurun_out/pytest_s.txt 2>&1; tail -2 gpurun_out/pytest_s.txt
+export PIPEDP_LIB=paper_2008_01938_b200/_lib/libpipedp_cuda_prof.so
+timeout 60 python tools/v2_profile.py 22

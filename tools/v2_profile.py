@@ -21,6 +21,6 @@ nb = max(p[3], 1)
 print(plan.describe(), f"{e0.elapsed_time(e1):.2f} ms", "batches", nb)
 names = {0: "chain.wait_mid", 1: "chain.work", 2: "chain.total", 8: "comb.wait_chain", 9: "comb.wait_near",
          10: "comb.wait_remote", 11: "comb.work", 16: "near0.wait", 17: "near0.fold", 18: "nearX.wait(sum)",
-         19: "nearX.fold(sum)", 24: "prod.wait_pub(warp0)", 25: "prod.fold+combine(warp0)"}
+         19: "nearX.fold(sum)", 28: "writer.wait_chain", 29: "writer.publish", 24: "prod.wait_pub(warp0)", 25: "prod.fold+combine(warp0)"}
 for i, nm in names.items():
     print(f"  {nm:28s} {p[i] / nb:10.1f} cycles/batch (summed over warps)")
