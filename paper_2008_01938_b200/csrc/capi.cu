@@ -301,17 +301,22 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   // preference: enough fetchers (a fetcher serialises poll + L2 read per
   // batch), then near groups, then combiners (cheap per batch)
   const int nf_max = std::max(1, env_int("PIPEDP_SDP2_FETCH", 4));
+  const int nw_max = std::max(1, std::min(8, env_int("PIPEDP_SDP2_WRITERS", 1)));
   const int ng_max = std::max(1, env_int("PIPEDP_SDP2_NEAR_GROUP", 2));
   const int nc_min = std::max(1, env_int("PIPEDP_SDP2_COMB", 2));
+  int NWR = 1;
   for (int nf = nf_max; nf >= 1 && !fit; nf = nf > 1 ? nf / 2 : 0) {
-    for (int ng = ng_max; ng >= 1 && !fit; --ng) {
-      for (int nc = nc_min; nc >= 1 && !fit; --nc) {
-        const int f = remote ? nf : 0;
-        if (sdp2_warps(NW, ng, nc, f) <= kMaxWarpsV2) {
-          NC = nc;
-          NG = ng;
-          NF = f;
-          fit = true;
+    for (int nwr = nw_max; nwr >= 1 && !fit; nwr = nwr > 1 ? nwr / 2 : 0) {
+      for (int ng = ng_max; ng >= 1 && !fit; --ng) {
+        for (int nc = nc_min; nc >= 1 && !fit; --nc) {
+          const int f = remote ? nf : 0, wr = remote ? nwr : 1;
+          if (sdp2_warps(NW, ng, nc, f, wr) <= kMaxWarpsV2) {
+            NC = nc;
+            NG = ng;
+            NF = f;
+            NWR = wr;
+            fit = true;
+          }
         }
       }
     }
@@ -332,6 +337,7 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   s.comb_warps = NC;
   s.near_group = NG;
   s.fetchers = std::max(1, NF);
+  s.writers = NWR;
   for (int j = 0; j <= NW; ++j) s.near_lo[j] = (int32_t)(jr + (NW ? count * j / NW : 0));
   const size_t smem = sdp_v2_smem(R, kpad, vb, NW, NC);
   if (smem > kSmemBudget) return false;
@@ -341,7 +347,7 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   d->gfar = false;
   d->warp_kernel = false;
   d->smem = smem;
-  d->threads = 32 * sdp2_warps(NW, NG, NC, remote ? NF : 0);
+  d->threads = 32 * sdp2_warps(NW, NG, NC, remote ? NF : 0, NWR);
   d->grid_extra = 0;
   SdpShape& ps = d->shape;  // the producers' view
   ps.n = n;
@@ -349,6 +355,7 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   ps.a1 = (int32_t)a1;
   ps.a_remote = a_rem;
   ps.remote_warps = 0;
+  ps.writers = NWR;
   if (remote) {
     ps.remote_warps = std::min(24, env_int("PIPEDP_SDP_REMOTE_WARPS", 16));
     d->grid_extra = std::min(sm_count() - 1, env_int("PIPEDP_SDP_REMOTE_CTAS", 64));
@@ -375,6 +382,7 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
   s.a_mid = kAMid;
   s.a_remote = 1 << 30;
   s.remote_warps = 0;
+  s.writers = 1;
   d->grid_extra = 0;
   d->remote = false;
   const int64_t kpad = (k + 3) & ~3ll;

@@ -57,13 +57,14 @@ struct SdpShape {
   int32_t mid_warps;
   int32_t far_warps;
   int32_t remote_warps;  // warps per producer CTA
+  int32_t writers;       // finisher writer warps publishing progress (published[0..writers))
 };
 
 // Global workspace of the multi-CTA mode (zeroed before every launch).
 struct SdpRemote {
   void* part;               // [kRemSlots][32] T
   int* ready;               // [kRemSlots] batch+1
-  unsigned long long* published;  // batches written to the table and released
+  unsigned long long* published;  // [writers] batches < published[w] of writer w's share are in HBM
 };
 
 template <typename T, typename S>
@@ -771,7 +772,9 @@ __device__ __forceinline__ void sdp_producer(const SdpShape& S, const int64_t* _
     long long t0 = PROF_NOW();
     if (tid == 0) {
       const long long need = (long long)max(b + 1 - look, b + 1 - (int64_t)kRemSlots);
-      spin_ge_gpu64(reinterpret_cast<const long long*>(RM.published), need, 128);
+      // every writer's share below `need` (batch y belongs to writer y % writers)
+      for (int w = 0; w < S.writers; ++w)
+        spin_ge_gpu64(reinterpret_cast<const long long*>(RM.published) + w, need, 128);
     }
     __syncthreads();
     PROF_ADD(p_wait, t0);

@@ -47,6 +47,7 @@ struct SdpV2Shape {
   int32_t a_chain;     // offsets in [l+33, a_chain) are folded by the chain warp itself
   int32_t pub_every;   // writer publishes the finished prefix every pub_every batches
   int32_t fetchers;    // fetcher warps (remote mode): batch b -> fetcher b % fetchers
+  int32_t writers;     // writer warps: batch b -> writer b % writers (each publishes its share)
   int32_t near_warps;  // NW
   int32_t comb_warps;  // NC
   int32_t near_group;  // NG warps per offset range (batch b -> warp b % NG)
@@ -55,10 +56,10 @@ struct SdpV2Shape {
   int32_t pre_u[kPreUMax];            //   as negative ring byte offsets (uniform-register operands)
 };
 
-__host__ __device__ __forceinline__ int sdp2_warps(int NW, int NG, int NC, int NF) {
-  // chain + NC + NW*NG + writer + NF fetchers, skipping
+__host__ __device__ __forceinline__ int sdp2_warps(int NW, int NG, int NC, int NF, int NWR) {
+  // chain + NC + NW*NG + NWR writers + NF fetchers, skipping
   // warp ids = 0 mod 4 (SMSP 0 is the chain's)
-  return sdp_warps_for_roles(NC + NW * NG + 1 + NF);
+  return sdp_warps_for_roles(NC + NW * NG + NWR + NF);
 }
 
 template <int OP, typename T, bool REMOTE>
@@ -347,12 +348,12 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
     PROF_FLUSH(16 + (j == 0 ? 0 : 2), p_nw);
     PROF_FLUSH(17 + (j == 0 ? 0 : 2), p_nf);
     (void)g;
-  } else if (REMOTE && role > NC + NW * NG && role <= NC + NW * NG + S.fetchers) {
+  } else if (REMOTE && role >= NC + NW * NG + S.writers && role < NC + NW * NG + S.writers + S.fetchers) {
     // ================================ fetchers ==============================
     // copy the remote producers' partials into shared slots ahead of the
     // combiners (batch b -> fetcher b % kFetchers), so no global-memory
     // latency sits on the combine path
-    const int f = role - (NC + NW * NG + 1);
+    const int f = role - (NC + NW * NG + S.writers);
     for (int64_t b = f; b < nb; b += S.fetchers) {
       const int fs = (int)(b % kFetchSlots);
       wait_batches(batch_done, b + 1 - kFetchSlots);  // slot consumed by the combiner
@@ -364,11 +365,15 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
       __syncwarp();
       if (lane == 0) mbar_arrive(&rem_full[fs]);
     }
-  } else if (role == NC + NW * NG) {
-    // ================================= writer ===============================
+  } else if (role >= NC + NW * NG && role < NC + NW * NG + S.writers) {
+    // ================================= writers ==============================
+    // batch b -> writer b % writers; each writer's gpu-scope release of its own
+    // share overlaps the other writers' stores
+    const int w = role - (NC + NW * NG), NWR = S.writers;
     PROF_DECL(p_ww);
     PROF_DECL(p_wp);
-    for (int64_t b = 0; b < nb; ++b) {
+    int done = 0;
+    for (int64_t b = w; b < nb; b += NWR) {
       long long t0 = PROF_NOW();
       mbar_wait(&batch_done[b % kBatchBars], (unsigned)((b / kBatchBars) & 1));
       PROF_ADD(p_ww, t0);
@@ -376,12 +381,12 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
       if (c < n) out[c] = (int64_t)ring[(uint32_t)c & (R - 1)];
       __syncwarp();
       if (lane == 0) mbar_arrive(&written[b % kBatchBars]);
-      if (REMOTE && ((b + 1) % S.pub_every == 0 || b + 1 == nb)) {
+      if (REMOTE && (++done % S.pub_every == 0 || b + NWR >= nb)) {
         t0 = PROF_NOW();
         __syncwarp();
         if (lane == 0) {  // one gpu-scope release per publish (not one fence per lane)
           __threadfence();
-          st_release_gpu(reinterpret_cast<long long*>(RM.published), (long long)(b + 1));
+          st_release_gpu(reinterpret_cast<long long*>(RM.published) + w, (long long)(b + 1));
         }
         __syncwarp();
         PROF_ADD(p_wp, t0);
