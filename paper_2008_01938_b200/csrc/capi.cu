@@ -200,6 +200,7 @@ struct SdpDispatch {
   size_t smem;
   int wpb;  // warp kernel: warps per block
   bool v2;   // offset-partitioned single-instance pipeline (sdp_v2.cuh)
+  bool serial;  // tiny offset sets: one-thread chain (sdp_serial_thread / sdp_serial_regs)
   SdpV2Shape s2;
 };
 
@@ -405,6 +406,8 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
   }
   d->warp_kernel = false;
   d->small = a1 < 64;
+  d->serial = batch == 1 && d->small && k <= 8 && env_int("PIPEDP_SDP_SERIAL", 1) != 0;
+
   if (d->small) {
     s.ring_log2 = ceil_log2((uint64_t)(a1 + 128));
     s.ring_cover = (int32_t)a1;
@@ -522,6 +525,11 @@ template <int OP, typename T, bool ASSOC>
 int launch_sdp_t(const SdpDispatch& d, int64_t batch, const int64_t* offs, const int64_t* init,
                  int64_t* out, const SdpRemote& rm, cudaStream_t st) {
   if (ASSOC && d.v2 && !(OP == kModAdd && sizeof(T) == 8)) return launch_v2<OP, T>(d, offs, init, out, rm, st);
+  if (d.serial) {
+    sdp_serial_thread<OP, T><<<1, 32, 0, st>>>(d.shape.n, d.shape.k, offs, init, out);
+    CK(cudaGetLastError());
+    return PIPEDP_OK;
+  }
   if (d.warp_kernel) {
     return d.small ? launch_warp<OP, T, true, ASSOC>(d, batch, offs, init, out, st)
                    : launch_warp<OP, T, false, ASSOC>(d, batch, offs, init, out, st);
@@ -551,6 +559,7 @@ int launch_sdp(const SdpDispatch& d, int64_t batch, const int64_t* offs, const i
 }
 
 const char* sdp_kernel_name(const SdpDispatch& d) {
+  if (d.serial) return "sdp_serial_thread";
   if (d.v2) return d.remote ? "sdp_v2_multi" : "sdp_v2_cta";
   if (d.warp_kernel) return "sdp_batch_warp";
   if (d.small) return "sdp_pipeline_cta[chain]";

@@ -987,3 +987,55 @@ __global__ void sdp_chain_fold_probe(int64_t batches, uint32_t hi, uint32_t m32,
 }
 
 }  // namespace pipedp_dev
+
+namespace pipedp_dev {
+
+// -----------------------------------------------------------------------------
+// Serial chain for tiny offset sets (k <= 8, a_1 < 64; BASELINE config 1 is
+// the Fibonacci recurrence, offsets {2, 1}): when a cell has only a handful of
+// operands, the warp-wide pipeline's shuffle hand-off costs more than doing
+// the recurrence in one thread.  One thread walks the cells in order with the
+// reference's exact fold order (sdp.cpp:52-59: assign ST[i-a_1], then fold
+// a_2..a_k), keeping the previous cell in a register (offset 1 is the only
+// operand that is not already in shared memory when the cell starts) and the
+// last 64 cells in a shared ring; lanes 1..31 stream the finished cells to HBM
+// in coalesced 32-cell rows.
+template <int OP, typename T>
+__global__ void __launch_bounds__(32)
+    sdp_serial_thread(const int64_t n, const int32_t k, const int64_t* __restrict__ g_offsets,
+                      const int64_t* __restrict__ g_init, int64_t* __restrict__ out) {
+  using O = SemiOp<OP, T>;
+  __shared__ T ring[64];
+  __shared__ T row[2][32];
+  __shared__ int32_t offs[8];
+  const int lane = threadIdx.x;
+  if (lane < k) offs[lane] = (int32_t)g_offsets[lane];
+  __syncwarp();
+  const int a1 = offs[0];
+  for (int i = lane; i < a1; i += 32) {
+    ring[i & 63] = (T)g_init[i];
+    out[i] = g_init[i];
+  }
+  __syncwarp();
+  const bool last_is_1 = offs[k - 1] == 1;
+  const int kk = last_is_1 ? k - 1 : k;  // operands read from the ring
+  T prev = ring[(a1 - 1) & 63];
+  for (int64_t c0 = a1; c0 < n; c0 += 32) {
+    const int64_t cend = c0 + 32 < n ? c0 + 32 : n;
+    const int rb = (int)((c0 / 32) & 1);
+    if (lane == 0) {
+      for (int64_t c = c0; c < cend; ++c) {
+        T acc = ring[(c - offs[0]) & 63];
+        for (int j = 1; j < kk; ++j) acc = O::apply(acc, ring[(c - offs[j]) & 63]);
+        if (last_is_1) acc = kk > 0 ? O::apply(acc, prev) : prev;
+        ring[c & 63] = acc;
+        row[rb][c - c0] = acc;
+        prev = acc;
+      }
+    }
+    __syncwarp();
+    if (c0 + lane < cend) out[c0 + lane] = (int64_t)row[rb][lane];
+  }
+}
+
+}  // namespace pipedp_dev
