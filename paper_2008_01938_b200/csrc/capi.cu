@@ -735,8 +735,28 @@ std::vector<unsigned long long> mcm_tiled_tasks(int N) {
   return out;
 }
 
+size_t mcm_square_bytes(int64_t n, size_t vb) {
+  const int64_t P = n + 1;
+  return (size_t)(P * P + 1) * vb + (size_t)(n + 1 + 4) * 4;
+}
+
 int mcm_smem_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split, cudaStream_t st) {
   const int64_t n = P->n;
+  const size_t sq = mcm_square_bytes(n, bits / 8);
+  if (sq <= kSmemBudget && env_int("PIPEDP_MCM_SQUARE", 1) != 0) {
+    // row-major square table: incremental operand addresses (mcm_smem_square)
+    if (bits == 32) {
+      CK(cudaFuncSetAttribute(mcm_smem_square<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq));
+      mcm_smem_square<uint32_t><<<(unsigned)P->batch, 128, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
+                                                                      split, P->d_overflow);
+    } else {
+      CK(cudaFuncSetAttribute(mcm_smem_square<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq));
+      mcm_smem_square<int64_t><<<(unsigned)P->batch, 128, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
+                                                                     split, P->d_overflow);
+    }
+    CK(cudaGetLastError());
+    return PIPEDP_OK;
+  }
   if (bits == 32) {
     CK(cudaFuncSetAttribute(mcm_smem_cta<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)P->d.smem32));
@@ -1096,7 +1116,9 @@ int32_t pipedp_mcm_plan_execute(pipedp_mcm_plan_t P, int64_t* d_cells, int64_t* 
 int32_t pipedp_mcm_plan_describe(pipedp_mcm_plan_t P, char* name, size_t cap, int32_t* bits,
                                  int32_t* launches) {
   if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
-  const char* nm = P->d.kernel == PIPEDP_MCM_SMEM         ? "mcm_smem_cta"
+  const bool square = mcm_square_bytes(P->n, (P->last_bits ? P->last_bits : P->d.bits) / 8) <= kSmemBudget &&
+                      env_int("PIPEDP_MCM_SQUARE", 1) != 0;
+  const char* nm = P->d.kernel == PIPEDP_MCM_SMEM         ? (square ? "mcm_smem_square" : "mcm_smem_cta")
                    : P->d.kernel == PIPEDP_MCM_TOURNAMENT ? "mcm_tournament"
                    : (P->d.kernel == PIPEDP_MCM_TILED && P->last_bits != 64)
                        ? (P->d.tile == 32 ? "mcm_tiled_kernel<32>" : "mcm_tiled_kernel<64>")

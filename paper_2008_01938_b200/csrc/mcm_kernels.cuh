@@ -406,3 +406,81 @@ __global__ void mcm_bruteforce_kernel(const int64_t* __restrict__ p, int n, int6
 }
 
 }  // namespace pipedp_dev
+
+namespace pipedp_dev {
+
+// -----------------------------------------------------------------------------
+// Batched small-n MCM (BASELINE config 5a: 65,536 instances of n = 64), one CTA
+// per instance.  The instance's table lives in shared memory as a row-major
+// (n+1) x (n+1) square (pitch P = n + 1, odd-stride rows keep a warp's loads
+// on distinct banks), so term j of cell (r, c) reads
+//   left  = M[r][r+j-1]   (walks along row r:      +1 per term)
+//   right = M[r+j][c]     (walks down column c:    +P per term)
+// with incremental 32-bit addresses -- no per-term index arithmetic.  Lanes
+// per cell G = 2^lg grows as the diagonal shortens; each lane scans its terms
+// j ascending with strict '<' and the G partials reduce lexicographically on
+// (value, j): the reference's first-min split (mcm.cpp:95-104).
+template <typename T>
+__global__ void __launch_bounds__(128)
+    mcm_smem_square(int32_t n, int64_t batch, const int64_t* __restrict__ g_dims,
+                    int64_t* __restrict__ out_cells, int64_t* __restrict__ out_split,
+                    int* __restrict__ overflow) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int64_t inst = blockIdx.x;
+  if (inst >= batch) return;
+  const int P = n + 1;
+  T* M = reinterpret_cast<T*>(smem);                         // [P][P], row r = 1..n
+  int32_t* p = reinterpret_cast<int32_t*>(M + P * P + 1);    // dims p_0..p_n
+  const int64_t cc = (int64_t)n * (n + 1) / 2;
+  const int64_t* gd = g_dims + inst * (n + 1);
+  int64_t* oc = out_cells + inst * (cc + 1);
+  int64_t* os = out_split + inst * (cc + 1);
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i <= n; i += nt) {
+    p[i] = (int32_t)gd[i];
+    if (i >= 1) M[i * P + i] = T(0);  // base cells m[i][i] = 0
+    oc[i] = 0;                        // slot 0 and base cells 1..n (mcm.cpp:77-83)
+    os[i] = 0;
+  }
+  __syncthreads();
+  bool ovf = false;
+  int64_t db = 0;  // lin(r, r+D) = db(D) + r, db(D) = D*n - D(D-1)/2
+  for (int D = 1; D < n; ++D) {
+    db += n - (D - 1);
+    const int ncell = n - D;
+    int lg = 0;  // lanes per cell: spread the D terms when the diagonal is short
+    while (lg < 5 && (ncell << (lg + 1)) <= nt && (1 << lg) < D) ++lg;
+    const int G = 1 << lg;
+    const int slots = (nt >> lg) << lg;
+    for (int base = 0; base < ncell * G; base += slots) {
+      const int t = base + tid;
+      const bool live = tid < slots && t < ncell * G;
+      const int r = 1 + (t >> lg), q = t & (G - 1), c = r + D;
+      McmBest<T> best{mcm_max_value<T>(), 0};
+      if (live) {
+        const T prc = (T)p[r - 1] * (T)p[c];
+        const T* L = M + r * P + r - 1;  // m[r][r+j-1] at L[j]
+        const T* Rt = M + r * P + c;     // m[r+j][c]   at Rt[j*P]
+        const int32_t* pk = p + r - 1;   // p[r+j-1]    at pk[j]
+        for (int j = 1 + q; j <= D; j += G) {
+          const T cost = L[j] + Rt[j * P] + prc * (T)pk[j];
+          if (cost < best.v) {  // j ascending in this lane: first minimum
+            best.v = cost;
+            best.j = j;
+          }
+        }
+      }
+      if (G > 1) best = mcm_group_reduce(best, G);
+      if (live && q == 0) {
+        M[r * P + c] = best.v;
+        oc[db + r] = (int64_t)best.v;
+        os[db + r] = best.j;
+        if (sizeof(T) == 4 && (uint64_t)best.v >= kMcm32Limit) ovf = true;
+      }
+    }
+    __syncthreads();
+  }
+  if (ovf) atomicOr(overflow, 1);
+}
+
+}  // namespace pipedp_dev
