@@ -56,6 +56,7 @@ struct McmTiled {
   int64_t* out_cells;          // reference layout (diagonal-major, slot 0)
   int64_t* out_split;
   int* overflow;
+  int32_t blocked;             // 1: blocked in-tile pipeline (8x8 sub-blocks), 0: CTA-wide steps
 };
 
 __host__ __device__ __forceinline__ int64_t tiled_index(int64_t I, int64_t J, int64_t N) {

@@ -107,3 +107,13 @@ def test_batch(gpu, oracle):
     for inst, (t, split) in zip(insts, gpu.solve_mcm_batch(insts)):
         wc, _, ws = oracle.mcm_solve(inst.dims)
         assert np.array_equal(t.cells, wc) and np.array_equal(split, ws)
+
+
+@pytest.mark.parametrize("t32_maxn", ["0", "100000"])
+@pytest.mark.parametrize("n", [33, 64, 130, 300])
+def test_tiled_blocked_variant(gpu, oracle, n, t32_maxn, monkeypatch):
+    # the 8x8 sub-blocked in-tile pipeline (PIPEDP_MCM_BLOCKED=1) gives the same tables
+    monkeypatch.setenv("PIPEDP_MCM_T32_MAXN", t32_maxn)
+    monkeypatch.setenv("PIPEDP_MCM_BLOCKED", "1")
+    _check(gpu, oracle, oracle.generate_mcm(n, 5 + n, 1, 100), 4)
+    _check(gpu, oracle, [7] * (n + 1), 4)
