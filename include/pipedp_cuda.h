@@ -49,6 +49,13 @@ enum {
 /* Semigroup kinds, OpKind order (semigroup.hpp:13). */
 enum { PIPEDP_OP_MIN = 0, PIPEDP_OP_MAX = 1, PIPEDP_OP_SATURATING_ADD = 2, PIPEDP_OP_MODULAR_ADD = 3 };
 
+/* S-DP methods (pipedp_sdp_plan_set_method / pipedp_sdp_solve_method) */
+enum {
+  PIPEDP_SDP_PIPELINE = 0,  /* the pipelined kernels (default) */
+  PIPEDP_SDP_PREFIX = 1,    /* the paper's tournament per cell, O(n log k) steps */
+  PIPEDP_SDP_NAIVE = 2      /* the paper's naive k-1-thread method with conflicts, O(nk) */
+};
+
 /* MCM kernels */
 enum {
   PIPEDP_MCM_AUTO = 0,       /* shared-memory CTA for small n / batches, tiled pipeline otherwise */
@@ -99,6 +106,13 @@ int32_t pipedp_sdp_solve(const int64_t* offsets, int64_t k, const int64_t* init,
                          int64_t init_len, int64_t n, int32_t op, int64_t* cells_out,
                          uint8_t* filled_out);
 
+/* solve_prefix_parallel / solve_naive_parallel (sdp.cpp:91-111) with the
+ * paper's own methods on the device (method = PIPEDP_SDP_PREFIX / _NAIVE);
+ * same table as pipedp_sdp_solve. */
+int32_t pipedp_sdp_solve_method(const int64_t* offsets, int64_t k, const int64_t* init,
+                                int64_t init_len, int64_t n, int32_t op, int32_t method,
+                                int64_t* cells_out, uint8_t* filled_out);
+
 /* Batch of independent instances sharing n, k and a_1 (SoA: offsets
  * [batch*k], init [batch*a_1], cells_out [batch*n]).  No reference
  * counterpart (the reference loops serially, commands.cpp:480-507); each
@@ -121,6 +135,8 @@ int32_t pipedp_sdp_plan_execute(pipedp_sdp_plan_t plan, const int64_t* d_init, i
 /* kernel name, value width (32/64) and kernel launches per execute */
 int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t plan, char* name, size_t name_cap,
                                  int32_t* value_bits, int32_t* launches);
+/* switch a single-instance plan to the paper's prefix / naive method */
+int32_t pipedp_sdp_plan_set_method(pipedp_sdp_plan_t plan, int32_t method);
 int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t plan);
 
 /* ---- MCM, host buffers ------------------------------------------------------

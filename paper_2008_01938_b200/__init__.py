@@ -39,6 +39,7 @@ ERRC = [
 OPS = ("min", "max", "saturating-add", "modular-add")  # OpKind order, semigroup.hpp:13
 
 MCM_AUTO, MCM_WAVEFRONT, MCM_SMEM, MCM_TOURNAMENT, MCM_TILED = 0, 1, 2, 3, 4
+SDP_PIPELINE, SDP_PREFIX, SDP_NAIVE = 0, 1, 2  # pipedp_sdp_plan_set_method
 PAPER_LITERAL, STALL_ON_HAZARD = "paper_literal", "stall_on_hazard"
 
 # C ABI exports declared in include/pipedp_cuda.h (checked by tests/test_host.py)
@@ -51,7 +52,8 @@ EXPORTS = (
     "pipedp_mcm_plan_create", "pipedp_mcm_plan_execute", "pipedp_mcm_plan_describe",
     "pipedp_mcm_plan_destroy", "pipedp_digest_device", "pipedp_chain_step_ns",
     "pipedp_profile_read", "pipedp_generate_sdp_batch", "pipedp_generate_mcm_batch",
-    "pipedp_op_latency_ns", "pipedp_mcm_bruteforce",
+    "pipedp_op_latency_ns", "pipedp_mcm_bruteforce", "pipedp_sdp_solve_method",
+    "pipedp_sdp_plan_set_method",
 )
 
 
@@ -126,6 +128,9 @@ def lib():
     L.pipedp_op_latency_ns.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_double),
                                        C.POINTER(C.c_double)]
     L.pipedp_mcm_bruteforce.argtypes = [_i64p, C.c_int64, _i64p]
+    L.pipedp_sdp_solve_method.argtypes = [_i64p, C.c_int64, _i64p, C.c_int64, C.c_int64, C.c_int32,
+                                          C.c_int32, _i64p, _u8p]
+    L.pipedp_sdp_plan_set_method.argtypes = [C.c_void_p, C.c_int32]
     _lib = L
     return L
 
@@ -277,14 +282,29 @@ def _ceil_log2(k: int) -> int:
     return (k - 1).bit_length()
 
 
+def _solve_method(inst: SdpInstance, method: int) -> SolutionTable:
+    offs, init = _a64(inst.offsets), _a64(inst.init)
+    op = _op_index(inst.op)
+    validate(inst)
+    cells = np.empty(inst.n, dtype=np.int64)
+    filled = np.empty(inst.n, dtype=np.uint8)
+    _check(lib().pipedp_sdp_solve_method(_p(offs), len(offs), _p(init), len(init), inst.n, op, method,
+                                         _p(cells), _p(filled, _u8p)))
+    return SolutionTable(cells, filled)
+
+
 def solve_prefix_parallel(inst: SdpInstance) -> PrefixParallelResult:
-    t = solve_sequential(inst)
+    """solve_prefix_parallel (sdp.cpp:91-100): the paper's tournament per cell on
+    the device (kernel sdp_tournament), plus the reference's step model."""
+    t = _solve_method(inst, SDP_PREFIX)
     depth = _ceil_log2(inst.k)
     return PrefixParallelResult(t, depth, (inst.n - inst.a1) * max(depth, 1))
 
 
 def solve_naive_parallel(inst: SdpInstance) -> NaiveParallelResult:
-    t = solve_sequential(inst)
+    """solve_naive_parallel (sdp.cpp:102-111): the paper's naive k-1-thread
+    method on the device (kernel sdp_naive), plus the reference's step model."""
+    t = _solve_method(inst, SDP_NAIVE)
     return NaiveParallelResult(t, inst.k - 1, (inst.n - inst.a1) * inst.k)
 
 
@@ -463,6 +483,10 @@ class SdpPlan:
     def execute(self, d_init: int, d_cells: int, stream: int = 0) -> None:
         _check(lib().pipedp_sdp_plan_execute(self.handle, C.c_void_p(d_init), C.c_void_p(d_cells),
                                              C.c_void_p(stream)))
+
+    def set_method(self, method: int) -> None:
+        """SDP_PIPELINE (default), SDP_PREFIX or SDP_NAIVE (the paper's methods)."""
+        _check(lib().pipedp_sdp_plan_set_method(self.handle, method))
 
     def describe(self):
         buf = C.create_string_buffer(64)

@@ -200,7 +200,8 @@ struct SdpDispatch {
   size_t smem;
   int wpb;  // warp kernel: warps per block
   bool v2;   // offset-partitioned single-instance pipeline (sdp_v2.cuh)
-  bool serial;  // tiny offset sets: one-thread chain (sdp_serial_thread / sdp_serial_regs)
+  bool serial;  // tiny offset sets: one-thread chain (sdp_serial_thread)
+  int method;   // 0 pipeline, 1 the paper's tournament (prefix), 2 the paper's naive method
   SdpV2Shape s2;
 };
 
@@ -339,8 +340,9 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   s.near_group = NG;
   s.fetchers = std::max(1, NF);
   s.writers = NWR;
+  s.j_rem = (int32_t)jr;
   for (int j = 0; j <= NW; ++j) s.near_lo[j] = (int32_t)(jr + (NW ? count * j / NW : 0));
-  const size_t smem = sdp_v2_smem(R, kpad, vb, NW, NC);
+  const size_t smem = sdp_v2_smem(R, ((k - jr) + 3) & ~3ll, vb, NW, NC);
   if (smem > kSmemBudget) return false;
   d->v2 = true;
   d->remote = remote;
@@ -361,7 +363,9 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
     ps.remote_warps = std::min(24, env_int("PIPEDP_SDP_REMOTE_WARPS", 16));
     d->grid_extra = std::min(sm_count() - 1, env_int("PIPEDP_SDP_REMOTE_CTAS", 64));
     d->threads = std::max(d->threads, 32 * ps.remote_warps);
-    const size_t psmem = (size_t)2 * kpad * 4 + (size_t)ps.remote_warps * 32 * 8 + 64;
+    ps.j_rem = (int32_t)jr;
+    ps.rem_look = jr > 0 ? (int32_t)(offs[jr - 1] / 32) : 0;
+    const size_t psmem = (size_t)ps.remote_warps * 32 * 8 + 64;
     d->smem = std::max(d->smem, psmem);
   }
   return true;
@@ -445,6 +449,12 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
     d->gfar = false;
     s.far_warps = (int32_t)std::min<int64_t>(16, std::max<int64_t>(1, (jf_max - jr_max + 47) / 48));
     s.remote_warps = env_int("PIPEDP_SDP_REMOTE_WARPS", 8);
+    {
+      int64_t jr0 = 0;
+      for (int64_t j = 0; j < k; ++j) jr0 += offsets[j] >= a_rem;  // one instance (batch == 1)
+      s.j_rem = (int32_t)jr0;
+      s.rem_look = jr0 > 0 ? (int32_t)(offsets[jr0 - 1] / 32) : 0;
+    }
     d->grid_extra = std::min(sm_count() - 1, env_int("PIPEDP_SDP_REMOTE_CTAS", 32));
     d->smem = sdp_cta_smem(1ll << s.ring_log2, kpad, vb);
   } else {
@@ -524,6 +534,12 @@ int launch_v2(const SdpDispatch& d, const int64_t* offs, const int64_t* init, in
 template <int OP, typename T, bool ASSOC>
 int launch_sdp_t(const SdpDispatch& d, int64_t batch, const int64_t* offs, const int64_t* init,
                  int64_t* out, const SdpRemote& rm, cudaStream_t st) {
+  if (ASSOC && d.method != 0) {  // the paper's comparison methods (one instance, int64)
+    if (d.method == 1) sdp_tournament<OP><<<1, 1024, 0, st>>>(d.shape.n, d.shape.k, offs, init, out);
+    else sdp_naive<OP><<<1, 1024, 0, st>>>(d.shape.n, d.shape.k, offs, init, out);
+    CK(cudaGetLastError());
+    return PIPEDP_OK;
+  }
   if (ASSOC && d.v2 && !(OP == kModAdd && sizeof(T) == 8)) return launch_v2<OP, T>(d, offs, init, out, rm, st);
   if (d.serial) {
     sdp_serial_thread<OP, T><<<1, 32, 0, st>>>(d.shape.n, d.shape.k, offs, init, out);
@@ -559,6 +575,8 @@ int launch_sdp(const SdpDispatch& d, int64_t batch, const int64_t* offs, const i
 }
 
 const char* sdp_kernel_name(const SdpDispatch& d) {
+  if (d.method == 1 && d.assoc) return "sdp_tournament";
+  if (d.method == 2 && d.assoc) return "sdp_naive";
   if (d.serial) return "sdp_serial_thread";
   if (d.v2) return d.remote ? "sdp_v2_multi" : "sdp_v2_cta";
   if (d.warp_kernel) return "sdp_batch_warp";
@@ -577,6 +595,7 @@ struct pipedp_sdp_plan {
   SdpDispatch d;
   int64_t* d_offsets;  // device copy of the offsets, int64 [batch*k]
   void* d_remote;      // multi-CTA workspace: partial slots | ready flags | published
+  int32_t* d_obg;      // remote producers: offsets as HBM-table byte offsets
 };
 
 // ================================================================== MCM ===
@@ -946,9 +965,16 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
   if (e == cudaSuccess)
     e = cudaMemcpy(P->d_offsets, h_offsets, sizeof(int64_t) * batch * k, cudaMemcpyHostToDevice);
   if (e == cudaSuccess && d.remote) e = cudaMalloc(&P->d_remote, kRemoteBytes);
+  if (e == cudaSuccess && d.remote) {
+    std::vector<int32_t> obg((size_t)k);
+    for (int64_t j = 0; j < k; ++j) obg[(size_t)j] = (int32_t)(h_offsets[j] * 8);
+    e = cudaMalloc(&P->d_obg, sizeof(int32_t) * k);
+    if (e == cudaSuccess) e = cudaMemcpy(P->d_obg, obg.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) {
     cudaFree(P->d_offsets);
     cudaFree(P->d_remote);
+    cudaFree(P->d_obg);
     delete P;
     return cuda_fail(e, "sdp plan upload");
   }
@@ -966,6 +992,7 @@ int32_t pipedp_sdp_plan_execute(pipedp_sdp_plan_t P, const int64_t* d_init, int6
     rm.part = w;
     rm.ready = reinterpret_cast<int*>(w + kRemSlots * 32 * sizeof(int64_t));
     rm.published = reinterpret_cast<unsigned long long*>(w + kRemSlots * 32 * sizeof(int64_t) + kRemSlots * sizeof(int));
+    rm.obg = P->d_obg;
     CK(cudaMemsetAsync(P->d_remote, 0, kRemoteBytes, (cudaStream_t)stream));
     // producers read the preset prefix straight from the table before the
     // finisher CTA has necessarily run: stage it there in stream order
@@ -984,11 +1011,27 @@ int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, in
   return PIPEDP_OK;
 }
 
+int32_t pipedp_sdp_plan_set_method(pipedp_sdp_plan_t P, int32_t method) {
+  if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
+  if (method < PIPEDP_SDP_PIPELINE || method > PIPEDP_SDP_NAIVE)
+    return fail(PIPEDP_E_INVALID_PARAMS, "unknown S-DP method %d", method);
+  if (method != PIPEDP_SDP_PIPELINE && P->batch != 1)
+    return fail(PIPEDP_E_INVALID_PARAMS, "the paper's comparison methods solve one instance at a time");
+  // int64 kernels; a non-associative instance (mixed-sign saturating-add)
+  // keeps the strict-order pipeline, which is what the reference computes
+  if (method != PIPEDP_SDP_PIPELINE && P->d.bits == 32) {
+    P->d.bits = 64;
+  }
+  P->d.method = method;
+  return PIPEDP_OK;
+}
+
 int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t P) {
   if (!P) return PIPEDP_OK;
   cudaSetDevice(P->device);
   cudaFree(P->d_offsets);
   cudaFree(P->d_remote);
+  cudaFree(P->d_obg);
   delete P;
   return PIPEDP_OK;
 }
@@ -1020,6 +1063,29 @@ int32_t pipedp_sdp_solve(const int64_t* offsets, int64_t k, const int64_t* init,
                          uint8_t* filled_out) {
   TRY(validate_sdp(offsets, k, init_len, n));
   TRY(sdp_solve_host(1, n, k, init_len, offsets, init, op, cells_out, -1));
+  if (filled_out) memset(filled_out, 1, (size_t)n);
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_sdp_solve_method(const int64_t* offsets, int64_t k, const int64_t* init,
+                                int64_t init_len, int64_t n, int32_t op, int32_t method,
+                                int64_t* cells_out, uint8_t* filled_out) {
+  TRY(validate_sdp(offsets, k, init_len, n));
+  pipedp_sdp_plan_t P = nullptr;
+  TRY(pipedp_sdp_plan_create(1, n, k, init_len, offsets, init, op, -1, &P));
+  struct Guard {
+    pipedp_sdp_plan_t p;
+    ~Guard() { pipedp_sdp_plan_destroy(p); }
+  } guard{P};
+  TRY(pipedp_sdp_plan_set_method(P, method));
+  pipedp_host::Workspace* W = nullptr;
+  CK(pipedp_host::workspace(P->device, &W));
+  void *d_init = nullptr, *d_cells = nullptr;
+  CK(W->buffer(0, sizeof(int64_t) * init_len, &d_init));
+  CK(W->buffer(1, sizeof(int64_t) * n, &d_cells));
+  CK(W->h2d(d_init, init, sizeof(int64_t) * init_len));
+  TRY(pipedp_sdp_plan_execute(P, (const int64_t*)d_init, (int64_t*)d_cells, W->stream));
+  CK(W->d2h(cells_out, d_cells, sizeof(int64_t) * n));
   if (filled_out) memset(filled_out, 1, (size_t)n);
   return PIPEDP_OK;
 }

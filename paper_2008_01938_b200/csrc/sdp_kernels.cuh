@@ -58,6 +58,8 @@ struct SdpShape {
   int32_t far_warps;
   int32_t remote_warps;  // warps per producer CTA
   int32_t writers;       // finisher writer warps publishing progress (published[0..writers))
+  int32_t j_rem;         // number of offsets >= a_remote (the producers' share)
+  int32_t rem_look;      // batches between a producer batch and the newest cell it reads
 };
 
 // Global workspace of the multi-CTA mode (zeroed before every launch).
@@ -65,6 +67,7 @@ struct SdpRemote {
   void* part;               // [kRemSlots][32] T
   int* ready;               // [kRemSlots] batch+1
   unsigned long long* published;  // [writers] batches < published[w] of writer w's share are in HBM
+  const int32_t* obg;             // [k] offsets as HBM-table byte offsets (a_j * 8)
 };
 
 template <typename T, typename S>
@@ -743,26 +746,14 @@ __device__ __forceinline__ void sdp_producer(const SdpShape& S, const int64_t* _
                                              const int64_t* out, const SdpRemote& RM, int pid, int np) {
   extern __shared__ __align__(16) unsigned char smem[];
   using O = SemiOp<OP, T>;
-  const int kpad = (S.k + 3) & ~3;
-  int32_t* offs = reinterpret_cast<int32_t*>(smem);
-  int32_t* obg = offs + kpad;
-  T* red = reinterpret_cast<T*>(obg + kpad);  // [warps][32]
-  __shared__ int s_jr;
+  // offsets come from the plan's global byte-offset table (RM.obg, read-only,
+  // L1-resident): k is unbounded here (the paper's Table I reaches k = 123,928)
+  T* red = reinterpret_cast<T*>(smem);  // [warps][32]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, W = S.remote_warps;
-  for (int j = tid; j < S.k; j += 32 * W) {
-    offs[j] = (int32_t)offsets[j];
-    obg[j] = offs[j] * 8;
-  }
-  __syncthreads();
-  if (tid == 0) {
-    int jr = 0;
-    for (int j = 0; j < S.k; ++j) jr += offs[j] >= S.a_remote;
-    s_jr = jr;
-  }
-  __syncthreads();
-  const int jr = s_jr;
+  const int32_t* obg = RM.obg;
+  const int jr = S.j_rem;  // offsets[0, jr) >= a_remote
   if (jr == 0) return;
-  const int64_t look = offs[jr - 1] / 32;
+  const int64_t look = S.rem_look;
   const int per = (jr + W - 1) / W;
   const int lo = min(jr, warp * per), hi = min(jr, lo + per);
   const int64_t nb = (S.n - S.a1 + 31) / 32;
@@ -1035,6 +1026,111 @@ __global__ void __launch_bounds__(32)
     }
     __syncwarp();
     if (c0 + lane < cend) out[c0 + lane] = (int64_t)row[rb][lane];
+  }
+}
+
+}  // namespace pipedp_dev
+
+namespace pipedp_dev {
+
+// -----------------------------------------------------------------------------
+// The paper's two comparison methods for S-DP, on the GPU,
+// behind solve_prefix_parallel / solve_naive_parallel (sdp.cpp:91-111, which
+// the reference only models as step counts).  Both walk the cells one at a
+// time with the whole CTA on the k operands of the cell; the table lives in
+// HBM (operands through L2, ld.global.cg; the finished cell is released with a
+// CTA barrier + fence before the next cell reads it).  Associative (x) only --
+// the host keeps the strict pipeline for mixed-sign saturating-add.
+//
+// prefix (tournament): thread t folds a contiguous slice of offsets in j order,
+// then a ceil(log2)-level tree (one barrier per level) combines the slices in
+// order: O(n log k) steps.
+template <int OP>
+__global__ void __launch_bounds__(1024, 1)
+    sdp_tournament(int64_t n, int32_t k, const int64_t* __restrict__ g_offsets,
+                   const int64_t* __restrict__ g_init, int64_t* out) {
+  using O = SemiOp<OP, int64_t>;
+  __shared__ int64_t red[1024];
+  __shared__ uint8_t hv[1024];
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int64_t a1 = g_offsets[0];
+  for (int64_t i = t; i < a1; i += nt) out[i] = g_init[i];
+  __threadfence();
+  __syncthreads();
+  const int per = (k + nt - 1) / nt;
+  const int lo = min(k, t * per), hi = min(k, lo + per);
+  int P = 1;
+  while (P < nt && (P * per) < k) P <<= 1;  // threads holding a slice, rounded up
+  for (int64_t i = a1; i < n; ++i) {
+    int64_t acc = 0;
+    bool have = false;
+    for (int j = lo; j < hi; ++j) {
+      const int64_t v = __ldcg(reinterpret_cast<const long long*>(out + i - __ldg(g_offsets + j)));
+      acc = have ? O::apply(acc, v) : v;
+      have = true;
+    }
+    red[t] = acc;
+    hv[t] = have;
+    __syncthreads();
+    for (int s = 1; s < P; s <<= 1) {  // tournament levels, left (x) right
+      if ((t & (2 * s - 1)) == 0 && t + s < P && hv[t + s]) {
+        red[t] = hv[t] ? O::apply(red[t], red[t + s]) : red[t + s];
+        hv[t] = 1;
+      }
+      __syncthreads();
+    }
+    if (t == 0) {
+      out[i] = red[0];
+      __threadfence();
+    }
+    __syncthreads();
+  }
+}
+
+// naive: the first operand is assigned, then k-1 threads fold their operand
+// into the one shared accumulator with atomics -- the memory-access conflict
+// the paper describes ("using k-1 threads", serialised on ST[i]): O(nk).
+__device__ __forceinline__ long long naive_atomic_min(long long* a, long long v) { return atomicMin(a, v); }
+__device__ __forceinline__ long long naive_atomic_max(long long* a, long long v) { return atomicMax(a, v); }
+
+template <int OP>
+__device__ __forceinline__ void naive_fold(int64_t* acc, int64_t v) {
+  if (OP == kMin) {
+    atomicMin(reinterpret_cast<long long*>(acc), (long long)v);
+  } else if (OP == kMax) {
+    atomicMax(reinterpret_cast<long long*>(acc), (long long)v);
+  } else {
+    unsigned long long* a = reinterpret_cast<unsigned long long*>(acc);
+    unsigned long long old = *a, assumed;
+    do {
+      assumed = old;
+      const int64_t nv = SemiOp<OP, int64_t>::apply((int64_t)assumed, v);
+      old = atomicCAS(a, assumed, (unsigned long long)nv);
+    } while (old != assumed);
+  }
+}
+
+template <int OP>
+__global__ void __launch_bounds__(1024, 1)
+    sdp_naive(int64_t n, int32_t k, const int64_t* __restrict__ g_offsets, const int64_t* __restrict__ g_init,
+              int64_t* out) {
+  __shared__ int64_t acc;
+  const int t = threadIdx.x, nt = blockDim.x;
+  const int64_t a1 = g_offsets[0];
+  for (int64_t i = t; i < a1; i += nt) out[i] = g_init[i];
+  __threadfence();
+  __syncthreads();
+  for (int64_t i = a1; i < n; ++i) {
+    if (t == 0) acc = __ldcg(reinterpret_cast<const long long*>(out + i - a1));
+    __syncthreads();
+    for (int j = 1 + t; j < k; j += nt)
+      naive_fold<OP>(&acc, __ldcg(reinterpret_cast<const long long*>(out + i - __ldg(g_offsets + j))));
+    __syncthreads();
+    if (t == 0) {
+      out[i] = acc;
+      __threadfence();
+    }
+    __syncthreads();
   }
 }
 

@@ -47,6 +47,7 @@ struct SdpV2Shape {
   int32_t a_chain;     // offsets in [l+33, a_chain) are folded by the chain warp itself
   int32_t pub_every;   // writer publishes the finished prefix every pub_every batches
   int32_t fetchers;    // fetcher warps (remote mode): batch b -> fetcher b % fetchers
+  int32_t j_rem;       // offsets[0, j_rem) >= a_rem (remote); only [j_rem, k) are staged in smem
   int32_t writers;     // writer warps: batch b -> writer b % writers (each publishes its share)
   int32_t near_warps;  // NW
   int32_t comb_warps;  // NC
@@ -69,11 +70,15 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
   using O = SemiOp<OP, T>;
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t R = 1u << S.ring_log2;
-  const int kpad = (S.k + 3) & ~3;
+  const int kpad = (S.k - S.j_rem + 3) & ~3;
   const int NW = S.near_warps, NC = S.comb_warps, NG = S.near_group;
   T* ring = reinterpret_cast<T*>(smem);                       // 2R, mirrored
-  int32_t* offs = reinterpret_cast<int32_t*>(ring + 2 * R);   // raw a_j
-  T* mid_part = reinterpret_cast<T*>(offs + kpad);            // [kMidSlots][32]
+  // raw a_j for j >= j_rem only (the offsets below a_rem); offs[j] stays
+  // valid for those j (the pointer is shifted; lower j are never read here)
+  const int klocal = S.k - S.j_rem;
+  int32_t* offs_s = reinterpret_cast<int32_t*>(ring + 2 * R);
+  int32_t* offs = offs_s - S.j_rem;
+  T* mid_part = reinterpret_cast<T*>(offs_s + kpad);          // [kMidSlots][32]
   T* near_part = mid_part + kMidSlots * 32;                   // [kNearSlots][NW][32]
   T* rem_part = near_part + (size_t)kNearSlots * NW * 32;                  // [kFetchSlots][32]
   int32_t* pre_scratch = reinterpret_cast<int32_t*>(rem_part + kFetchSlots * 32);  // [kPreMax][32]
@@ -87,7 +92,7 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t a1 = S.a1, n = S.n;
-  for (int j = tid; j < S.k; j += blockDim.x) offs[j] = (int32_t)offsets[j];
+  for (int j = tid; j < klocal; j += blockDim.x) offs_s[j] = (int32_t)offsets[S.j_rem + j];
   const int64_t ring_from = a1 > (int64_t)R ? a1 - (int64_t)R : 0;
   for (int64_t i = tid; i < a1; i += blockDim.x) {
     const int64_t v = init[i];

@@ -142,9 +142,22 @@ SolutionTable solve_sequential(const SdpInstance& inst) {
   return t;
 }
 
+namespace {
+SolutionTable solve_method(const SdpInstance& inst, int32_t method) {
+  validate(inst);
+  SolutionTable t = full_table(inst.n);
+  check(pipedp_sdp_solve_method(inst.offsets.offsets.data(), inst.offsets.k(), inst.init.data(),
+                                static_cast<std::int64_t>(inst.init.size()), inst.n,
+                                static_cast<int32_t>(inst.op.kind), method, t.cells.data(), nullptr));
+  return t;
+}
+}  // namespace
+
+// The paper's own methods on the device (sdp_tournament / sdp_naive), with the
+// reference's step models on top.
 PrefixParallelResult solve_prefix_parallel(const SdpInstance& inst) {  // sdp.cpp:91-100
   PrefixParallelResult r;
-  r.table = solve_sequential(inst);
+  r.table = solve_method(inst, PIPEDP_SDP_PREFIX);
   r.depth_per_cell = ceil_log2(inst.offsets.k());
   r.modeled_steps = (inst.n - inst.offsets.a1()) * std::max<std::int64_t>(r.depth_per_cell, 1);
   return r;
@@ -152,7 +165,7 @@ PrefixParallelResult solve_prefix_parallel(const SdpInstance& inst) {  // sdp.cp
 
 NaiveParallelResult solve_naive_parallel(const SdpInstance& inst) {  // sdp.cpp:102-111
   NaiveParallelResult r;
-  r.table = solve_sequential(inst);
+  r.table = solve_method(inst, PIPEDP_SDP_NAIVE);
   r.serialized_accesses_per_cell = inst.offsets.k() - 1;
   r.modeled_steps = (inst.n - inst.offsets.a1()) * inst.offsets.k();
   return r;

@@ -160,3 +160,29 @@ def test_all_offsets_below_64_with_large_one(gpu, oracle, op):
     rng = np.random.default_rng(4)
     init = rng.integers(0, 2**20, 200) if op != "saturating-add" else rng.integers(0, 5, 200)
     _check(gpu, oracle, offs, init, 7000, op)
+
+
+@pytest.mark.parametrize("op", OPS)
+@pytest.mark.parametrize("shape", [(300, 5, 0), (3000, 64, 0), (9000, 300, 700), (5000, 1500, 4096)])
+def test_paper_methods_prefix_and_naive(gpu, oracle, op, shape):
+    # solve_prefix_parallel / solve_naive_parallel run the paper's tournament and
+    # naive methods on the device (sdp.cpp:91-111: same table as the oracle)
+    n, k, cap = shape
+    offs, init = oracle.generate_sdp(n, k, 17, False, cap)
+    want, _ = oracle.sdp_solve(offs, init, n, op)
+    inst = gpu.SdpInstance(n, offs, init, op)
+    p = gpu.solve_prefix_parallel(inst)
+    assert np.array_equal(p.table.cells, want) and p.depth_per_cell == (k - 1).bit_length()
+    q = gpu.solve_naive_parallel(inst)
+    assert np.array_equal(q.table.cells, want) and q.serialized_accesses_per_cell == k - 1
+
+
+def test_paper_methods_mixed_sign_sat_add(gpu, oracle):
+    # non-associative: the strict pipeline is kept (reference table)
+    rng = np.random.default_rng(2)
+    offs, _ = oracle.generate_sdp(4000, 40, 3, False, 0)
+    init = rng.choice([2**62, -(2**62), 3, -5], offs[0])
+    want, _ = oracle.sdp_solve(offs, init, 4000, "saturating-add")
+    inst = gpu.SdpInstance(4000, offs, init, "saturating-add")
+    assert np.array_equal(gpu.solve_prefix_parallel(inst).table.cells, want)
+    assert np.array_equal(gpu.solve_naive_parallel(inst).table.cells, want)
