@@ -165,6 +165,73 @@ struct Workspace {
     }
     return cudaSuccess;
   }
+  // Device -> pageable host copy of a table that a running kernel is still
+  // producing front to back.  `progress(&ready)` reports how many leading
+  // bytes are final (it may itself issue small copies on `side`); chunks are
+  // copied out as soon as they are final, so only the tail is left when the
+  // kernel ends.  `done` is recorded on `stream` after the kernel: once it has
+  // completed everything is final.  Synchronous.
+  template <class Progress>
+  cudaError_t d2h_streamed(void* dst, const void* src, size_t bytes, cudaEvent_t done, Progress progress) {
+    constexpr size_t kPiece = 16u << 20;
+    if (!side) {
+      cudaError_t e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+      if (e != cudaSuccess) return e;
+    }
+    const size_t nchunks = (bytes + kPiece - 1) / kPiece;
+    size_t ready = 0, issued = 0, drained = 0;
+    bool finished = false;
+    cudaEvent_t* evs = ev;
+    auto drain = [&](size_t c) {  // chunk c: wait for its DMA, copy it out of pinned
+      cudaError_t e = cudaEventSynchronize(evs[c & 1]);
+      if (e != cudaSuccess) return e;
+      const size_t off = c * kPiece, len = std::min(kPiece, bytes - off);
+      parallel_memcpy(static_cast<char*>(dst) + off, pinned[c & 1], len);
+      return cudaSuccess;
+    };
+    while (drained < nchunks) {
+      // issue every final chunk that has a free pinned slot
+      while (issued < nchunks && issued < drained + 2) {
+        const size_t off = issued * kPiece, len = std::min(kPiece, bytes - off);
+        if (!finished && ready < off + len) break;
+        cudaError_t e = cudaMemcpyAsync(pinned[issued & 1], static_cast<const char*>(src) + off, len,
+                                        cudaMemcpyDeviceToHost, side);
+        if (e == cudaSuccess) e = cudaEventRecord(evs[issued & 1], side);
+        if (e != cudaSuccess) return e;
+        ++issued;
+      }
+      if (drained < issued) {
+        cudaError_t e = drain(drained++);
+        if (e != cudaSuccess) return e;
+        continue;
+      }
+      // nothing in flight: learn more progress
+      if (!finished) {
+        cudaError_t q = cudaEventQuery(done);
+        if (q == cudaSuccess) {
+          finished = true;
+        } else if (q != cudaErrorNotReady) {
+          return q;
+        } else {
+          cudaError_t e = progress(&ready);
+          if (e != cudaSuccess) return e;
+        }
+      }
+    }
+    return cudaStreamSynchronize(stream);
+  }
+  cudaStream_t side = nullptr;  // second copy stream (d2h_streamed)
+  unsigned long long* ctr = nullptr;  // pinned scratch for progress counters (8 words)
+  cudaEvent_t armed = nullptr, done = nullptr;
+  cudaError_t streaming_init() {
+    cudaError_t e = cudaSuccess;
+    if (!ctr) e = cudaHostAlloc(reinterpret_cast<void**>(&ctr), 64, cudaHostAllocDefault);
+    if (e == cudaSuccess && !armed) e = cudaEventCreateWithFlags(&armed, cudaEventDisableTiming);
+    if (e == cudaSuccess && !done) e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
+    if (e == cudaSuccess && !side) e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    return e;
+  }
+
   // device -> pageable host after the work queued on `stream`; synchronous
   cudaError_t d2h(void* dst, const void* src, size_t bytes) {
     const size_t nchunks = (bytes + kChunk - 1) / kChunk;

@@ -186,3 +186,25 @@ def test_paper_methods_mixed_sign_sat_add(gpu, oracle):
     inst = gpu.SdpInstance(4000, offs, init, "saturating-add")
     assert np.array_equal(gpu.solve_prefix_parallel(inst).table.cells, want)
     assert np.array_equal(gpu.solve_naive_parallel(inst).table.cells, want)
+
+
+@pytest.mark.parametrize("op,writers", [("min", "1"), ("modular-add", "2")])
+def test_streamed_copy_out_while_kernel_runs(gpu, oracle, op, writers, monkeypatch):
+    # >= 64 MiB single-instance multi-CTA solve: the host-buffer entry point
+    # copies finished 16 MiB chunks out while the kernel is still producing the
+    # tail (progress from the writers' published counters, min over writers)
+    monkeypatch.setenv("PIPEDP_SDP2_WRITERS", writers)
+    n = 9_000_000 + 777
+    offs, init = oracle.generate_sdp(n, 256, 5, False, 4096)
+    _check(gpu, oracle, offs, init, n, op)
+
+
+def test_cached_plan_reuse_with_new_init_and_op(gpu, oracle):
+    # the host-buffer entry point keeps its last plan: same offsets with new
+    # init values (same value class), then another value class, then another op
+    n = 50000
+    offs, init = oracle.generate_sdp(n, 500, 3, False, 3000)
+    rng = np.random.default_rng(5)
+    for op, lo, hi in [("min", -1000, 1000), ("min", -1000, 1000), ("min", -(2**60), 2**60),
+                       ("max", 0, 100), ("modular-add", 0, 2**31 - 1)]:
+        _check(gpu, oracle, offs, rng.integers(lo, hi, len(init)), n, op)
