@@ -57,7 +57,7 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
     """profile=True builds _lib/libpipedp_cuda_prof.so with the role profiler."""
     os.makedirs(LIB, exist_ok=True)
     nvcc = _nvcc()
-    cuda_srcs = _sources(CSRC, (".cu", ".cuh")) + [os.path.join(INCLUDE, "pipedp_cuda.h")]
+    cuda_srcs = _sources(CSRC, (".cu", ".cuh", ".inc", ".hpp")) + [os.path.join(INCLUDE, "pipedp_cuda.h")]
     target = PROF_SO if profile else CUDA_SO
     if force or _newer(target, cuda_srcs):
         cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",

@@ -721,7 +721,7 @@ int mcm_tiled_launch(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStr
   CK(cudaMemsetAsync(split, 0, sizeof(int64_t) * (n + 1), st));
   McmTiled S{n, (int32_t)N, P->ntasks, P->d_pp, P->d_tiles, P->d_keys, P->d_tile_flags,
              P->d_tile_flags + ntiles, P->d_tasks, P->d_next, cells, split, P->d_overflow,
-             env_int("PIPEDP_MCM_BLOCKED", 0)};
+             env_int("PIPEDP_MCM_BLOCKED", 0) ? 1 : env_int("PIPEDP_MCM_NEAR", 2)};
   if (P->d.tile == 32) {
     CK(cudaFuncSetAttribute(t32::mcm_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)t32::kTiledSmemBytes));

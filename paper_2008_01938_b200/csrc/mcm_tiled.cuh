@@ -56,7 +56,7 @@ struct McmTiled {
   int64_t* out_cells;          // reference layout (diagonal-major, slot 0)
   int64_t* out_split;
   int* overflow;
-  int32_t blocked;             // 1: blocked in-tile pipeline (8x8 sub-blocks), 0: CTA-wide steps
+  int32_t blocked;             // near in-tile pipeline: 0 CTA-wide folds per step, 1 8x8 sub-blocks, 2 pull
 };
 
 __host__ __device__ __forceinline__ int64_t tiled_index(int64_t I, int64_t J, int64_t N) {
@@ -110,6 +110,11 @@ __device__ __forceinline__ void tb_take(TBest& b, uint32_t v, uint32_t k) {
     b.v = v;
     b.k = k;
   }
+}
+__device__ __forceinline__ void tb_take_lex(uint32_t& bv, uint32_t& bk, uint32_t v, uint32_t k) {
+  const bool take = v < bv || (v == bv && k < bk);
+  bv = take ? v : bv;
+  bk = take ? k : bk;
 }
 __device__ __forceinline__ TBest tb_reduce4(TBest b) {  // over lanes l, l^1, l^2, l^3
 #pragma unroll
