@@ -280,9 +280,15 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
     has1 = has1 || offs[j] == 1;
     n64_128 += offs[j] >= 64 && offs[j] < 128;
   }
-  if ((d->op == PIPEDP_OP_MIN || d->op == PIPEDP_OP_MAX) && has1 && n64_128 <= kPreUMax &&
-      env_int("PIPEDP_SDP2_DOM", 1) != 0)
-    a_chain = 128;
+  // the dominance form takes [l+33, a_chain) with one shuffle per 32-wide
+  // range (a_chain up to 256: near warps then see >= 8 batches of look-ahead);
+  // its first a_chain/32 - 1 batches fold that range from the ring directly
+  bool dom = false;
+  if ((d->op == PIPEDP_OP_MIN || d->op == PIPEDP_OP_MAX) && has1 && env_int("PIPEDP_SDP2_DOM", 1) != 0) {
+    dom = true;
+    a_chain = std::min(256, std::max(128, env_int("PIPEDP_SDP2_DOM_ACHAIN", 256))) & ~31;
+  }
+  (void)n64_128;
   int64_t jr = 0, jn = 0;
   for (int64_t j = 0; j < k; ++j) {
     jr += offs[j] >= a_rem;
@@ -330,7 +336,8 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   s.a_chain = a_chain;
   s.pub_every = std::max(1, env_int("PIPEDP_SDP2_PUB", 4));
   s.n_pre_u = 0;
-  for (int64_t j = k - 1; j >= 0; --j) {
+  s.dom = dom ? 1 : 0;
+  for (int64_t j = k - 1; j >= 0 && !dom; --j) {
     if (offs[j] < 64) continue;
     if (offs[j] >= a_chain) break;
     s.pre_u[s.n_pre_u++] = -(int32_t)(offs[j] * (int64_t)vb);

@@ -739,6 +739,34 @@ __device__ __forceinline__ void sdp_finisher(const SdpShape& S, const int64_t* _
   }
 }
 
+// A producer warp's fold: 16 independent table loads in flight per chunk
+// (two chunks unrolled), so a warp's ~50 L2 reads cost ~2 L2 round trips, not
+// one per 4-load group.  Regrouped (associative (x) only).
+template <int OP, typename T>
+__device__ __forceinline__ T fold_wide(const int64_t* base_elem, const int32_t* __restrict__ ob, int j0, int j1) {
+  using O = SemiOp<OP, T>;
+  constexpr int W = 16;
+  const char* base = reinterpret_cast<const char*>(base_elem);
+  T acc = SemiId<OP, T>::value();
+  int j = j0;
+#pragma unroll 2
+  for (; j + W <= j1; j += W) {
+    int32_t o[W];
+    T v[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) o[q] = __ldg(ob + j + q);
+#pragma unroll
+    for (int q = 0; q < W; ++q) v[q] = at<T, int64_t, true>(base, o[q]);
+#pragma unroll
+    for (int w = W / 2; w >= 1; w >>= 1)
+#pragma unroll
+      for (int q = 0; q < w; ++q) v[q] = O::apply(v[q], v[q + w]);
+    acc = O::apply(acc, v[0]);
+  }
+  for (; j < j1; ++j) acc = O::apply(acc, at<T, int64_t, true>(base, __ldg(ob + j)));
+  return acc;
+}
+
 // The remote operand fold of one batch, split over the CTA's warps in
 // contiguous offset ranges and combined in order (requires ASSOC).
 template <int OP, typename T>
@@ -772,7 +800,7 @@ __device__ __forceinline__ void sdp_producer(const SdpShape& S, const int64_t* _
     t0 = PROF_NOW();
     const int64_t c = S.a1 + 32 * b + lane;
     if (lo < hi) {
-      red[warp * 32 + lane] = fold_range<OP, T, true, int64_t, true>(T(0), false, out + c, obg, lo, hi);
+      red[warp * 32 + lane] = fold_wide<OP, T>(out + c, obg, lo, hi);
     }
     __syncthreads();
     if (warp == 0) {
@@ -782,8 +810,7 @@ __device__ __forceinline__ void sdp_producer(const SdpShape& S, const int64_t* _
       }
       const int rs = (int)(b % kRemSlots);
       reinterpret_cast<int64_t*>(RM.part)[rs * 32 + lane] = (int64_t)acc;
-      __threadfence();
-      __syncwarp();
+      __syncwarp();  // orders the lanes' partial stores before lane 0's (cumulative) release
       if (lane == 0) st_release_gpu_i32(RM.ready + rs, (int)(b + 1));
     }
     PROF_ADD(p_fold, t0);

@@ -36,6 +36,7 @@ constexpr int kNearWarps = 20; // max near warps
 constexpr int kFetchSlots = 16; // fetcher -> combiner remote partial slots
 constexpr int kMaxWarpsV2 = 24; // 768 threads: the chain warp's register budget
 constexpr int kPreMax = 32;     // chain-folded offsets per lane in [l+33, 63] (<= 31)
+constexpr int kDomMax = 8;      // dominance form registers (power of two); a_chain <= 256 uses 7
 constexpr int kPreUMax = 32;    // chain-folded lane-independent offsets in [64, a_chain)
 
 struct SdpV2Shape {
@@ -53,6 +54,7 @@ struct SdpV2Shape {
   int32_t comb_warps;  // NC
   int32_t near_group;  // NG warps per offset range (batch b -> warp b % NG)
   int32_t near_lo[kNearWarps + 1];  // near warp j owns offset indices [near_lo[j], near_lo[j+1])
+  int32_t dom;                        // dominance form (min/max with offset 1), a_chain = 32 (M + 1), M <= kDomMax
   int32_t n_pre_u;                    // chain-folded offsets in [64, a_chain), lane-independent:
   int32_t pre_u[kPreUMax];            //   as negative ring byte offsets (uniform-register operands)
 };
@@ -186,25 +188,42 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
       pre_load(base, v);
       return pre_tree(v);
     };
-    T pre_cur = pre_fold(reinterpret_cast<const char*>(ring + (((uint32_t)(a1 + lane) & (R - 1)) + R)));
-    // Dominance form (idempotent (x) with offset 1, a_chain = 128): x of a
-    // finished batch is the prefix-(x) of its b vector (see idem_closure), so
-    // the terms a later batch takes from it, offsets d in a 32-wide range,
-    // fold to x at the single position of the smallest such d.  srcK: that
-    // position for the range landing K batches back (d in [l+32(K-1)+1,
-    // min(l+32K, 127)]), -1 when the range holds no offset.
-    const bool dom = IsIdem<OP>::value && im.scan && S.a_chain == 128;
-    int src2 = -1, src3 = -1, src4 = -1;
+    // Dominance form (idempotent (x) with offset 1, S.dom): x of a finished
+    // batch is the prefix-(x) of its b vector (see idem_closure), so the terms
+    // a later batch takes from it, offsets d in a 32-wide range, fold to x at
+    // the single position of the smallest such d.  src[K-2]: that position for
+    // the range landing K batches back (d in [l+32(K-1)+1, min(l+32K,
+    // a_chain-1)]), -1 when the range holds no offset; K = 2 .. M+1.
+    const bool dom = IsIdem<OP>::value && im.scan && S.dom;
+    const int M = dom ? S.a_chain / 32 - 1 : 0;  // 3 .. 7
+    int src[kDomMax];
+#pragma unroll
+    for (int q = 0; q < kDomMax; ++q) src[q] = -1;
     if (dom) {
       for (int j = S.k - 1; j >= 0; --j) {  // ascending d
         const int d = offs[j];
-        if (d > 127) break;
-        if (src2 < 0 && d >= lane + 33 && d <= lane + 64) src2 = lane + 64 - d;
-        if (src3 < 0 && d >= lane + 65 && d <= lane + 96) src3 = lane + 96 - d;
-        if (src4 < 0 && d >= lane + 97 && d <= lane + 128) src4 = lane + 128 - d;
+        if (d >= S.a_chain) break;
+#pragma unroll
+        for (int q = 0; q < kDomMax; ++q)
+          if (src[q] < 0 && d >= lane + 32 * (q + 1) + 1 && d <= lane + 32 * (q + 2)) src[q] = lane + 32 * (q + 2) - d;
       }
     }
-    T xm1 = id, xm2 = id, xm3 = id;  // x of batches b, b-1, b-2 after iteration b
+    // the dominance form's first M batches (and batch 0's pre-fold): offsets
+    // [l+33, a_chain) of the cell at `cn` straight from the ring
+    auto pre_ring = [&](int64_t cn) {
+      T v = id;
+      for (int j = S.k - 1; j >= 0; --j) {
+        const int d = offs[j];
+        if (d >= S.a_chain) break;
+        if (d >= lane + 33) v = O::apply(v, ring[((uint32_t)(cn - d) & (R - 1)) + R]);
+      }
+      return v;
+    };
+    T pre_cur = dom ? pre_ring(a1 + lane)
+                    : pre_fold(reinterpret_cast<const char*>(ring + (((uint32_t)(a1 + lane) & (R - 1)) + R)));
+    T xm[kDomMax];  // x of batches b-1, b-2, ... (before iteration b's shift)
+#pragma unroll
+    for (int q = 0; q < kDomMax; ++q) xm[q] = id;
     PROF_DECL(p_wait);
     PROF_DECL(p_fold);
     const long long p_start = PROF_NOW();
@@ -223,14 +242,24 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
       PROF_ADD(p_wait, t0);
       t0 = PROF_NOW();
       T acc = O::apply(O::apply(mid_part[slot * 32 + lane], pre_cur), nxt);
-      if (dom && b >= 3) {
-        // batch b+1's chain-local offsets from x of batches b-1, b-2, b-3 by
-        // the closure's prefix structure: one shuffle per batch range
+      if (dom && b >= M) {
+        // batch b+1's chain-local offsets from x of batches b-1 .. b-M by the
+        // closure's prefix structure: one shuffle per batch range
         idem_closure<OP, T>(acc, nxt, im);
-        const T v2 = shfl_idx(xm1, src2 < 0 ? 0 : src2);
-        const T v3 = shfl_idx(xm2, src3 < 0 ? 0 : src3);
-        const T v4 = shfl_idx(xm3, src4 < 0 ? 0 : src4);
-        pre_cur = O::apply(O::apply(src2 < 0 ? id : v2, src3 < 0 ? id : v3), src4 < 0 ? id : v4);
+        T pv[kDomMax];
+#pragma unroll
+        for (int q = 0; q < kDomMax; ++q) {
+          const T v = shfl_idx(xm[q], src[q] < 0 ? 0 : src[q]);
+          pv[q] = q < M && src[q] >= 0 ? v : id;
+        }
+#pragma unroll
+        for (int w = kDomMax / 2; w >= 1; w >>= 1)
+#pragma unroll
+          for (int q = 0; q < w; ++q) pv[q] = O::apply(pv[q], pv[q + w]);
+        pre_cur = pv[0];
+      } else if (dom) {
+        idem_closure<OP, T>(acc, nxt, im);
+        pre_cur = pre_ring(c + 32);  // reads batches <= b - 1 only
       } else {
         // batch b+1's chain-local offsets: independent of this batch's closure
         T pv[8];
@@ -243,9 +272,9 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
         }
         pre_cur = pre_tree(pv);
       }
-      xm3 = xm2;
-      xm2 = xm1;
-      xm1 = acc;
+#pragma unroll
+      for (int q = kDomMax - 1; q >= 1; --q) xm[q] = xm[q - 1];
+      xm[0] = acc;
       if (c < n) {
         ring[pos - R] = acc;
         ring[pos] = acc;
@@ -389,10 +418,10 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
       if (REMOTE && (++done % S.pub_every == 0 || b + NWR >= nb)) {
         t0 = PROF_NOW();
         __syncwarp();
-        if (lane == 0) {  // one gpu-scope release per publish (not one fence per lane)
-          __threadfence();
-          st_release_gpu(reinterpret_cast<long long*>(RM.published) + w, (long long)(b + 1));
-        }
+        // the warp barrier orders every lane's table stores before lane 0's
+        // gpu-scope release (release is cumulative; the bar.sync + single
+        // st.release idiom), so no separate full fence
+        if (lane == 0) st_release_gpu(reinterpret_cast<long long*>(RM.published) + w, (long long)(b + 1));
         __syncwarp();
         PROF_ADD(p_wp, t0);
       }
