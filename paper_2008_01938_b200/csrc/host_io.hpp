@@ -16,6 +16,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <condition_variable>
 #include <cstring>
 #include <functional>
@@ -181,6 +184,10 @@ struct Workspace {
     const size_t nchunks = (bytes + kPiece - 1) / kPiece;
     size_t ready = 0, issued = 0, drained = 0;
     bool finished = false;
+    static const bool trace = getenv("PIPEDP_TRACE_D2H") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+    long polls = 0;
     cudaEvent_t* evs = ev;
     auto drain = [&](size_t c) {  // chunk c: wait for its DMA, copy it out of pinned
       cudaError_t e = cudaEventSynchronize(evs[c & 1]);
@@ -198,6 +205,8 @@ struct Workspace {
                                         cudaMemcpyDeviceToHost, side);
         if (e == cudaSuccess) e = cudaEventRecord(evs[issued & 1], side);
         if (e != cudaSuccess) return e;
+        if (trace) fprintf(stderr, "d2h chunk %zu issued at %.2f ms (ready %zu MiB, finished %d, polls %ld)\n", issued,
+                           ms(), ready >> 20, (int)finished, polls);
         ++issued;
       }
       if (drained < issued) {
@@ -213,11 +222,18 @@ struct Workspace {
         } else if (q != cudaErrorNotReady) {
           return q;
         } else {
+          const size_t before = ready;
           cudaError_t e = progress(&ready);
+          ++polls;
           if (e != cudaSuccess) return e;
+          // no new chunk final yet: back off (each poll is a device read the
+          // running kernel's counters see as traffic)
+          if (ready == before || ready < std::min(bytes, (issued + 1) * kPiece))
+            std::this_thread::sleep_for(std::chrono::microseconds(200));
         }
       }
     }
+    if (trace) fprintf(stderr, "d2h done at %.2f ms\n", ms());
     return cudaStreamSynchronize(stream);
   }
   cudaStream_t side = nullptr;  // second copy stream (d2h_streamed)
