@@ -436,10 +436,19 @@ def main():
         bits = W.value_bits()
         op_ns, op_cyc = pd.op_latency_ns(i.op, bits, local)
         hand_ns, _ = pd.chain_step_ns(i.op, bits, local) if (i.op, bits) != ("saturating-add", 32) else (None, None)
-        steps = i.n - i.a1  # a_k = 1: one cell per step
+        if W.kernel_name() == "sdp_jump":
+            # jump-ahead segments: the longest dependent chain is one 64-cell
+            # segment after its entry state (log2(segments) matrix levels)
+            nseg = -(-(i.n - i.a1) // 64)
+            steps = 64 + max(1, (nseg - 1).bit_length())
+            definition = ("sdp_jump: 64-cell segment chain + log2(segments) entry-state levels, "
+                          "each x latency of one dependent (x)")
+        else:
+            steps = i.n - i.a1  # a_k = 1: one cell per step
+            definition = "(n - a_1) dependent steps x latency of one dependent (x) in a register chain"
         floor_ms = steps * op_ns / 1e6
         extra["chain_roofline"] = {
-            "definition": "(n - a_1) dependent steps x latency of one dependent (x) in a register chain",
+            "definition": definition,
             "steps": steps, "t_op_ns": op_ns, "t_op_cycles": op_cyc, "floor_ms": floor_ms,
             "achieved_ms": avg_ms, "frac": floor_ms / avg_ms,
             "t_warp_handoff_ns": hand_ns, "value_bits": bits}

@@ -22,6 +22,7 @@
 #include "mcm_kernels.cuh"
 #include "mcm_tiled.cuh"
 #include "sdp_kernels.cuh"
+#include "sdp_jump.cuh"
 #include "sdp_v2.cuh"
 #include "host_io.hpp"
 
@@ -202,6 +203,7 @@ struct SdpDispatch {
   int wpb;  // warp kernel: warps per block
   bool v2;   // offset-partitioned single-instance pipeline (sdp_v2.cuh)
   bool serial;  // tiny offset sets: one-thread chain (sdp_serial_thread)
+  bool jump;    // a_1 <= 8: jump-ahead segments (sdp_jump)
   int method;   // 0 pipeline, 1 the paper's tournament (prefix), 2 the paper's naive method
   SdpV2Shape s2;
 };
@@ -419,6 +421,14 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
   d->warp_kernel = false;
   d->small = a1 < 64;
   d->serial = batch == 1 && d->small && k <= 8 && env_int("PIPEDP_SDP_SERIAL", 1) != 0;
+  {  // jump-ahead segments (sdp_jump.cuh): a_1 <= 8, an operator whose matrix form is exact
+    bool nonneg = true;
+    for (int64_t i = 0; i < a1; ++i) nonneg = nonneg && init[i] >= 0;
+    const bool ring_ok = op == PIPEDP_OP_MIN || op == PIPEDP_OP_MAX || op == PIPEDP_OP_MODULAR_ADD ||
+                         (op == PIPEDP_OP_SATURATING_ADD && nonneg);
+    d->jump = batch == 1 && a1 >= 2 && a1 <= 8 && k >= 2 && ring_ok && n - a1 >= 4096 &&
+              env_int("PIPEDP_SDP_JUMP", 1) != 0;
+  }
 
   if (d->small) {
     s.ring_log2 = ceil_log2((uint64_t)(a1 + 128));
@@ -539,6 +549,27 @@ int launch_v2(const SdpDispatch& d, const int64_t* offs, const int64_t* init, in
   return PIPEDP_OK;
 }
 
+template <int OP>
+int launch_jump(const SdpDispatch& d, const int64_t* offs, const int64_t* init, int64_t* out, cudaStream_t st) {
+  const int64_t nseg = (d.shape.n - d.shape.a1 + (1 << kJumpLog2L) - 1) >> kJumpLog2L;
+  const unsigned grid = (unsigned)((nseg + kJumpThreads - 1) / kJumpThreads);
+  switch (d.shape.a1) {
+#define PIPEDP_JUMP_CASE(A) \
+  case A: sdp_jump<OP, A><<<grid, kJumpThreads, 0, st>>>(d.shape.n, d.shape.k, offs, init, out); break;
+    PIPEDP_JUMP_CASE(2)
+    PIPEDP_JUMP_CASE(3)
+    PIPEDP_JUMP_CASE(4)
+    PIPEDP_JUMP_CASE(5)
+    PIPEDP_JUMP_CASE(6)
+    PIPEDP_JUMP_CASE(7)
+    PIPEDP_JUMP_CASE(8)
+#undef PIPEDP_JUMP_CASE
+    default: return fail(PIPEDP_E_INVALID_PARAMS, "sdp_jump: a_1 = %d", d.shape.a1);
+  }
+  CK(cudaGetLastError());
+  return PIPEDP_OK;
+}
+
 template <int OP, typename T, bool ASSOC>
 int launch_sdp_t(const SdpDispatch& d, int64_t batch, const int64_t* offs, const int64_t* init,
                  int64_t* out, const SdpRemote& rm, cudaStream_t st) {
@@ -549,6 +580,7 @@ int launch_sdp_t(const SdpDispatch& d, int64_t batch, const int64_t* offs, const
     return PIPEDP_OK;
   }
   if (ASSOC && d.v2 && !(OP == kModAdd && sizeof(T) == 8)) return launch_v2<OP, T>(d, offs, init, out, rm, st);
+  if (d.jump) return launch_jump<OP>(d, offs, init, out, st);
   if (d.serial) {
     sdp_serial_thread<OP, T><<<1, 32, 0, st>>>(d.shape.n, d.shape.k, offs, init, out);
     CK(cudaGetLastError());
@@ -585,6 +617,7 @@ int launch_sdp(const SdpDispatch& d, int64_t batch, const int64_t* offs, const i
 const char* sdp_kernel_name(const SdpDispatch& d) {
   if (d.method == 1 && d.assoc) return "sdp_tournament";
   if (d.method == 2 && d.assoc) return "sdp_naive";
+  if (d.jump) return "sdp_jump";
   if (d.serial) return "sdp_serial_thread";
   if (d.v2) return d.remote ? "sdp_v2_multi" : "sdp_v2_cta";
   if (d.warp_kernel) return "sdp_batch_warp";

@@ -208,3 +208,33 @@ def test_cached_plan_reuse_with_new_init_and_op(gpu, oracle):
     for op, lo, hi in [("min", -1000, 1000), ("min", -1000, 1000), ("min", -(2**60), 2**60),
                        ("max", 0, 100), ("modular-add", 0, 2**31 - 1)]:
         _check(gpu, oracle, offs, rng.integers(lo, hi, len(init)), n, op)
+
+
+@pytest.mark.parametrize("op", OPS)
+@pytest.mark.parametrize("seed", range(6))
+def test_jump_segments_small_a1(gpu, oracle, op, seed):
+    # a_1 <= 8, k >= 2: jump-ahead segments (sdp_jump); sat-add takes the jump
+    # path only with non-negative presets (otherwise the serial kernel)
+    rng = np.random.default_rng(100 + seed * 4 + OPS.index(op))
+    a1 = int(rng.integers(2, 9))
+    k = int(rng.integers(2, a1 + 1))
+    offs = np.sort(rng.choice(np.arange(1, a1), k - 1, replace=False))[::-1] if k > 1 else []
+    offs = np.concatenate([[a1], offs]).astype(np.int64)
+    n = int(rng.integers(4200, 60000))
+    if op == "saturating-add":
+        init = rng.integers(0, 2**40, a1) if seed % 2 == 0 else rng.integers(0, 3, a1)
+    elif op == "modular-add":
+        init = rng.integers(-(2**40), 2**40, a1)
+    else:
+        init = rng.integers(-(2**62), 2**62, a1)
+    inst = gpu.SdpInstance(n, offs, init, op)
+    plan = gpu.SdpPlan(1, n, len(offs), a1, offs, init, op)
+    assert plan.describe()[0] == "sdp_jump"
+    plan.close()
+    _check(gpu, oracle, offs, init, n, op)
+
+
+def test_jump_fibonacci_saturates_like_reference(gpu, oracle):
+    # the C1 shape: clamped counts in the jump matrices, INT64_MAX tail
+    _check(gpu, oracle, [2, 1], [1, 1], 300000, "saturating-add")
+    _check(gpu, oracle, [3, 2], [0, 5, 7], 100000, "saturating-add")

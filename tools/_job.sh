@@ -1,2 +1,2 @@
-PYTHONPATH=. PIPEDP_TRACE_D2H=1 timeout 200 python tools/e2e_probe.py 2>&1 | tail -14
-timeout 200 python bench.py --workload c2 --no-cpu-baseline --steps 3 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c2', round(d['ms_per_step'],1), d['e2e']['ms_per_step'], d['parity']['match'])"
+timeout 400 python -m pytest tests/test_gpu_sdp.py -x -q 2>&1 | tail -3
+timeout 300 python bench.py --workload c1 --steps 5 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c1', d['ms_per_step'], d['value'], d['e2e']['value'], d['cpu_baseline']['value'], d['parity'], d['roofline']['kernel'], d.get('chain_roofline'))"
