@@ -23,6 +23,7 @@
 #include "mcm_tiled.cuh"
 #include "sdp_kernels.cuh"
 #include "sdp_jump.cuh"
+#include "sdp_chunked.cuh"
 #include "sdp_v2.cuh"
 #include "host_io.hpp"
 
@@ -204,6 +205,8 @@ struct SdpDispatch {
   bool v2;   // offset-partitioned single-instance pipeline (sdp_v2.cuh)
   bool serial;  // tiny offset sets: one-thread chain (sdp_serial_thread)
   bool jump;    // a_1 <= 8: jump-ahead segments (sdp_jump)
+  bool chunked; // one large min/max instance as a batch of chunks (sdp_chunked.cuh)
+  int32_t chunk_log2;  // chunk length L = 1 << chunk_log2
   int method;   // 0 pipeline, 1 the paper's tournament (prefix), 2 the paper's naive method
   SdpV2Shape s2;
 };
@@ -430,6 +433,21 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
               env_int("PIPEDP_SDP_JUMP", 1) != 0;
   }
 
+  {  // chunks: cells [a1, n) in G ~ 256 chunks of L = 2^m >= max(4096, 8 a1)
+    d->chunked = false;
+    if (batch == 1 && (op == PIPEDP_OP_MIN || op == PIPEDP_OP_MAX) && a1 >= 64 && a1 <= 8192 &&
+        env_int("PIPEDP_SDP_CHUNKED", 1) != 0) {
+      int m = 12;
+      while ((1ll << m) < 8 * a1) ++m;
+      const int target = std::max(1, env_int("PIPEDP_SDP_CHUNKS", 256));
+      while (((n - a1) >> m) >= target) ++m;
+      const int64_t G = (n - a1 + (1ll << m) - 1) >> m;
+      if (G >= 16) {
+        d->chunked = true;
+        d->chunk_log2 = m;
+      }
+    }
+  }
   if (d->small) {
     s.ring_log2 = ceil_log2((uint64_t)(a1 + 128));
     s.ring_cover = (int32_t)a1;
@@ -634,6 +652,16 @@ struct pipedp_sdp_plan {
   int device;
   int64_t batch, n, k, a1;
   SdpDispatch d;
+  // chunked mode (d.chunked): G chunks of Lc cells, each an instance of n_i =
+  // a1 + Lc cells solved by the batch dispatch dc
+  int64_t G = 0, Lc = 0, n_i = 0;
+  int32_t W = 0;                       // 64-bit words per boolean matrix row
+  SdpDispatch dc{};
+  unsigned long long* d_bm = nullptr;  // X, XT, Z, ZT: [64 W][W] each
+  int64_t* d_E = nullptr;              // two state vectors [64 W]
+  int64_t* d_cinit = nullptr;          // [G][a1] chunk preset cells
+  int64_t* d_offs_rep = nullptr;       // [G][k]
+  int64_t* d_pad = nullptr;            // [G][n_i] chunk tables
   int64_t* d_offsets;  // device copy of the offsets, int64 [batch*k]
   void* d_remote;      // multi-CTA workspace: partial slots | ready flags | published
   int32_t* d_obg;      // remote producers: offsets as HBM-table byte offsets
@@ -1012,21 +1040,94 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
     e = cudaMalloc(&P->d_obg, sizeof(int32_t) * k);
     if (e == cudaSuccess) e = cudaMemcpy(P->d_obg, obg.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice);
   }
+  if (e == cudaSuccess && d.chunked) {
+    P->Lc = 1ll << d.chunk_log2;
+    P->G = (n - a1 + P->Lc - 1) / P->Lc;
+    P->n_i = a1 + P->Lc;
+    // 64-bit words per row: rows padded to 2048 bits (whole 128-wide product
+    // tiles and whole 64-word K stages)
+    P->W = (int32_t)((a1 + 2047) / 2048 * 32);
+    std::vector<int64_t> orep((size_t)(P->G * k)), irep((size_t)(P->G * a1));
+    for (int64_t g = 0; g < P->G; ++g) {
+      std::copy(h_offsets, h_offsets + k, orep.begin() + g * k);
+      std::copy(h_init, h_init + a1, irep.begin() + g * a1);
+    }
+    const int rc = plan_sdp(P->G, P->n_i, k, a1, orep.data(), irep.data(), op, &P->dc);
+    if (rc != PIPEDP_OK) {
+      pipedp_sdp_plan_destroy(P);
+      return rc;
+    }
+    const size_t mat = (size_t)64 * P->W * P->W;
+    e = cudaMalloc(&P->d_bm, sizeof(unsigned long long) * 4 * mat);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_E, sizeof(int64_t) * 2 * 64 * P->W + 256);  // + squaring flags
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_cinit, sizeof(int64_t) * P->G * a1);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_offs_rep, sizeof(int64_t) * P->G * k);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_pad, sizeof(int64_t) * P->G * P->n_i);
+    if (e == cudaSuccess)
+      e = cudaMemcpy(P->d_offs_rep, orep.data(), sizeof(int64_t) * P->G * k, cudaMemcpyHostToDevice);
+  }
   if (e != cudaSuccess) {
-    cudaFree(P->d_offsets);
-    cudaFree(P->d_remote);
-    cudaFree(P->d_obg);
-    delete P;
+    pipedp_sdp_plan_destroy(P);
     return cuda_fail(e, "sdp plan upload");
   }
   *plan_out = P;
   return PIPEDP_OK;
 }
 
+// Chunked mode (sdp_chunked.cuh): Q = M^Lc by boolean squarings, the chunk
+// entry states by Q (.) state, then all chunks as one batch.
+extern "C++" {
+template <int OP>
+static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64_t* d_cells, cudaStream_t st) {
+  const int32_t W = P->W, a1 = (int32_t)P->a1;
+  const size_t mat = (size_t)64 * W * W;
+  unsigned long long *X = P->d_bm, *XT = X + mat, *Z = XT + mat, *ZT = Z + mat;
+  CK(cudaMemsetAsync(X, 0, sizeof(unsigned long long) * 2 * mat, st));
+  bm_build<<<1, 1024, 0, st>>>(P->d_offsets, (int32_t)P->k, a1, W, X, XT);
+  CK(cudaGetLastError());
+  const size_t smem = sizeof(uint32_t) * (kBmR + kBmC) * (kBmK + 4);
+  CK(cudaFuncSetAttribute(bm_mul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const dim3 grid((unsigned)W, (unsigned)(W / 2));  // 128 x 64 output tiles
+  auto x32 = [](const unsigned long long* p) { return reinterpret_cast<const uint32_t*>(p); };
+  int* flags = reinterpret_cast<int*>(P->d_E + 2 * 64 * W);  // [chunk_log2] changed flags
+  CK(cudaMemsetAsync(flags, 0, sizeof(int) * 64, st));
+  for (int i = 0; i < P->d.chunk_log2; ++i) {  // X <- X X (then its transpose)
+    bm_mul<<<grid, 256, smem, st>>>(x32(X), x32(XT), 2 * W, Z, i ? flags + i - 1 : nullptr, flags + i);
+    bm_transpose<<<dim3((unsigned)W, (unsigned)W), 64, 0, st>>>(Z, W, ZT);
+    CK(cudaGetLastError());
+    std::swap(X, Z);
+    std::swap(XT, ZT);
+  }
+  int64_t* E[2] = {P->d_E, P->d_E + 64 * W};
+  CK(cudaFuncSetAttribute(bm_matvec<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)(sizeof(int64_t) * 64 * W)));
+  bm_state0<<<(a1 + 255) / 256, 256, 0, st>>>(d_init, a1, E[0], P->d_cinit);
+  for (int64_t g = 1; g < P->G; ++g)
+    bm_matvec<OP><<<(a1 + 7) / 8, 256, sizeof(int64_t) * 64 * W, st>>>(X, W, a1, E[(g - 1) & 1], E[g & 1],
+                                                                       P->d_cinit + g * a1);
+  CK(cudaGetLastError());
+  TRY(launch_sdp(P->dc, P->G, P->d_offs_rep, P->d_cinit, P->d_pad, SdpRemote{}, st));
+  // chunk tables -> the instance's table
+  CK(cudaMemcpyAsync(d_cells, d_init, sizeof(int64_t) * a1, cudaMemcpyDeviceToDevice, st));
+  if (P->G > 1)
+    CK(cudaMemcpy2DAsync(d_cells + a1, sizeof(int64_t) * P->Lc, P->d_pad + a1, sizeof(int64_t) * P->n_i,
+                         sizeof(int64_t) * P->Lc, (size_t)(P->G - 1), cudaMemcpyDeviceToDevice, st));
+  const int64_t last = P->n - a1 - (P->G - 1) * P->Lc;
+  CK(cudaMemcpyAsync(d_cells + a1 + (P->G - 1) * P->Lc, P->d_pad + (P->G - 1) * P->n_i + a1,
+                     sizeof(int64_t) * last, cudaMemcpyDeviceToDevice, st));
+  return PIPEDP_OK;
+}
+}  // extern "C++"
+
 // `armed` (optional) is recorded once the remote workspace is reset, before
 // the launch: copies ordered after it may read the progress counters.
 static int32_t sdp_execute(pipedp_sdp_plan_t P, const int64_t* d_init, int64_t* d_cells,
                            void* stream, cudaEvent_t armed) {
+  if (P->d.chunked) {
+    CK(cudaSetDevice(P->device));
+    return P->d.op == PIPEDP_OP_MAX ? sdp_chunked_run<kMax>(P, d_init, d_cells, (cudaStream_t)stream)
+                                    : sdp_chunked_run<kMin>(P, d_init, d_cells, (cudaStream_t)stream);
+  }
   CK(cudaSetDevice(P->device));
   SdpRemote rm{};
   if (P->d.remote) {
@@ -1087,9 +1188,14 @@ static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* 
 int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, int32_t* bits,
                                  int32_t* launches) {
   if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
-  if (name && cap) snprintf(name, cap, "%s", sdp_kernel_name(P->d));
-  if (bits) *bits = P->d.bits;
-  if (launches) *launches = 1;  // kernels (remote mode adds a memset + a prefix copy)
+  if (name && cap) {
+    if (P->d.chunked) snprintf(name, cap, "sdp_chunked[%s]", sdp_kernel_name(P->dc));
+    else snprintf(name, cap, "%s", sdp_kernel_name(P->d));
+  }
+  if (bits) *bits = P->d.chunked ? P->dc.bits : P->d.bits;
+  // kernels (remote mode adds a memset + a prefix copy); chunked: build,
+  // product + transpose per squaring, state 0, G - 1 matrix-vector steps, the batch
+  if (launches) *launches = P->d.chunked ? (int32_t)(1 + 2 * P->d.chunk_log2 + 1 + (P->G - 1) + 1) : 1;
   return PIPEDP_OK;
 }
 
@@ -1105,6 +1211,7 @@ int32_t pipedp_sdp_plan_set_method(pipedp_sdp_plan_t P, int32_t method) {
     P->d.bits = 64;
   }
   P->d.method = method;
+  if (method != PIPEDP_SDP_PIPELINE) P->d.chunked = false;  // the paper's methods run the instance as is
   return PIPEDP_OK;
 }
 
@@ -1114,6 +1221,11 @@ int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t P) {
   cudaFree(P->d_offsets);
   cudaFree(P->d_remote);
   cudaFree(P->d_obg);
+  cudaFree(P->d_bm);
+  cudaFree(P->d_E);
+  cudaFree(P->d_cinit);
+  cudaFree(P->d_offs_rep);
+  cudaFree(P->d_pad);
   delete P;
   return PIPEDP_OK;
 }

@@ -1,0 +1,173 @@
+// sdp_chunked.cuh -- one large min/max S-DP instance as independent chunks
+// (sm_100a).
+//
+// The recurrence reads a_1 cells back, so the table is a linear system on the
+// state s_t = (ST[t], ST[t-1], ..., ST[t-a_1+1]) over the idempotent semiring
+// of (x) (min or max):  s_{t+1} = M (.) s_t  with M[0][a_j - 1] = 1 for every
+// offset and M[r][r-1] = 1 (shift).  For an idempotent, commutative (x) the
+// product "(.)" is reachability: (M^L (.) s)[r] = (x) of s[c] over the c with
+// (M^L)[r][c] = 1, so the state L cells later is a boolean matrix power
+// applied to the state now.
+//
+// Cells [a_1, n) are cut into G chunks of L (a power of two).  Q = M^L is
+// formed by log2(L) boolean squarings (bit-packed rows, 64 x 64 output tiles,
+// AND/OR over 64-bit words; the transpose is carried along so both operands
+// of every product are read row-wise), the entry state of chunk g is
+// Q (.) (entry state of chunk g-1), and then every chunk is solved as one
+// instance of a batch by the regular pipeline kernels with its entry state as
+// the preset cells -- every cell's k relaxations run in the reference's
+// fold; the matrix powers only replace the serial dependency between chunks.
+#pragma once
+
+#include "common.cuh"
+
+namespace pipedp_dev {
+
+
+// Set the ones of M and M^T (bit-packed, W words per row; the host zeroes
+// both first).  Rows and columns >= a1 stay empty.
+__global__ void bm_build(const int64_t* __restrict__ offsets, int32_t k, int32_t a1, int32_t W,
+                         unsigned long long* __restrict__ M, unsigned long long* __restrict__ MT) {
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    const int c = (int)offsets[j] - 1;  // row 0, column a_j - 1
+    atomicOr(&M[c / 64], 1ull << (c % 64));
+    atomicOr(&MT[(int64_t)c * W], 1ull);  // row c of M^T, column 0
+  }
+  for (int64_t r = 1 + threadIdx.x; r < a1; r += blockDim.x) {
+    const int64_t c = r - 1;  // M[r][r-1]
+    atomicOr(&M[r * W + c / 64], 1ull << (c % 64));
+    atomicOr(&MT[c * W + r / 64], 1ull << (r % 64));
+  }
+}
+
+// Z = X * Y (boolean), given X (rows) and YT (rows of Y^T): Z[r][c] = any(X[r] & YT[c]).
+// Rows are read as 32-bit words; acc |= a & b is one LOP3.  CTA tile 128 rows
+// x 64 columns (one output word per row), thread tile 8 x 4, K staged through
+// shared memory 64 words at a time.  Grid (A1P/64, A1P/128).
+// Squaring support: `prev_changed` (nullable) = did the previous squaring
+// change the matrix; if not, X is idempotent (X X = X) and the tile is copied.
+// `changed` (nullable) records whether this product differs from X.
+constexpr int kBmR = 128;  // CTA output rows
+constexpr int kBmC = 64;   // CTA output columns (one 64-bit word)
+constexpr int kBmK = 64;   // 32-bit words per K stage
+__global__ void __launch_bounds__(256, 2) bm_mul(const uint32_t* __restrict__ X, const uint32_t* __restrict__ YT,
+                                                 int32_t W32, unsigned long long* __restrict__ Z,
+                                                 const int* __restrict__ prev_changed, int* __restrict__ changed) {
+  extern __shared__ __align__(16) uint32_t bm_smem[];
+  constexpr int P = kBmK + 4;  // padded pitch (words), 16-byte rows
+  uint32_t* xs = bm_smem;            // [128][P]
+  uint32_t* ys = bm_smem + kBmR * P;  // [64][P]
+  __shared__ unsigned long long zw[kBmR];
+  const int t = threadIdx.x;
+  const int64_t r0 = (int64_t)blockIdx.y * kBmR, c0 = (int64_t)blockIdx.x * kBmC;
+  const int W64 = W32 / 2;
+  const unsigned long long* X64 = reinterpret_cast<const unsigned long long*>(X);
+  if (prev_changed && *prev_changed == 0) {  // stable: X X = X
+    if (t < kBmR) Z[(r0 + t) * W64 + c0 / 64] = X64[(r0 + t) * W64 + c0 / 64];
+    return;
+  }
+  const int tr = t / 16, tc = t % 16;  // rows 8 tr .. +8, columns tc + 16 j (j < 4)
+  uint32_t acc[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0;
+  if (t < kBmR) zw[t] = 0;
+  for (int k0 = 0; k0 < W32; k0 += kBmK) {
+    __syncthreads();
+    for (int e = t; e < kBmR * (kBmK / 4); e += 256) {  // 16-byte loads
+      const int i = e / (kBmK / 4), q = e % (kBmK / 4);
+      *reinterpret_cast<uint4*>(xs + i * P + 4 * q) =
+          *reinterpret_cast<const uint4*>(X + (r0 + i) * W32 + k0 + 4 * q);
+      if (i < kBmC)
+        *reinterpret_cast<uint4*>(ys + i * P + 4 * q) =
+            *reinterpret_cast<const uint4*>(YT + (c0 + i) * W32 + k0 + 4 * q);
+    }
+    __syncthreads();
+#pragma unroll 4
+    for (int w = 0; w < kBmK; w += 4) {
+      uint4 a[8], b[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = *reinterpret_cast<const uint4*>(xs + (8 * tr + i) * P + w);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = *reinterpret_cast<const uint4*>(ys + (tc + 16 * j) * P + w);
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          acc[i][j] |= (a[i].x & b[j].x) | (a[i].y & b[j].y) | (a[i].z & b[j].z) | (a[i].w & b[j].w);
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    unsigned long long bits = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bits |= (unsigned long long)(acc[i][j] != 0) << (tc + 16 * j);
+    if (bits) atomicOr(&zw[8 * tr + i], bits);
+  }
+  __syncthreads();
+  if (t < kBmR) {
+    const int64_t o = (r0 + t) * W64 + c0 / 64;
+    Z[o] = zw[t];
+    if (changed && zw[t] != X64[o]) atomicOr(changed, 1);
+  }
+}
+
+// ZT = Z^T for bit-packed square matrices (W words per row): one 64 x 64 bit
+// block per CTA (64 threads), through shared memory.
+__global__ void __launch_bounds__(64) bm_transpose(const unsigned long long* __restrict__ Z, int32_t W,
+                                                   unsigned long long* __restrict__ ZT) {
+  __shared__ unsigned long long blk[64];
+  const int t = threadIdx.x;
+  const int64_t bi = blockIdx.y, bj = blockIdx.x;  // source block (rows 64 bi, word bj)
+  blk[t] = Z[(64 * bi + t) * W + bj];
+  __syncthreads();
+  unsigned long long out = 0;  // row t of the transposed block = bit t of every source row
+#pragma unroll 8
+  for (int i = 0; i < 64; ++i) out |= ((blk[i] >> t) & 1ull) << i;
+  ZT[(64 * bj + t) * W + bi] = out;
+}
+
+// E1 = Q (.) E0 over rows [0, a1): one warp per row; lane l takes columns
+// l + 32 i (coalesced E0 reads from shared memory, one broadcast word per
+// 64 columns), branch-free select, then a warp reduction.
+// Also writes the chunk's preset cells: init_out[a1 - 1 - r] = E1[r].
+template <int OP>
+__global__ void __launch_bounds__(256) bm_matvec(const unsigned long long* __restrict__ Q, int32_t W, int32_t a1,
+                                                 const int64_t* __restrict__ E0, int64_t* __restrict__ E1,
+                                                 int64_t* __restrict__ init_out) {
+  using O = SemiOp<OP, int64_t>;
+  extern __shared__ __align__(16) int64_t es[];  // [64 W]
+  for (int c = threadIdx.x; c < 64 * W; c += blockDim.x) es[c] = c < a1 ? E0[c] : SemiId<OP, int64_t>::value();
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= a1) return;
+  const int64_t id = SemiId<OP, int64_t>::value();
+  int64_t acc0 = id, acc1 = id;
+  const unsigned long long* qr = Q + r * W;
+  for (int w = 0; w < W; ++w) {
+    const unsigned long long bits = __ldg(qr + w);
+    const int64_t v0 = es[64 * w + lane], v1 = es[64 * w + 32 + lane];
+    acc0 = O::apply(acc0, (bits >> lane) & 1 ? v0 : id);
+    acc1 = O::apply(acc1, (bits >> (32 + lane)) & 1 ? v1 : id);
+  }
+  int64_t acc = O::apply(acc0, acc1);
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) acc = O::apply(acc, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)acc, s));
+  if (lane == 0) {
+    E1[r] = acc;
+    init_out[a1 - 1 - r] = acc;
+  }
+}
+
+// E0[r] = init[a1 - 1 - r] (state order) and chunk 0's preset cells = init.
+__global__ void bm_state0(const int64_t* __restrict__ init, int32_t a1, int64_t* __restrict__ E0,
+                          int64_t* __restrict__ init0) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < a1; r += gridDim.x * blockDim.x) {
+    E0[r] = init[a1 - 1 - r];
+    init0[r] = init[r];
+  }
+}
+
+}  // namespace pipedp_dev

@@ -238,3 +238,32 @@ def test_jump_fibonacci_saturates_like_reference(gpu, oracle):
     # the C1 shape: clamped counts in the jump matrices, INT64_MAX tail
     _check(gpu, oracle, [2, 1], [1, 1], 300000, "saturating-add")
     _check(gpu, oracle, [3, 2], [0, 5, 7], 100000, "saturating-add")
+
+
+@pytest.mark.parametrize("op", ["min", "max"])
+@pytest.mark.parametrize("shape", [(70000, 20, 64), (66000, 150, 300), (140000, 400, 1000), (560000, 1024, 4096)])
+def test_chunked_min_max(gpu, oracle, op, shape):
+    # one large min/max instance as a batch of chunks with entry states from
+    # boolean matrix powers (sdp_chunked.cuh); ragged last chunk
+    n, k, cap = shape
+    offs, init = oracle.generate_sdp(n + 777, k, 31, False, cap)
+    n = n + 777
+    plan = gpu.SdpPlan(1, n, len(offs), len(init), offs, init, op)
+    assert plan.describe()[0].startswith("sdp_chunked")
+    plan.close()
+    _check(gpu, oracle, offs, init, n, op)
+
+
+@pytest.mark.parametrize("op", ["min", "max"])
+def test_chunked_periodic_reachability(gpu, oracle, op):
+    # even offsets only (gcd 2): the matrix powers stay periodic, half the
+    # preset cells are unreachable from each cell
+    rng = np.random.default_rng(9)
+    a1 = 512
+    offs = np.array([512] + sorted(rng.choice(np.arange(2, 511, 2), 40, replace=False).tolist(), reverse=True))
+    init = rng.integers(-(2**40), 2**40, a1)
+    n = 16 * 4096 + a1 + 1234
+    plan = gpu.SdpPlan(1, n, len(offs), a1, offs, init, op)
+    assert plan.describe()[0].startswith("sdp_chunked")
+    plan.close()
+    _check(gpu, oracle, offs, init, n, op)
