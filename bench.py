@@ -436,7 +436,27 @@ def main():
         bits = W.value_bits()
         op_ns, op_cyc = pd.op_latency_ns(i.op, bits, local)
         hand_ns, _ = pd.chain_step_ns(i.op, bits, local) if (i.op, bits) != ("saturating-add", 32) else (None, None)
-        if W.kernel_name() == "sdp_jump":
+        kname = W.kernel_name()
+        if kname.startswith("sdp_chunked"):
+            # chunked: the longest dependent chains are one chunk's cells and
+            # the chunk entry-state chain (G matrix-vector steps)
+            L = 1 << max(12, (8 * i.a1 - 1).bit_length())
+            while (i.n - i.a1) // L >= 256:
+                L *= 2
+            G = -(-(i.n - i.a1) // L)
+            steps = L + G
+            definition = ("sdp_chunked: one chunk (L cells) + G entry-state steps, "
+                          "each x latency of one dependent (x)")
+            # relaxation phase: one 4-byte shared-memory operand read per relaxation
+            sms = torch.cuda.get_device_properties(0).multi_processor_count
+            smem_gbs = sms * 128 * 1.965e9 / 1e9  # 128 B/cycle/SM at the max SM clock
+            relax_bytes = (i.n - i.a1) * i.k * 4
+            extra["relaxation_roofline"] = {
+                "bound": "shared-memory bandwidth, one 4-byte operand read per relaxation",
+                "bytes": relax_bytes, "peak_gbs": smem_gbs, "floor_ms": relax_bytes / smem_gbs / 1e6,
+                "achieved_ms": avg_ms, "frac": relax_bytes / smem_gbs / 1e6 / avg_ms,
+                "chunks": G, "chunk_cells": L}
+        elif kname == "sdp_jump":
             # jump-ahead segments: the longest dependent chain is one 64-cell
             # segment after its entry state (log2(segments) matrix levels)
             nseg = -(-(i.n - i.a1) // 64)

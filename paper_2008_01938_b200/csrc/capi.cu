@@ -1059,7 +1059,7 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
     }
     const size_t mat = (size_t)64 * P->W * P->W;
     e = cudaMalloc(&P->d_bm, sizeof(unsigned long long) * 4 * mat);
-    if (e == cudaSuccess) e = cudaMalloc(&P->d_E, sizeof(int64_t) * 2 * 64 * P->W + 256);  // + squaring flags
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_E, sizeof(int64_t) * 2 * 64 * P->W + 512);  // + flags, barrier
     if (e == cudaSuccess) e = cudaMalloc(&P->d_cinit, sizeof(int64_t) * P->G * a1);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_offs_rep, sizeof(int64_t) * P->G * k);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_pad, sizeof(int64_t) * P->G * P->n_i);
@@ -1102,10 +1102,29 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
   CK(cudaFuncSetAttribute(bm_matvec<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(sizeof(int64_t) * 64 * W)));
   bm_state0<<<(a1 + 255) / 256, 256, 0, st>>>(d_init, a1, E[0], P->d_cinit);
-  for (int64_t g = 1; g < P->G; ++g)
-    bm_matvec<OP><<<(a1 + 7) / 8, 256, sizeof(int64_t) * 64 * W, st>>>(X, W, a1, E[(g - 1) & 1], E[g & 1],
-                                                                       P->d_cinit + g * a1);
-  CK(cudaGetLastError());
+  if (env_int("PIPEDP_SDP_CHAIN_PERSISTENT", 1) != 0) {
+    // one persistent launch for the whole chain (grid barrier between steps)
+    unsigned* bar = reinterpret_cast<unsigned*>(flags + 64);
+    CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st));
+    const size_t es = sizeof(int64_t) * 64 * W;
+    CK(cudaFuncSetAttribute(bm_chain<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)es));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bm_chain<OP>, 1024, es));
+    if (per_sm < 1) return fail(PIPEDP_ERR_UNSUPPORTED, "bm_chain does not fit an SM");
+    const int nblk = std::min(sm_count(), (a1 + 31) / 32);
+    const unsigned long long* q = X;
+    int32_t w = W, a = a1;
+    int64_t gg = P->G;
+    int64_t* e0 = P->d_E;
+    int64_t* ci = P->d_cinit;
+    void* args[] = {(void*)&q, (void*)&w, (void*)&a, (void*)&gg, (void*)&e0, (void*)&ci, (void*)&bar};
+    CK(cudaLaunchCooperativeKernel((const void*)bm_chain<OP>, dim3((unsigned)nblk), dim3(1024), args, es, st));
+  } else {
+    for (int64_t g = 1; g < P->G; ++g)
+      bm_matvec<OP><<<(a1 + 7) / 8, 256, sizeof(int64_t) * 64 * W, st>>>(X, W, a1, E[(g - 1) & 1], E[g & 1],
+                                                                         P->d_cinit + g * a1);
+    CK(cudaGetLastError());
+  }
   TRY(launch_sdp(P->dc, P->G, P->d_offs_rep, P->d_cinit, P->d_pad, SdpRemote{}, st));
   // chunk tables -> the instance's table
   CK(cudaMemcpyAsync(d_cells, d_init, sizeof(int64_t) * a1, cudaMemcpyDeviceToDevice, st));
@@ -1161,6 +1180,7 @@ static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* 
   if (!(P->d.remote && P->batch == 1 && P->d.method == PIPEDP_SDP_PIPELINE) || bytes < (64u << 20) ||
       env_int("PIPEDP_STREAM_D2H", 1) == 0) {
     TRY(sdp_execute(P, d_init, d_cells, W->stream, nullptr));
+    if (bytes >= (16u << 20)) pipedp_host::parallel_prefault(cells_out, bytes);  // overlaps the kernel
     CK(W->d2h(cells_out, d_cells, bytes));
     return PIPEDP_OK;
   }
@@ -1194,8 +1214,8 @@ int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, in
   }
   if (bits) *bits = P->d.chunked ? P->dc.bits : P->d.bits;
   // kernels (remote mode adds a memset + a prefix copy); chunked: build,
-  // product + transpose per squaring, state 0, G - 1 matrix-vector steps, the batch
-  if (launches) *launches = P->d.chunked ? (int32_t)(1 + 2 * P->d.chunk_log2 + 1 + (P->G - 1) + 1) : 1;
+  // product + transpose per squaring, state 0, the persistent chain, the batch
+  if (launches) *launches = P->d.chunked ? (int32_t)(1 + 2 * P->d.chunk_log2 + 1 + 1 + 1) : 1;
   return PIPEDP_OK;
 }
 
@@ -1492,7 +1512,17 @@ static int32_t mcm_solve_host(int64_t batch, int64_t n, const int64_t* dims, int
   void *d_cells = nullptr, *d_split = nullptr;
   CK(W->buffer(1, sizeof(int64_t) * size, &d_cells));
   CK(W->buffer(2, sizeof(int64_t) * size, &d_split));
-  TRY(pipedp_mcm_plan_execute(P, (int64_t*)d_cells, (int64_t*)d_split, W->stream));
+  // first-touch the host outputs while the kernels run (execute may wait on
+  // the device for the overflow check)
+  std::thread touch;
+  if (sizeof(int64_t) * size >= (16u << 20))
+    touch = std::thread([&] {
+      pipedp_host::parallel_prefault(cells_out, sizeof(int64_t) * size);
+      if (split_out) pipedp_host::parallel_prefault(split_out, sizeof(int64_t) * size);
+    });
+  const int32_t rc = pipedp_mcm_plan_execute(P, (int64_t*)d_cells, (int64_t*)d_split, W->stream);
+  if (touch.joinable()) touch.join();
+  TRY(rc);
   CK(W->d2h(cells_out, d_cells, sizeof(int64_t) * size));
   if (split_out) CK(W->d2h(split_out, d_split, sizeof(int64_t) * size));
   return PIPEDP_OK;

@@ -113,6 +113,19 @@ inline void parallel_memcpy(void* dst, const void* src, size_t bytes) {
   });
 }
 
+// Touch every page of a pageable destination (one write per 4 KiB, split over
+// the pool) so the later copy does not take the first-touch faults; run while
+// the kernel that produces the data is still executing.
+inline void parallel_prefault(void* dst, size_t bytes) {
+  constexpr size_t kPage = 4096, kPiece = 8u << 20;
+  const int pieces = (int)((bytes + kPiece - 1) / kPiece);
+  CopyPool::get().parallel_for(pieces, [&](int i) {
+    char* p = static_cast<char*>(dst) + (size_t)i * kPiece;
+    const size_t len = std::min(kPiece, bytes - (size_t)i * kPiece);
+    for (size_t o = 0; o < len; o += kPage) reinterpret_cast<volatile char*>(p)[o] = 0;
+  });
+}
+
 // Per-thread, per-device transfer workspace.
 struct Workspace {
   static constexpr size_t kChunk = 64u << 20;
@@ -250,6 +263,14 @@ struct Workspace {
 
   // device -> pageable host after the work queued on `stream`; synchronous
   cudaError_t d2h(void* dst, const void* src, size_t bytes) {
+    static const int mode = [] {
+      const char* v = getenv("PIPEDP_D2H_MODE");
+      return v && *v ? atoi(v) : 0;
+    }();
+    if (mode == 1) {  // the driver's own pageable path
+      cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream);
+      return e == cudaSuccess ? cudaStreamSynchronize(stream) : e;
+    }
     const size_t nchunks = (bytes + kChunk - 1) / kChunk;
     auto issue = [&](size_t c) {
       const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);

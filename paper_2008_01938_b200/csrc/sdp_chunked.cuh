@@ -161,6 +161,57 @@ __global__ void __launch_bounds__(256) bm_matvec(const unsigned long long* __res
   }
 }
 
+// The whole entry-state chain in one persistent launch (one CTA per SM, all
+// co-resident): step g computes E_g = Q (.) E_{g-1} and chunk g's preset
+// cells, then a grid barrier.  E is exchanged through L2 (ld.cg).
+template <int OP>
+__global__ void __launch_bounds__(1024, 1) bm_chain(const unsigned long long* __restrict__ Q, int32_t W,
+                                                    int32_t a1, int64_t G, int64_t* E, int64_t* cinit,
+                                                    unsigned* bar) {
+  using O = SemiOp<OP, int64_t>;
+  extern __shared__ __align__(16) int64_t es[];  // [64 W]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int64_t id = SemiId<OP, int64_t>::value();
+  for (int64_t g = 1; g < G; ++g) {
+    const int64_t* src = E + ((g - 1) & 1) * 64 * W;
+    int64_t* dst = E + (g & 1) * 64 * W;
+    for (int c = threadIdx.x; c < 64 * W; c += blockDim.x)
+      es[c] = c < a1 ? (int64_t)__ldcg(reinterpret_cast<const long long*>(src) + c) : id;
+    __syncthreads();
+    for (int64_t r = (int64_t)blockIdx.x * nw + warp; r < a1; r += (int64_t)gridDim.x * nw) {
+      int64_t acc0 = id, acc1 = id;
+      const unsigned long long* qr = Q + r * W;
+      for (int w = 0; w < W; ++w) {
+        const unsigned long long bits = __ldg(qr + w);
+        acc0 = O::apply(acc0, (bits >> lane) & 1 ? es[64 * w + lane] : id);
+        acc1 = O::apply(acc1, (bits >> (32 + lane)) & 1 ? es[64 * w + 32 + lane] : id);
+      }
+      int64_t acc = O::apply(acc0, acc1);
+#pragma unroll
+      for (int s = 16; s >= 1; s >>= 1) acc = O::apply(acc, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)acc, s));
+      if (lane == 0) {
+        dst[r] = acc;
+        cinit[g * a1 + a1 - 1 - r] = acc;
+      }
+    }
+    // grid barrier (generation counter)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned gen = (unsigned)ld_relaxed_gpu_i32(reinterpret_cast<const int*>(bar + 1));
+      __threadfence();
+      if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+        atomicExch(bar, 0u);
+        __threadfence();
+        atomicAdd(bar + 1, 1u);
+      } else {
+        while ((unsigned)ld_relaxed_gpu_i32(reinterpret_cast<const int*>(bar + 1)) == gen) __nanosleep(32);
+      }
+      __threadfence();
+    }
+    __syncthreads();
+  }
+}
+
 // E0[r] = init[a1 - 1 - r] (state order) and chunk 0's preset cells = init.
 __global__ void bm_state0(const int64_t* __restrict__ init, int32_t a1, int64_t* __restrict__ E0,
                           int64_t* __restrict__ init0) {

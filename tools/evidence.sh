@@ -11,11 +11,12 @@ for w in c1 c3 c4 c5a c5b; do
   timeout 600 python bench.py --workload $w > $O/bench_$w.json 2> $O/bench_$w.err; tail -c 200 $O/bench_$w.json; echo
 done
 timeout 600 python bench.py --impl reference > $O/bench_ref_c2.json 2>&1; tail -c 200 $O/bench_ref_c2.json; echo
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $O/launches_c2.csv \
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $O/launches_c2.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
-K='regex:sdp_v2|mcm_tiled|mcm_smem|sdp_batch|sdp_serial'
-for w in c2 c3 c4 c5a c5b; do
-  timeout 600 ncu --set full --clock-control none --import-source on -k "$K" -c 1 -f -o /tmp/ncu_$w \
+declare -A K=([c1]='regex:sdp_jump' [c2]='regex:sdp_pipeline_cta' [c3]='regex:mcm_tiled' [c4]='regex:mcm_tiled'
+             [c5a]='regex:mcm_smem' [c5b]='regex:sdp_batch')
+for w in c1 c2 c3 c4 c5a c5b; do
+  timeout 600 ncu --set full --clock-control none --import-source on -k "${K[$w]}" -c 1 -f -o /tmp/ncu_$w \
     python bench.py --workload $w --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
   ncu -i /tmp/ncu_$w.ncu-rep --page raw --csv > $O/ncu_full_$w.raw.csv 2>/dev/null
   ncu -i /tmp/ncu_$w.ncu-rep --page details --csv > $O/ncu_full_$w.details.csv 2>/dev/null
