@@ -658,6 +658,7 @@ struct pipedp_sdp_plan {
   int32_t W = 0;                       // 64-bit words per boolean matrix row
   SdpDispatch dc{};
   unsigned long long* d_bm = nullptr;  // X, XT, Z, ZT: [64 W][W] each
+  unsigned long long* d_q = nullptr;   // Q = M^Lc kept while Q^16 is formed
   int64_t* d_E = nullptr;              // two state vectors [64 W]
   int64_t* d_cinit = nullptr;          // [G][a1] chunk preset cells
   int64_t* d_offs_rep = nullptr;       // [G][k]
@@ -1059,6 +1060,7 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
     }
     const size_t mat = (size_t)64 * P->W * P->W;
     e = cudaMalloc(&P->d_bm, sizeof(unsigned long long) * 4 * mat);
+    if (e == cudaSuccess) e = cudaMalloc(&P->d_q, sizeof(unsigned long long) * mat);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_E, sizeof(int64_t) * 2 * 64 * P->W + 512);  // + flags, barrier
     if (e == cudaSuccess) e = cudaMalloc(&P->d_cinit, sizeof(int64_t) * P->G * a1);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_offs_rep, sizeof(int64_t) * P->G * k);
@@ -1102,22 +1104,36 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
   CK(cudaFuncSetAttribute(bm_matvec<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(sizeof(int64_t) * 64 * W)));
   bm_state0<<<(a1 + 255) / 256, 256, 0, st>>>(d_init, a1, E[0], P->d_cinit);
+  const int B = P->G >= 64 ? 16 : 1;  // two-level chain block
   if (env_int("PIPEDP_SDP_CHAIN_PERSISTENT", 1) != 0) {
-    // one persistent launch for the whole chain (grid barrier between steps)
+    // Q_B = Q^B: log2(B) more squarings of the saved Q
+    const unsigned long long* Q = X;
+    unsigned long long* QB = X;
+    if (B > 1) {
+      CK(cudaMemcpyAsync(P->d_q, X, sizeof(unsigned long long) * mat, cudaMemcpyDeviceToDevice, st));
+      Q = P->d_q;
+      for (int b = 1, i = P->d.chunk_log2; b < B; b *= 2, ++i) {
+        bm_mul<<<grid, 256, smem, st>>>(x32(X), x32(XT), 2 * W, Z, flags + i - 1, flags + i);
+        bm_transpose<<<dim3((unsigned)W, (unsigned)W), 64, 0, st>>>(Z, W, ZT);
+        CK(cudaGetLastError());
+        std::swap(X, Z);
+        std::swap(XT, ZT);
+      }
+      QB = X;
+    }
     unsigned* bar = reinterpret_cast<unsigned*>(flags + 64);
     CK(cudaMemsetAsync(bar, 0, 2 * sizeof(unsigned), st));
-    const size_t es = sizeof(int64_t) * 64 * W;
+    const size_t es = sizeof(int64_t) * 65 * W;  // E + per-word (x)
     CK(cudaFuncSetAttribute(bm_chain<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)es));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, bm_chain<OP>, 1024, es));
     if (per_sm < 1) return fail(PIPEDP_ERR_UNSUPPORTED, "bm_chain does not fit an SM");
-    const int nblk = std::min(sm_count(), (a1 + 31) / 32);
-    const unsigned long long* q = X;
-    int32_t w = W, a = a1;
+    const int nblk = sm_count();
+    const unsigned long long* qb = QB;
+    int32_t bb = B, w = W, a = a1;
     int64_t gg = P->G;
-    int64_t* e0 = P->d_E;
     int64_t* ci = P->d_cinit;
-    void* args[] = {(void*)&q, (void*)&w, (void*)&a, (void*)&gg, (void*)&e0, (void*)&ci, (void*)&bar};
+    void* args[] = {(void*)&Q, (void*)&qb, (void*)&bb, (void*)&w, (void*)&a, (void*)&gg, (void*)&ci, (void*)&bar};
     CK(cudaLaunchCooperativeKernel((const void*)bm_chain<OP>, dim3((unsigned)nblk), dim3(1024), args, es, st));
   } else {
     for (int64_t g = 1; g < P->G; ++g)
@@ -1242,6 +1258,7 @@ int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t P) {
   cudaFree(P->d_remote);
   cudaFree(P->d_obg);
   cudaFree(P->d_bm);
+  cudaFree(P->d_q);
   cudaFree(P->d_E);
   cudaFree(P->d_cinit);
   cudaFree(P->d_offs_rep);

@@ -161,54 +161,99 @@ __global__ void __launch_bounds__(256) bm_matvec(const unsigned long long* __res
   }
 }
 
-// The whole entry-state chain in one persistent launch (one CTA per SM, all
-// co-resident): step g computes E_g = Q (.) E_{g-1} and chunk g's preset
-// cells, then a grid barrier.  E is exchanged through L2 (ld.cg).
+// Grid barrier for a co-resident (cooperative) grid: generation counter.
+__device__ __forceinline__ void bm_grid_sync(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = (unsigned)ld_relaxed_gpu_i32(reinterpret_cast<const int*>(bar + 1));
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while ((unsigned)ld_relaxed_gpu_i32(reinterpret_cast<const int*>(bar + 1)) == gen) __nanosleep(32);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// One warp's row of P (.) E into chunk dst's preset cells (state order r ->
+// cell a1 - 1 - r); E is in shared memory in state order, wmin[w] = (x) of
+// E's 64 entries under word w.  Lane l takes words l, l + 32, ...: a full word
+// contributes wmin[w] (one operation for 64 columns -- dense powers are the
+// common case), a partial word its set bits one by one.
 template <int OP>
-__global__ void __launch_bounds__(1024, 1) bm_chain(const unsigned long long* __restrict__ Q, int32_t W,
-                                                    int32_t a1, int64_t G, int64_t* E, int64_t* cinit,
+__device__ __forceinline__ void bm_row(const unsigned long long* __restrict__ P, int32_t W, int32_t a1, int64_t r,
+                                       const int64_t* es, const int64_t* wmin, int64_t* dst_init) {
+  using O = SemiOp<OP, int64_t>;
+  const int lane = threadIdx.x & 31;
+  int64_t acc = SemiId<OP, int64_t>::value();
+  const unsigned long long* qr = P + r * W;
+  for (int w = lane; w < W; w += 32) {
+    unsigned long long bits = __ldg(qr + w);
+    if (bits == ~0ull) {
+      acc = O::apply(acc, wmin[w]);
+    } else {
+      while (bits) {
+        const int b = __ffsll((long long)bits) - 1;
+        bits &= bits - 1;
+        acc = O::apply(acc, es[64 * w + b]);
+      }
+    }
+  }
+#pragma unroll
+  for (int s = 16; s >= 1; s >>= 1) acc = O::apply(acc, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)acc, s));
+  if (lane == 0) dst_init[a1 - 1 - r] = acc;
+}
+
+// The entry-state chain in one persistent launch (all CTAs co-resident).
+// Chunk g's preset cells cinit[g] are E_g in cell order.  Two levels:
+//   A: E_{B m} = Q_B (.) E_{B (m-1)}          (Q_B = Q^B; G/B sequential steps)
+//   B: E_{B m + j} = Q (.) E_{B m + j - 1}   (all groups m at once; B - 1 steps)
+// so G - 1 dependent steps become G/B + B - 2 (B = 16 for G = 256: 30).
+template <int OP>
+__global__ void __launch_bounds__(1024, 1) bm_chain(const unsigned long long* __restrict__ Q,
+                                                    const unsigned long long* __restrict__ QB, int32_t B,
+                                                    int32_t W, int32_t a1, int64_t G, int64_t* cinit,
                                                     unsigned* bar) {
   using O = SemiOp<OP, int64_t>;
-  extern __shared__ __align__(16) int64_t es[];  // [64 W]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  extern __shared__ __align__(16) int64_t es[];  // [64 W] E, then [W] per-word (x)
+  int64_t* wmin = es + 64 * W;
+  const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5, lane = threadIdx.x & 31;
   const int64_t id = SemiId<OP, int64_t>::value();
-  for (int64_t g = 1; g < G; ++g) {
-    const int64_t* src = E + ((g - 1) & 1) * 64 * W;
-    int64_t* dst = E + (g & 1) * 64 * W;
-    for (int c = threadIdx.x; c < 64 * W; c += blockDim.x)
-      es[c] = c < a1 ? (int64_t)__ldcg(reinterpret_cast<const long long*>(src) + c) : id;
+  auto load = [&](int64_t g) {  // E_g (state order) from chunk g's preset cells
+    const long long* src = reinterpret_cast<const long long*>(cinit + g * a1);
+    for (int c = threadIdx.x; c < 64 * W; c += blockDim.x) es[c] = c < a1 ? (int64_t)__ldcg(src + a1 - 1 - c) : id;
     __syncthreads();
-    for (int64_t r = (int64_t)blockIdx.x * nw + warp; r < a1; r += (int64_t)gridDim.x * nw) {
-      int64_t acc0 = id, acc1 = id;
-      const unsigned long long* qr = Q + r * W;
-      for (int w = 0; w < W; ++w) {
-        const unsigned long long bits = __ldg(qr + w);
-        acc0 = O::apply(acc0, (bits >> lane) & 1 ? es[64 * w + lane] : id);
-        acc1 = O::apply(acc1, (bits >> (32 + lane)) & 1 ? es[64 * w + 32 + lane] : id);
-      }
-      int64_t acc = O::apply(acc0, acc1);
+    for (int w = warp; w < W; w += nw) {  // one warp per word
+      int64_t v = O::apply(es[64 * w + lane], es[64 * w + 32 + lane]);
 #pragma unroll
-      for (int s = 16; s >= 1; s >>= 1) acc = O::apply(acc, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)acc, s));
-      if (lane == 0) {
-        dst[r] = acc;
-        cinit[g * a1 + a1 - 1 - r] = acc;
-      }
-    }
-    // grid barrier (generation counter)
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned gen = (unsigned)ld_relaxed_gpu_i32(reinterpret_cast<const int*>(bar + 1));
-      __threadfence();
-      if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-        atomicExch(bar, 0u);
-        __threadfence();
-        atomicAdd(bar + 1, 1u);
-      } else {
-        while ((unsigned)ld_relaxed_gpu_i32(reinterpret_cast<const int*>(bar + 1)) == gen) __nanosleep(32);
-      }
-      __threadfence();
+      for (int s = 16; s >= 1; s >>= 1) v = O::apply(v, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)v, s));
+      if (lane == 0) wmin[w] = v;
     }
     __syncthreads();
+  };
+  const int64_t groups = (G + B - 1) / B;
+  // A: the group heads, every CTA on one matrix-vector product per step
+  for (int64_t m = 1; m < groups; ++m) {
+    load(B * (m - 1));
+    for (int64_t r = (int64_t)blockIdx.x * nw + warp; r < a1; r += (int64_t)gridDim.x * nw)
+      bm_row<OP>(QB, W, a1, r, es, wmin, cinit + B * m * a1);
+    bm_grid_sync(bar);
+  }
+  // B: inside every group at once; CTA b serves group b % groups
+  const int64_t m = blockIdx.x % groups;
+  const int64_t per = gridDim.x / groups + ((int64_t)(blockIdx.x % groups) < (int64_t)(gridDim.x % groups) ? 1 : 0);
+  const int64_t slot = blockIdx.x / groups;  // this CTA's index among its group's CTAs
+  for (int j = 1; j < B; ++j) {
+    const int64_t g = B * m + j;
+    if (g < G && per > 0) {
+      load(g - 1);
+      for (int64_t r = slot * nw + warp; r < a1; r += per * nw) bm_row<OP>(Q, W, a1, r, es, wmin, cinit + g * a1);
+    }
+    bm_grid_sync(bar);
   }
 }
 
