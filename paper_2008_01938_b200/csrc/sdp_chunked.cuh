@@ -49,7 +49,7 @@ __global__ void bm_build(const int64_t* __restrict__ offsets, int32_t k, int32_t
 // `changed` (nullable) records whether this product differs from X.
 constexpr int kBmR = 128;  // CTA output rows
 constexpr int kBmC = 64;   // CTA output columns (one 64-bit word)
-constexpr int kBmK = 64;   // 32-bit words per K stage
+constexpr int kBmK = 32;   // 32-bit words per K stage (early exit between stages)
 __global__ void __launch_bounds__(256, 2) bm_mul(const uint32_t* __restrict__ X, const uint32_t* __restrict__ YT,
                                                  int32_t W32, unsigned long long* __restrict__ Z,
                                                  const int* __restrict__ prev_changed, int* __restrict__ changed) {
@@ -75,16 +75,19 @@ __global__ void __launch_bounds__(256, 2) bm_mul(const uint32_t* __restrict__ X,
   if (t < kBmR) zw[t] = 0;
   for (int k0 = 0; k0 < W32; k0 += kBmK) {
     __syncthreads();
+    bool nz = false;
     for (int e = t; e < kBmR * (kBmK / 4); e += 256) {  // 16-byte loads
       const int i = e / (kBmK / 4), q = e % (kBmK / 4);
-      *reinterpret_cast<uint4*>(xs + i * P + 4 * q) =
-          *reinterpret_cast<const uint4*>(X + (r0 + i) * W32 + k0 + 4 * q);
+      const uint4 xv = *reinterpret_cast<const uint4*>(X + (r0 + i) * W32 + k0 + 4 * q);
+      *reinterpret_cast<uint4*>(xs + i * P + 4 * q) = xv;
+      nz = nz || (xv.x | xv.y | xv.z | xv.w) != 0;
       if (i < kBmC)
         *reinterpret_cast<uint4*>(ys + i * P + 4 * q) =
             *reinterpret_cast<const uint4*>(YT + (c0 + i) * W32 + k0 + 4 * q);
     }
-    __syncthreads();
-#pragma unroll 4
+    // an all-zero X stage contributes nothing (sparse early powers: mostly shifts)
+    if (!__syncthreads_or(nz)) continue;
+#pragma unroll 2
     for (int w = 0; w < kBmK; w += 4) {
       uint4 a[8], b[4];
 #pragma unroll
@@ -97,6 +100,13 @@ __global__ void __launch_bounds__(256, 2) bm_mul(const uint32_t* __restrict__ X,
         for (int j = 0; j < 4; ++j)
           acc[i][j] |= (a[i].x & b[j].x) | (a[i].y & b[j].y) | (a[i].z & b[j].z) | (a[i].w & b[j].w);
     }
+    // every output of the tile already 1: the remaining K stages cannot change it
+    bool full = true;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) full = full && acc[i][j] != 0;
+    if (__syncthreads_and(full)) break;
   }
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
