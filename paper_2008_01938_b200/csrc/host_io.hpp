@@ -271,9 +271,16 @@ struct Workspace {
       cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream);
       return e == cudaSuccess ? cudaStreamSynchronize(stream) : e;
     }
-    const size_t nchunks = (bytes + kChunk - 1) / kChunk;
+    // piece size (PIPEDP_D2H_PIECE_MB, default the whole 64 MiB buffer: smaller
+    // pieces measured slower -- per-call pool overhead outweighs the overlap)
+    static const size_t piece = [] {
+      const char* v = getenv("PIPEDP_D2H_PIECE_MB");
+      const size_t mb = v && *v ? (size_t)atoi(v) : 64;
+      return std::min(kChunk, std::max<size_t>(1, mb) << 20);
+    }();
+    const size_t nchunks = (bytes + piece - 1) / piece;
     auto issue = [&](size_t c) {
-      const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+      const size_t off = c * piece, len = std::min(piece, bytes - off);
       cudaError_t e = cudaMemcpyAsync(pinned[c & 1], static_cast<const char*>(src) + off, len,
                                       cudaMemcpyDeviceToHost, stream);
       return e == cudaSuccess ? cudaEventRecord(ev[c & 1], stream) : e;
@@ -284,7 +291,7 @@ struct Workspace {
       if (c + 1 < nchunks) e = issue(c + 1);  // overlaps the host copy of chunk c
       if (e == cudaSuccess) e = cudaEventSynchronize(ev[c & 1]);
       if (e != cudaSuccess) break;
-      const size_t off = c * kChunk, len = std::min(kChunk, bytes - off);
+      const size_t off = c * piece, len = std::min(piece, bytes - off);
       parallel_memcpy(static_cast<char*>(dst) + off, pinned[c & 1], len);
     }
     return e;
