@@ -1,1 +1,2 @@
-for pm in 64 16 8; do for w in c2 c4 c5b; do PIPEDP_D2H_PIECE_MB=$pm timeout 300 python bench.py --workload $w --no-cpu-baseline --steps 3 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('piece $pm $w', round(d['ms_per_step'],2), round(d['e2e']['ms_per_step'],2))"; done; done
+timeout 600 python -m pytest tests/test_gpu_sdp.py -x -q -k "chunked" 2>&1 | tail -2
+timeout 200 python bench.py --workload c2 --no-cpu-baseline --steps 3 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c2', round(d['ms_per_step'],2), d['e2e']['ms_per_step'], d['parity']['match'], d['roofline']['kernel'], d['relaxation_roofline']['frac'])"
