@@ -1,2 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_sdp.py -x -q -k "chunked" 2>&1 | tail -2
-timeout 200 python bench.py --workload c2 --no-cpu-baseline --steps 3 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('c2', round(d['ms_per_step'],2), d['e2e']['ms_per_step'], d['parity']['match'], d['roofline']['kernel'], d['relaxation_roofline']['frac'])"
+for g in 256 444 512; do for fm in 3 4 6 8; do G=$g TAG="far$fm mid1" PIPEDP_SDP_FAR_MAX=$fm PIPEDP_SDP_MID_WARPS=1 PYTHONPATH=. timeout 100 python tools/chunk_probe.py 2>&1 | tail -1; done; done
