@@ -267,3 +267,24 @@ def test_chunked_periodic_reachability(gpu, oracle, op):
     assert plan.describe()[0].startswith("sdp_chunked")
     plan.close()
     _check(gpu, oracle, offs, init, n, op)
+
+
+@pytest.mark.parametrize("a1,k,op", [(7000, 300, "min"), (8192, 1500, "max")])
+def test_chunked_wide_state(gpu, oracle, a1, k, op):
+    # a_1 > 4096: 128-word matrix rows (the padded 8192-bit state)
+    n = 16 * 65536 + a1 + 4321
+    offs, init = oracle.generate_sdp(n, k, 5, False, a1)
+    assert offs[0] == a1
+    plan = gpu.SdpPlan(1, n, len(offs), len(init), offs, init, op)
+    assert plan.describe()[0].startswith("sdp_chunked")
+    plan.close()
+    _check(gpu, oracle, offs, init, n, op)
+
+
+def test_chunked_equals_pipeline(gpu, monkeypatch):
+    # the same instance through the chunked mode and the pipeline-only path
+    inst = gpu.generate_sdp(n=1_200_000, k=512, op="min", seed=4, a1_cap=4096)
+    a = gpu.solve_sequential(inst).cells
+    monkeypatch.setenv("PIPEDP_SDP_CHUNKED", "0")
+    b = gpu.solve_sequential(inst).cells
+    assert np.array_equal(a, b)
