@@ -7,14 +7,18 @@
 //                          lin/coord/deps, generators, digests
 //   dropin_test nogpu      every solver must throw pipedp::DeviceError (no CPU path)
 //   dropin_test solve      GPU: prints "<case> <cells digest> [<split digest>]" lines
+//   dropin_test io         host-side: instance text round trips, batched loader,
+//                          parenthesisation from a split table
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <sstream>
 #include <string>
 #include <vector>
 
 #include "pipedp/error.hpp"
 #include "pipedp/generate.hpp"
+#include "pipedp/io.hpp"
 #include "pipedp/mcm.hpp"
 #include "pipedp/mcm_pipeline.hpp"
 #include "pipedp/sdp.hpp"
@@ -199,12 +203,102 @@ static int run_solve() {
   return failures ? 1 : 0;
 }
 
+// host MCM DP (test-side, tiny n) for a split table in the reference layout
+static std::vector<std::int64_t> host_split(const McmInstance& m, std::int64_t* best_cost) {
+  const std::int64_t n = m.n();
+  std::vector<std::int64_t> cost((size_t)cell_count(n) + 1, 0), split((size_t)cell_count(n) + 1, 0);
+  for (std::int64_t D = 1; D < n; ++D)
+    for (std::int64_t r = 1; r + D <= n; ++r) {
+      const std::int64_t c = r + D, a = lin(TriCoord{r, c}, n);
+      std::int64_t best = INT64_MAX, bj = 0;
+      for (std::int64_t j = 1; j <= D; ++j) {
+        const std::int64_t k = r + j - 1;
+        const std::int64_t v = cost[(size_t)lin(TriCoord{r, k}, n)] + cost[(size_t)lin(TriCoord{k + 1, c}, n)] +
+                               m.dims[(size_t)(r - 1)] * m.dims[(size_t)k] * m.dims[(size_t)c];
+        if (v < best) best = v, bj = j;
+      }
+      cost[(size_t)a] = best;
+      split[(size_t)a] = bj;
+    }
+  *best_cost = n > 1 ? cost[(size_t)apex_address(n)] : 0;
+  return split;
+}
+
+// cost of a parenthesised product string over dims (A1..An)
+static std::int64_t paren_cost(const std::string& s, const std::vector<std::int64_t>& p, size_t& i,
+                               std::int64_t& rows, std::int64_t& cols) {
+  if (s[i] == 'A') {
+    ++i;
+    std::int64_t idx = 0;
+    while (i < s.size() && s[i] >= '0' && s[i] <= '9') idx = idx * 10 + (s[i++] - '0');
+    rows = p[(size_t)idx - 1];
+    cols = p[(size_t)idx];
+    return 0;
+  }
+  ++i;  // '('
+  std::int64_t r1, c1, r2, c2;
+  const std::int64_t a = paren_cost(s, p, i, r1, c1), b = paren_cost(s, p, i, r2, c2);
+  ++i;  // ')'
+  rows = r1;
+  cols = c2;
+  return a + b + r1 * c1 * c2;
+}
+
+static int run_io() {
+  // round trips (reference io.cpp:10-42 format)
+  const SdpInstance s = sdp(40, {7, 3, 1}, {5, -4, 3, 2, 1, 0, 9}, OpKind::modular_add);
+  McmInstance m;
+  m.dims = {30, 35, 15, 5, 10, 20, 25};
+  EXPECT(to_text(s) == "sdp 40 3 modular-add\n7 3 1\n5 -4 3 2 1 0 9\n");
+  EXPECT(to_text(m) == "mcm 6\n30 35 15 5 10 20 25\n");
+  std::istringstream one(to_text(s));
+  const ParsedInstance ps = read_instance(one);
+  EXPECT(ps.kind == InstanceKind::sdp && ps.sdp && *ps.sdp == s);
+  // batched loader: every instance in order
+  std::istringstream many(to_text(m) + to_text(s) + to_text(m));
+  const std::vector<ParsedInstance> all = read_instances(many);
+  EXPECT(all.size() == 3 && all[0].kind == InstanceKind::mcm && *all[0].mcm == m &&
+         all[1].kind == InstanceKind::sdp && *all[1].sdp == s && *all[2].mcm == m);
+  // errors as the reference raises them
+  EXPECT(throws_errc([] { std::istringstream in("dp 3\n"); read_instance(in); }, errc::invalid_params,
+                     "InvalidParams: "));
+  EXPECT(throws_errc([] { std::istringstream in("mcm 3\n1 2 3\n"); read_instance(in); },
+                     errc::invalid_params, "InvalidParams: "));
+  EXPECT(throws_errc([] { std::istringstream in("sdp 10 2 min\n2 2\n0 0\n"); read_instance(in); },
+                     errc::non_decreasing_offsets, "NonDecreasingOffsets: "));
+  EXPECT(throws_errc([] { std::istringstream in(""); read_instances(in); }, errc::invalid_params,
+                     "InvalidParams: "));
+  // parenthesisation: CLRS 15.2 example and random instances, cost == apex
+  std::int64_t best = 0;
+  const std::vector<std::int64_t> sp = host_split(m, &best);
+  const std::string paren = mcm_parenthesization(m, sp);
+  EXPECT(paren == "((A1(A2A3))((A4A5)A6))");
+  EXPECT(best == 15125);
+  unsigned long long x = 88172645463325252ull;
+  for (int t = 0; t < 50; ++t) {
+    McmInstance r;
+    const int n = 1 + (int)(x % 40);
+    for (int i = 0; i <= n; ++i) {
+      x ^= x << 13, x ^= x >> 7, x ^= x << 17;
+      r.dims.push_back(1 + (std::int64_t)(x % 100));
+    }
+    const std::vector<std::int64_t> rs = host_split(r, &best);
+    const std::string pr = mcm_parenthesization(r, rs);
+    size_t i = 0;
+    std::int64_t rows, cols;
+    EXPECT(paren_cost(pr, r.dims, i, rows, cols) == best && i == pr.size());
+  }
+  std::printf("%s\n", failures ? "FAILED" : "OK");
+  return failures ? 1 : 0;
+}
+
 int main(int argc, char** argv) {
   const std::string mode = argc > 1 ? argv[1] : "validate";
   try {
     if (mode == "validate") return run_validate();
     if (mode == "nogpu") return run_nogpu();
     if (mode == "solve") return run_solve();
+    if (mode == "io") return run_io();
   } catch (const std::exception& e) {
     std::printf("EXCEPTION %s\n", e.what());
     return 2;

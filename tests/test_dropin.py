@@ -65,3 +65,9 @@ def test_dropin_solvers_on_gpu(binary, gpu):
             else:
                 want = next(c for c in GOLDEN["mcm"] if c.get("gen", [0])[0] == n)
             assert f[2] == want["digest"] and f[3] == want["split_digest"], line
+
+
+def test_dropin_instance_io_and_parenthesization(binary):
+    # reference io.cpp formats, the batched loader, split-table parenthesisation
+    rc, out = _run(binary, "io")
+    assert rc == 0 and out.strip().endswith("OK"), out

@@ -141,3 +141,51 @@ def test_product_never_imports_oracle():
                 for pat in ("import oracle", "from oracle", "pyoracle", "pipedp_oracle", "libpipedp_ref",
                             "oracle/_ref", "oracle/_build"):
                     assert pat not in text, (os.path.join(dirpath, f), pat)
+
+
+def test_instance_text_io_round_trip_and_batch(pd):
+    from paper_2008_01938_b200 import io
+    s = pd.SdpInstance(40, [7, 3, 1], [5, -4, 3, 2, 1, 0, 9], "modular-add")
+    m = pd.McmInstance([30, 35, 15, 5, 10, 20, 25])
+    assert io.to_text(s) == "sdp 40 3 modular-add\n7 3 1\n5 -4 3 2 1 0 9\n"
+    assert io.to_text(m) == "mcm 6\n30 35 15 5 10 20 25\n"
+    back = io.read_instances(io.to_text(m) + io.to_text(s) + io.to_text(m))
+    assert [type(x).__name__ for x in back] == ["McmInstance", "SdpInstance", "McmInstance"]
+    assert list(back[1].offsets) == [7, 3, 1] and list(back[1].init) == [5, -4, 3, 2, 1, 0, 9]
+    assert back[1].op == "modular-add" and list(back[0].dims) == list(m.dims)
+    for bad, code in [("dp 3\n", 11), ("mcm 3\n1 2 3\n", 11), ("sdp 10 2 min\n2 2\n0 0\n", 1), ("", 11)]:
+        with pytest.raises(pd.Error) as e:
+            io.read_instances(bad)
+        assert e.value.code == code
+
+
+def test_parenthesization_from_oracle_split(pd, oracle):
+    from paper_2008_01938_b200 import io
+    dims = [30, 35, 15, 5, 10, 20, 25]  # CLRS 15.2: cost 15125
+    cells, _, split = oracle.mcm_solve(dims)
+    assert io.mcm_parenthesization(dims, split) == "((A1(A2A3))((A4A5)A6))"
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        n = int(rng.integers(1, 60))
+        d = rng.integers(1, 100, n + 1).tolist()
+        cells, _, split = oracle.mcm_solve(d)
+        s = io.mcm_parenthesization(d, split)
+        # evaluate the product order's cost; it must equal the apex cell
+        stack = []
+        i = 0
+        while i < len(s):
+            if s[i] == "A":
+                j = i + 1
+                while j < len(s) and s[j].isdigit():
+                    j += 1
+                a = int(s[i + 1:j])
+                stack.append((d[a - 1], d[a], 0))
+                i = j
+            elif s[i] == ")":
+                r2, c2, x2 = stack.pop()
+                r1, c1, x1 = stack.pop()
+                stack.append((r1, c2, x1 + x2 + r1 * c1 * c2))
+                i += 1
+            else:
+                i += 1
+        assert stack[0][2] == (int(cells[-1]) if n > 1 else 0)
