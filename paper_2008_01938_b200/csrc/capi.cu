@@ -1206,7 +1206,9 @@ int32_t pipedp_sdp_plan_execute(pipedp_sdp_plan_t P, const int64_t* d_init, int6
 static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* W,
                                    const int64_t* d_init, int64_t* d_cells, int64_t* cells_out) {
   const size_t bytes = sizeof(int64_t) * P->batch * P->n;
-  if (!(P->d.remote && P->batch == 1 && P->d.method == PIPEDP_SDP_PIPELINE) || bytes < (64u << 20) ||
+  // (chunked plans never run the remote pipeline: no progress counters)
+  if (!(P->d.remote && !P->d.chunked && P->batch == 1 && P->d.method == PIPEDP_SDP_PIPELINE) ||
+      bytes < (64u << 20) ||
       env_int("PIPEDP_STREAM_D2H", 1) == 0) {
     TRY(sdp_execute(P, d_init, d_cells, W->stream, nullptr));
     if (bytes >= (16u << 20)) pipedp_host::parallel_prefault(cells_out, bytes);  // overlaps the kernel

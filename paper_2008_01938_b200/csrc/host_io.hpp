@@ -286,13 +286,18 @@ struct Workspace {
       return e == cudaSuccess ? cudaEventRecord(ev[c & 1], stream) : e;
     };
     if (nchunks == 0) return cudaStreamSynchronize(stream);
+    static const bool trace = getenv("PIPEDP_TRACE_D2H") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
     cudaError_t e = issue(0);
     for (size_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
       if (c + 1 < nchunks) e = issue(c + 1);  // overlaps the host copy of chunk c
       if (e == cudaSuccess) e = cudaEventSynchronize(ev[c & 1]);
       if (e != cudaSuccess) break;
+      const double tw = trace ? ms() : 0;
       const size_t off = c * piece, len = std::min(piece, bytes - off);
       parallel_memcpy(static_cast<char*>(dst) + off, pinned[c & 1], len);
+      if (trace) fprintf(stderr, "d2h piece %zu: ready at %.2f ms, host copy %.2f ms\n", c, tw, ms() - tw);
     }
     return e;
   }
