@@ -288,3 +288,11 @@ def test_chunked_equals_pipeline(gpu, monkeypatch):
     monkeypatch.setenv("PIPEDP_SDP_CHUNKED", "0")
     b = gpu.solve_sequential(inst).cells
     assert np.array_equal(a, b)
+
+
+def test_chunked_large_table_host_copy(gpu, oracle):
+    # >= 64 MiB output through the host-buffer entry point of a chunked plan
+    # (whose copy-out must not take the pipeline's progress-polling path)
+    n = 9_000_000 + 17
+    offs, init = oracle.generate_sdp(n, 20, 8, False, 64)
+    _check(gpu, oracle, offs, init, n, "max")
