@@ -100,8 +100,8 @@ class CopyPool {
 };
 
 inline void parallel_memcpy(void* dst, const void* src, size_t bytes) {
-  constexpr size_t kPiece = 4u << 20;
-  const int pieces = (int)std::min<size_t>((bytes + kPiece - 1) / kPiece, (size_t)CopyPool::get().size() * 2);
+  constexpr size_t kPiece = 1u << 20;  // >= 1 MiB per thread; every pool thread busy from 16 MiB on
+  const int pieces = (int)std::min<size_t>((bytes + kPiece - 1) / kPiece, (size_t)CopyPool::get().size());
   if (pieces <= 1) {
     std::memcpy(dst, src, bytes);
     return;
