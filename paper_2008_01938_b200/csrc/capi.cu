@@ -649,6 +649,30 @@ const char* sdp_kernel_name(const SdpDispatch& d) {
 
 constexpr size_t kRemoteBytes = kRemSlots * 32 * sizeof(int64_t) + kRemSlots * sizeof(int) + 64;
 
+// int64 -> int32 for a table whose values are proven to fit (the host widens
+// it back while copying out: half the device -> host bytes).
+__global__ void narrow_i64_i32(const int64_t* __restrict__ src, int32_t* __restrict__ dst, int64_t count) {
+  const int64_t pairs = count / 2;
+  const int4* s2 = reinterpret_cast<const int4*>(src);
+  int2* d2 = reinterpret_cast<int2*>(dst);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < pairs; i += (int64_t)gridDim.x * blockDim.x) {
+    const int4 v = s2[i];  // two int64: (x, y) and (z, w) little-endian halves
+    d2[i] = make_int2(v.x, v.z);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (count & 1)) dst[count - 1] = (int32_t)src[count - 1];
+}
+
+// Copy an int64 device table out through an int32 staging copy (W->buffer slot).
+static int32_t d2h_narrowed(pipedp_host::Workspace* W, int slot, int64_t* host, const int64_t* dev, int64_t count) {
+  void* tmp = nullptr;
+  CK(W->buffer(slot, sizeof(int32_t) * (size_t)count + 16, &tmp));
+  narrow_i64_i32<<<(unsigned)std::min<int64_t>(4 * 148, (count / 2 + 255) / 256 + 1), 256, 0, W->stream>>>(
+      dev, static_cast<int32_t*>(tmp), count);
+  CK(cudaGetLastError());
+  CK(W->d2h_widen(host, static_cast<const int32_t*>(tmp), (size_t)count));
+  return PIPEDP_OK;
+}
+
 struct pipedp_sdp_plan {
   int device;
   int64_t batch, n, k, a1;
@@ -1212,6 +1236,12 @@ static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* 
       env_int("PIPEDP_STREAM_D2H", 1) == 0) {
     TRY(sdp_execute(P, d_init, d_cells, W->stream, nullptr));
     if (bytes >= (16u << 20)) pipedp_host::parallel_prefault(cells_out, bytes);  // overlaps the kernel
+    // 32-bit value class (min/max of int32 presets, normalised mod-add): every
+    // table value fits int32 -- copy out half the bytes
+    const int bits = P->d.chunked ? P->dc.bits : P->d.bits;
+    if (bits == 32 && P->d.method == PIPEDP_SDP_PIPELINE && bytes >= (16u << 20) &&
+        env_int("PIPEDP_D2H_NARROW", 1) != 0)
+      return d2h_narrowed(W, 4, cells_out, d_cells, P->batch * P->n);
     CK(W->d2h(cells_out, d_cells, bytes));
     return PIPEDP_OK;
   }
@@ -1555,7 +1585,15 @@ static int32_t mcm_solve_host(int64_t batch, int64_t n, const int64_t* dims, int
   const int32_t rc = pipedp_mcm_plan_execute(P, (int64_t*)d_cells, (int64_t*)d_split, W->stream);
   if (touch.joinable()) touch.join();
   TRY(rc);
-  CK(W->d2h(cells_out, d_cells, sizeof(int64_t) * size));
+  // 32-bit run without the overflow flag: every cell < 2^30; split indices
+  // always fit int32 -- copy out half the bytes
+  const bool narrow = sizeof(int64_t) * size >= (16u << 20) && env_int("PIPEDP_D2H_NARROW", 1) != 0;
+  if (narrow && P->last_bits == 32) TRY(d2h_narrowed(W, 4, cells_out, (const int64_t*)d_cells, size));
+  else CK(W->d2h(cells_out, d_cells, sizeof(int64_t) * size));
+  if (split_out && narrow) {
+    TRY(d2h_narrowed(W, 5, split_out, (const int64_t*)d_split, size));
+    split_out = nullptr;  // done
+  }
   if (split_out) CK(W->d2h(split_out, d_split, sizeof(int64_t) * size));
   return PIPEDP_OK;
 }

@@ -126,6 +126,22 @@ inline void parallel_prefault(void* dst, size_t bytes) {
   });
 }
 
+// dst[i] = src[i] widened, split over the pool (the host half of a narrowed
+// device -> host copy).
+inline void parallel_widen(int64_t* dst, const int32_t* src, size_t count) {
+  constexpr size_t kSlice = 256u << 10;  // values per slice (>= 1 MiB of int32)
+  const int pieces = (int)std::min<size_t>((count + kSlice - 1) / kSlice, (size_t)CopyPool::get().size());
+  if (pieces <= 1) {
+    for (size_t i = 0; i < count; ++i) dst[i] = src[i];
+    return;
+  }
+  const size_t per = (count + pieces - 1) / pieces;
+  CopyPool::get().parallel_for(pieces, [&](int i) {
+    const size_t lo = (size_t)i * per, hi = std::min(count, lo + per);
+    for (size_t j = lo; j < hi; ++j) dst[j] = src[j];
+  });
+}
+
 // Per-thread, per-device transfer workspace.
 struct Workspace {
   static constexpr size_t kChunk = 64u << 20;
@@ -137,7 +153,7 @@ struct Workspace {
     void* p = nullptr;
     size_t cap = 0;
   };
-  Buf bufs[4];
+  Buf bufs[6];
 
   cudaError_t init(int dev) {
     device = dev;
@@ -258,6 +274,28 @@ struct Workspace {
     if (e == cudaSuccess && !armed) e = cudaEventCreateWithFlags(&armed, cudaEventDisableTiming);
     if (e == cudaSuccess && !done) e = cudaEventCreateWithFlags(&done, cudaEventDisableTiming);
     if (e == cudaSuccess && !side) e = cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking);
+    return e;
+  }
+
+  // int64 host table from an int32 device copy (values proven to fit int32):
+  // half the PCIe bytes, widened on the host while the next piece is in flight.
+  cudaError_t d2h_widen(int64_t* dst, const int32_t* src, size_t count) {
+    const size_t per = kChunk / sizeof(int32_t);
+    const size_t nchunks = (count + per - 1) / per;
+    auto issue = [&](size_t c) {
+      const size_t off = c * per, len = std::min(per, count - off);
+      cudaError_t e = cudaMemcpyAsync(pinned[c & 1], src + off, len * sizeof(int32_t), cudaMemcpyDeviceToHost, stream);
+      return e == cudaSuccess ? cudaEventRecord(ev[c & 1], stream) : e;
+    };
+    if (nchunks == 0) return cudaStreamSynchronize(stream);
+    cudaError_t e = issue(0);
+    for (size_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
+      if (c + 1 < nchunks) e = issue(c + 1);
+      if (e == cudaSuccess) e = cudaEventSynchronize(ev[c & 1]);
+      if (e != cudaSuccess) break;
+      const size_t off = c * per, len = std::min(per, count - off);
+      parallel_widen(dst + off, static_cast<const int32_t*>(pinned[c & 1]), len);
+    }
     return e;
   }
 
