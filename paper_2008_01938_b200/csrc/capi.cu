@@ -663,13 +663,15 @@ __global__ void narrow_i64_i32(const int64_t* __restrict__ src, int32_t* __restr
 }
 
 // Copy an int64 device table out through an int32 staging copy (W->buffer slot).
-static int32_t d2h_narrowed(pipedp_host::Workspace* W, int slot, int64_t* host, const int64_t* dev, int64_t count) {
+static int32_t d2h_narrowed(pipedp_host::Workspace* W, int slot, int64_t* host, const int64_t* dev, int64_t count,
+                            cudaStream_t st = nullptr) {
+  if (!st) st = W->stream;
   void* tmp = nullptr;
   CK(W->buffer(slot, sizeof(int32_t) * (size_t)count + 16, &tmp));
-  narrow_i64_i32<<<(unsigned)std::min<int64_t>(4 * 148, (count / 2 + 255) / 256 + 1), 256, 0, W->stream>>>(
+  narrow_i64_i32<<<(unsigned)std::min<int64_t>(4 * 148, (count / 2 + 255) / 256 + 1), 256, 0, st>>>(
       dev, static_cast<int32_t*>(tmp), count);
   CK(cudaGetLastError());
-  CK(W->d2h_widen(host, static_cast<const int32_t*>(tmp), (size_t)count));
+  CK(W->d2h_widen(host, static_cast<const int32_t*>(tmp), (size_t)count, st));
   return PIPEDP_OK;
 }
 
@@ -1117,7 +1119,8 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
 // entry states by Q (.) state, then all chunks as one batch.
 extern "C++" {
 template <int OP>
-static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64_t* d_cells, cudaStream_t st) {
+static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64_t* d_cells, cudaStream_t st,
+                               int64_t split_at = 0, cudaEvent_t split_event = nullptr) {
   const int32_t W = P->W, a1 = (int32_t)P->a1;
   const size_t mat = (size_t)64 * W * W;
   unsigned long long *X = P->d_bm, *XT = X + mat, *Z = XT + mat, *ZT = Z + mat;
@@ -1178,15 +1181,26 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
                                                                          P->d_cinit + g * a1);
     CK(cudaGetLastError());
   }
-  TRY(launch_sdp(P->dc, P->G, P->d_offs_rep, P->d_cinit, P->d_pad, SdpRemote{}, st));
-  // chunk tables -> the instance's table
   CK(cudaMemcpyAsync(d_cells, d_init, sizeof(int64_t) * a1, cudaMemcpyDeviceToDevice, st));
-  if (P->G > 1)
-    CK(cudaMemcpy2DAsync(d_cells + a1, sizeof(int64_t) * P->Lc, P->d_pad + a1, sizeof(int64_t) * P->n_i,
-                         sizeof(int64_t) * P->Lc, (size_t)(P->G - 1), cudaMemcpyDeviceToDevice, st));
-  const int64_t last = P->n - a1 - (P->G - 1) * P->Lc;
-  CK(cudaMemcpyAsync(d_cells + a1 + (P->G - 1) * P->Lc, P->d_pad + (P->G - 1) * P->n_i + a1,
-                     sizeof(int64_t) * last, cudaMemcpyDeviceToDevice, st));
+  // chunks [0, gs) then [gs, G), each gathered into the instance's table; an
+  // event after the first range lets the host copy it out while the second runs
+  const int64_t gs = split_at > 0 && split_at < P->G ? split_at : P->G;
+  for (int64_t g0 = 0; g0 < P->G; g0 = gs == P->G ? P->G : (g0 == 0 ? gs : P->G)) {
+    const int64_t g1 = g0 == 0 ? gs : P->G;
+    TRY(launch_sdp(P->dc, g1 - g0, P->d_offs_rep + g0 * P->k, P->d_cinit + g0 * a1, P->d_pad + g0 * P->n_i,
+                   SdpRemote{}, st));
+    const int64_t full = std::min(g1, P->G - 1) - g0;  // whole chunks in the range
+    if (full > 0)
+      CK(cudaMemcpy2DAsync(d_cells + a1 + g0 * P->Lc, sizeof(int64_t) * P->Lc, P->d_pad + g0 * P->n_i + a1,
+                           sizeof(int64_t) * P->n_i, sizeof(int64_t) * P->Lc, (size_t)full,
+                           cudaMemcpyDeviceToDevice, st));
+    if (g1 == P->G) {  // the ragged last chunk
+      const int64_t last = P->n - a1 - (P->G - 1) * P->Lc;
+      CK(cudaMemcpyAsync(d_cells + a1 + (P->G - 1) * P->Lc, P->d_pad + (P->G - 1) * P->n_i + a1,
+                         sizeof(int64_t) * last, cudaMemcpyDeviceToDevice, st));
+    }
+    if (g0 == 0 && split_event) CK(cudaEventRecord(split_event, st));
+  }
   return PIPEDP_OK;
 }
 }  // extern "C++"
@@ -1234,14 +1248,31 @@ static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* 
   if (!(P->d.remote && !P->d.chunked && P->batch == 1 && P->d.method == PIPEDP_SDP_PIPELINE) ||
       bytes < (64u << 20) ||
       env_int("PIPEDP_STREAM_D2H", 1) == 0) {
+    const int bits = P->d.chunked ? P->dc.bits : P->d.bits;
+    const bool narrow = bits == 32 && P->d.method == PIPEDP_SDP_PIPELINE && bytes >= (16u << 20) &&
+                        env_int("PIPEDP_D2H_NARROW", 1) != 0;
+    if (P->d.chunked && narrow && P->G > sm_count() && env_int("PIPEDP_CHUNK_OVERLAP", 0) != 0) {
+      // chunks in two launches (one per SM, then the rest): the first range's
+      // cells leave the device while the second range computes.  Off by
+      // default (PIPEDP_CHUNK_OVERLAP=1): on C2 the split launch costs more
+      // than the overlap saves (e2e 13.6 vs 12.2 ms measured)
+      CK(W->streaming_init());
+      CK(cudaSetDevice(P->device));
+      const int64_t gs = sm_count();
+      TRY(P->d.op == PIPEDP_OP_MAX ? sdp_chunked_run<kMax>(P, d_init, d_cells, W->stream, gs, W->armed)
+                                   : sdp_chunked_run<kMin>(P, d_init, d_cells, W->stream, gs, W->armed));
+      pipedp_host::parallel_prefault(cells_out, bytes);  // overlaps the kernels
+      const int64_t cut = P->a1 + gs * P->Lc;             // cells [0, cut) final at `armed`
+      CK(cudaStreamWaitEvent(W->side, W->armed, 0));
+      TRY(d2h_narrowed(W, 4, cells_out, d_cells, cut, W->side));
+      TRY(d2h_narrowed(W, 5, cells_out + cut, d_cells + cut, P->n - cut, W->stream));
+      return PIPEDP_OK;
+    }
     TRY(sdp_execute(P, d_init, d_cells, W->stream, nullptr));
     if (bytes >= (16u << 20)) pipedp_host::parallel_prefault(cells_out, bytes);  // overlaps the kernel
     // 32-bit value class (min/max of int32 presets, normalised mod-add): every
     // table value fits int32 -- copy out half the bytes
-    const int bits = P->d.chunked ? P->dc.bits : P->d.bits;
-    if (bits == 32 && P->d.method == PIPEDP_SDP_PIPELINE && bytes >= (16u << 20) &&
-        env_int("PIPEDP_D2H_NARROW", 1) != 0)
-      return d2h_narrowed(W, 4, cells_out, d_cells, P->batch * P->n);
+    if (narrow) return d2h_narrowed(W, 4, cells_out, d_cells, P->batch * P->n);
     CK(W->d2h(cells_out, d_cells, bytes));
     return PIPEDP_OK;
   }

@@ -279,15 +279,16 @@ struct Workspace {
 
   // int64 host table from an int32 device copy (values proven to fit int32):
   // half the PCIe bytes, widened on the host while the next piece is in flight.
-  cudaError_t d2h_widen(int64_t* dst, const int32_t* src, size_t count) {
+  cudaError_t d2h_widen(int64_t* dst, const int32_t* src, size_t count, cudaStream_t st = nullptr) {
+    if (!st) st = stream;
     const size_t per = kChunk / sizeof(int32_t);
     const size_t nchunks = (count + per - 1) / per;
     auto issue = [&](size_t c) {
       const size_t off = c * per, len = std::min(per, count - off);
-      cudaError_t e = cudaMemcpyAsync(pinned[c & 1], src + off, len * sizeof(int32_t), cudaMemcpyDeviceToHost, stream);
-      return e == cudaSuccess ? cudaEventRecord(ev[c & 1], stream) : e;
+      cudaError_t e = cudaMemcpyAsync(pinned[c & 1], src + off, len * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+      return e == cudaSuccess ? cudaEventRecord(ev[c & 1], st) : e;
     };
-    if (nchunks == 0) return cudaStreamSynchronize(stream);
+    if (nchunks == 0) return cudaStreamSynchronize(st);
     cudaError_t e = issue(0);
     for (size_t c = 0; c < nchunks && e == cudaSuccess; ++c) {
       if (c + 1 < nchunks) e = issue(c + 1);

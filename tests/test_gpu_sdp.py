@@ -296,3 +296,13 @@ def test_chunked_large_table_host_copy(gpu, oracle):
     n = 9_000_000 + 17
     offs, init = oracle.generate_sdp(n, 20, 8, False, 64)
     _check(gpu, oracle, offs, init, n, "max")
+
+
+@pytest.mark.parametrize("op", ["min", "max"])
+def test_chunked_overlapped_copy_out(gpu, oracle, op, monkeypatch):
+    # G = 200 > SM count: chunks run in two launches and the first range is
+    # copied out (narrowed to int32, widened on the host) while the second runs
+    monkeypatch.setenv("PIPEDP_CHUNK_OVERLAP", "1")
+    n = 200 * 16384 + 512 + 99
+    offs, init = oracle.generate_sdp(n, 50, 12, False, 512)
+    _check(gpu, oracle, offs, init, n, op)
