@@ -445,10 +445,9 @@ def main():
         if kname.startswith("sdp_chunked"):
             # chunked: the longest dependent chains are one chunk's cells and
             # the chunk entry-state chain (G matrix-vector steps)
-            L = 1 << max(12, (8 * i.a1 - 1).bit_length())
-            while (i.n - i.a1) // L >= 256:
-                L *= 2
-            G = -(-(i.n - i.a1) // L)
+            import re
+            m = re.search(r"L=(\d+),G=(\d+)", kname)
+            L, G = (int(m.group(1)), int(m.group(2))) if m else (i.n - i.a1, 1)
             steps = L + G
             definition = ("sdp_chunked: one chunk (L cells) + G entry-state steps, "
                           "each x latency of one dependent (x)")

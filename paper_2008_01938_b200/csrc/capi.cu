@@ -206,7 +206,7 @@ struct SdpDispatch {
   bool serial;  // tiny offset sets: one-thread chain (sdp_serial_thread)
   bool jump;    // a_1 <= 8: jump-ahead segments (sdp_jump)
   bool chunked; // one large min/max instance as a batch of chunks (sdp_chunked.cuh)
-  int32_t chunk_log2;  // chunk length L = 1 << chunk_log2
+  int64_t chunk_len;  // chunk length L (a multiple of 32 with few set bits: square-and-multiply)
   int method;   // 0 pipeline, 1 the paper's tournament (prefix), 2 the paper's naive method
   SdpV2Shape s2;
 };
@@ -433,18 +433,22 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
               env_int("PIPEDP_SDP_JUMP", 1) != 0;
   }
 
-  {  // chunks: cells [a1, n) in G ~ 256 chunks of L = 2^m >= max(4096, 8 a1)
+  {  // chunks: cells [a1, n) in G <= 2 x SMs chunks (two chunk CTAs share an
+     // SM) of L cells, L >= max(4096, 8 a1), L / 32 with <= 3 set bits (each
+     // set bit beyond the first costs one matrix product)
     d->chunked = false;
     if (batch == 1 && (op == PIPEDP_OP_MIN || op == PIPEDP_OP_MAX) && a1 >= 64 && a1 <= 8192 &&
         env_int("PIPEDP_SDP_CHUNKED", 1) != 0) {
-      int m = 12;
-      while ((1ll << m) < 8 * a1) ++m;
-      const int target = std::max(1, env_int("PIPEDP_SDP_CHUNKS", 256));
-      while (((n - a1) >> m) >= target) ++m;
-      const int64_t G = (n - a1 + (1ll << m) - 1) >> m;
+      const int64_t slots = std::max(1, env_int("PIPEDP_SDP_CHUNKS", 2 * sm_count()));
+      const int64_t lmin = std::max<int64_t>(4096, 8 * a1);
+      int64_t target = std::max<int64_t>(lmin, (n - a1 + slots - 1) / slots);
+      int64_t L = (target + 31) / 32;  // in units of 32 cells
+      while (__builtin_popcountll((unsigned long long)L) > 3) ++L;
+      L *= 32;
+      const int64_t G = (n - a1 + L - 1) / L;
       if (G >= 16) {
         d->chunked = true;
-        d->chunk_log2 = m;
+        d->chunk_len = L;
       }
     }
   }
@@ -1069,7 +1073,7 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
     if (e == cudaSuccess) e = cudaMemcpy(P->d_obg, obg.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice);
   }
   if (e == cudaSuccess && d.chunked) {
-    P->Lc = 1ll << d.chunk_log2;
+    P->Lc = d.chunk_len;
     P->G = (n - a1 + P->Lc - 1) / P->Lc;
     P->n_i = a1 + P->Lc;
     // 64-bit words per row: rows padded to 2048 bits (whole 128-wide product
@@ -1098,7 +1102,7 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
       dc.threads = 32 * sdp_warps_for_roles(dc.shape.mid_warps + dc.shape.far_warps + 1);
     }
     const size_t mat = (size_t)64 * P->W * P->W;
-    e = cudaMalloc(&P->d_bm, sizeof(unsigned long long) * 4 * mat);
+    e = cudaMalloc(&P->d_bm, sizeof(unsigned long long) * 6 * mat);  // X, XT, Z, ZT, R, RT
     if (e == cudaSuccess) e = cudaMalloc(&P->d_q, sizeof(unsigned long long) * mat);
     if (e == cudaSuccess) e = cudaMalloc(&P->d_E, sizeof(int64_t) * 2 * 64 * P->W + 512);  // + flags, barrier
     if (e == cudaSuccess) e = cudaMalloc(&P->d_cinit, sizeof(int64_t) * P->G * a1);
@@ -1131,15 +1135,38 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
   CK(cudaFuncSetAttribute(bm_mul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const dim3 grid((unsigned)W, (unsigned)(W / 2));  // 128 x 64 output tiles
   auto x32 = [](const unsigned long long* p) { return reinterpret_cast<const uint32_t*>(p); };
-  int* flags = reinterpret_cast<int*>(P->d_E + 2 * 64 * W);  // [chunk_log2] changed flags
+  int* flags = reinterpret_cast<int*>(P->d_E + 2 * 64 * W);  // per-squaring changed flags
   CK(cudaMemsetAsync(flags, 0, sizeof(int) * 64, st));
-  for (int i = 0; i < P->d.chunk_log2; ++i) {  // X <- X X (then its transpose)
+  unsigned long long *R = ZT + mat, *RT = R + mat;
+  auto square = [&](int i) {  // X <- X X (then its transpose); flags track idempotence
     bm_mul<<<grid, 256, smem, st>>>(x32(X), x32(XT), 2 * W, Z, i ? flags + i - 1 : nullptr, flags + i);
     bm_transpose<<<dim3((unsigned)W, (unsigned)W), 64, 0, st>>>(Z, W, ZT);
-    CK(cudaGetLastError());
     std::swap(X, Z);
     std::swap(XT, ZT);
+  };
+  // Q = M^Lc by square-and-multiply over the bits of Lc (R accumulates)
+  const int top = 63 - __builtin_clzll((unsigned long long)P->Lc);
+  int nsq = 0;
+  bool have_r = false;
+  for (int i = 0; i <= top; ++i) {
+    if ((P->Lc >> i) & 1) {
+      if (!have_r) {
+        CK(cudaMemcpyAsync(R, X, sizeof(unsigned long long) * 2 * mat, cudaMemcpyDeviceToDevice, st));  // R, RT
+        have_r = true;
+      } else {  // R <- R X (powers of M commute)
+        bm_mul<<<grid, 256, smem, st>>>(x32(R), x32(XT), 2 * W, Z, nullptr, nullptr);
+        bm_transpose<<<dim3((unsigned)W, (unsigned)W), 64, 0, st>>>(Z, W, ZT);
+        std::swap(R, Z);
+        std::swap(RT, ZT);
+      }
+    }
+    if (i < top) square(nsq++);
+    CK(cudaGetLastError());
   }
+  // from here X, XT hold Q
+  std::swap(X, R);
+  std::swap(XT, RT);
+  CK(cudaMemsetAsync(flags + nsq, 0xFF, sizeof(int), st));  // Q's own squarings start fresh ("changed")
   int64_t* E[2] = {P->d_E, P->d_E + 64 * W};
   CK(cudaFuncSetAttribute(bm_matvec<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(sizeof(int64_t) * 64 * W)));
@@ -1152,7 +1179,7 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
     if (B > 1) {
       CK(cudaMemcpyAsync(P->d_q, X, sizeof(unsigned long long) * mat, cudaMemcpyDeviceToDevice, st));
       Q = P->d_q;
-      for (int b = 1, i = P->d.chunk_log2; b < B; b *= 2, ++i) {
+      for (int b = 1, i = nsq + 1; b < B; b *= 2, ++i) {
         bm_mul<<<grid, 256, smem, st>>>(x32(X), x32(XT), 2 * W, Z, flags + i - 1, flags + i);
         bm_transpose<<<dim3((unsigned)W, (unsigned)W), 64, 0, st>>>(Z, W, ZT);
         CK(cudaGetLastError());
@@ -1301,13 +1328,21 @@ int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, in
                                  int32_t* launches) {
   if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
   if (name && cap) {
-    if (P->d.chunked) snprintf(name, cap, "sdp_chunked[%s]", sdp_kernel_name(P->dc));
+    if (P->d.chunked)
+      snprintf(name, cap, "sdp_chunked[L=%lld,G=%lld,%s]", (long long)P->Lc, (long long)P->G, sdp_kernel_name(P->dc));
     else snprintf(name, cap, "%s", sdp_kernel_name(P->d));
   }
   if (bits) *bits = P->d.chunked ? P->dc.bits : P->d.bits;
   // kernels (remote mode adds a memset + a prefix copy); chunked: build,
   // product + transpose per squaring, state 0, the persistent chain, the batch
-  if (launches) *launches = P->d.chunked ? (int32_t)(1 + 2 * P->d.chunk_log2 + 1 + 1 + 1) : 1;
+  if (launches) {
+    int32_t nl = 1;
+    if (P->d.chunked) {  // build, 2 per squaring / multiply, state 0, 2 x 4 for Q^16, chain, batch
+      const int top = 63 - __builtin_clzll((unsigned long long)P->Lc);
+      nl = 1 + 2 * (top + __builtin_popcountll((unsigned long long)P->Lc) - 1) + 1 + (P->G >= 64 ? 8 : 0) + 1 + 1;
+    }
+    *launches = nl;
+  }
   return PIPEDP_OK;
 }
 
