@@ -1138,11 +1138,24 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
   int* flags = reinterpret_cast<int*>(P->d_E + 2 * 64 * W);  // per-squaring changed flags
   CK(cudaMemsetAsync(flags, 0, sizeof(int) * 64, st));
   unsigned long long *R = ZT + mat, *RT = R + mat;
+  // out = A B for the power M^t_new: rows >= t_new (t_new < a1) are shifts,
+  // written directly; only the rows above them are multiplied
+  auto product = [&](const unsigned long long* A, const unsigned long long* BT, unsigned long long* out,
+                     int64_t t_new, const int* prev, int* chg) {
+    const int64_t rows = 64ll * W;
+    const int64_t lim = t_new < a1 ? std::min<int64_t>(rows, (t_new + kBmR - 1) / kBmR * kBmR) : rows;
+    bm_mul<<<dim3((unsigned)W, (unsigned)(lim / kBmR)), 256, smem, st>>>(x32(A), x32(BT), 2 * W, out, prev, chg);
+    if (lim < rows)
+      bm_shift_rows<<<(unsigned)std::min<int64_t>(1024, ((rows - lim) * W + 255) / 256), 256, 0, st>>>(
+          out, W, t_new, lim, a1, chg);
+  };
+  int64_t ex = 1, er = 0;  // exponents of X and R
   auto square = [&](int i) {  // X <- X X (then its transpose); flags track idempotence
-    bm_mul<<<grid, 256, smem, st>>>(x32(X), x32(XT), 2 * W, Z, i ? flags + i - 1 : nullptr, flags + i);
+    product(X, XT, Z, 2 * ex, i ? flags + i - 1 : nullptr, flags + i);
     bm_transpose<<<dim3((unsigned)W, (unsigned)W), 64, 0, st>>>(Z, W, ZT);
     std::swap(X, Z);
     std::swap(XT, ZT);
+    ex *= 2;
   };
   // Q = M^Lc by square-and-multiply over the bits of Lc (R accumulates)
   const int top = 63 - __builtin_clzll((unsigned long long)P->Lc);
@@ -1153,11 +1166,13 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
       if (!have_r) {
         CK(cudaMemcpyAsync(R, X, sizeof(unsigned long long) * 2 * mat, cudaMemcpyDeviceToDevice, st));  // R, RT
         have_r = true;
+        er = ex;
       } else {  // R <- R X (powers of M commute)
-        bm_mul<<<grid, 256, smem, st>>>(x32(R), x32(XT), 2 * W, Z, nullptr, nullptr);
+        product(R, XT, Z, er + ex, nullptr, nullptr);
         bm_transpose<<<dim3((unsigned)W, (unsigned)W), 64, 0, st>>>(Z, W, ZT);
         std::swap(R, Z);
         std::swap(RT, ZT);
+        er += ex;
       }
     }
     if (i < top) square(nsq++);
@@ -1180,7 +1195,7 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
       CK(cudaMemcpyAsync(P->d_q, X, sizeof(unsigned long long) * mat, cudaMemcpyDeviceToDevice, st));
       Q = P->d_q;
       for (int b = 1, i = nsq + 1; b < B; b *= 2, ++i) {
-        bm_mul<<<grid, 256, smem, st>>>(x32(X), x32(XT), 2 * W, Z, flags + i - 1, flags + i);
+        product(X, XT, Z, er * 2 * b, flags + i - 1, flags + i);
         bm_transpose<<<dim3((unsigned)W, (unsigned)W), 64, 0, st>>>(Z, W, ZT);
         CK(cudaGetLastError());
         std::swap(X, Z);

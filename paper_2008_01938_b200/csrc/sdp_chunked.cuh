@@ -123,6 +123,20 @@ __global__ void __launch_bounds__(256, 2) bm_mul(const uint32_t* __restrict__ X,
   }
 }
 
+// Rows [r0, 64 W) of M^t for t < a1 are pure shifts: row r (state position r
+// at time T + t) is state position r - t at time T.  Written directly instead
+// of multiplied; they differ from every other power's rows, so `changed` is set.
+__global__ void bm_shift_rows(unsigned long long* __restrict__ Z, int32_t W, int64_t t, int64_t r0, int32_t a1,
+                              int* changed) {
+  const int64_t rows = 64ll * W;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (rows - r0) * W;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = r0 + e / W, w = e % W, c = r - t;
+    Z[r * W + w] = (r < a1 && c >= 0 && c / 64 == w) ? 1ull << (c % 64) : 0ull;
+  }
+  if (changed && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(changed, 1);
+}
+
 // ZT = Z^T for bit-packed square matrices (W words per row): one 64 x 64 bit
 // block per CTA (64 threads), through shared memory.
 __global__ void __launch_bounds__(64) bm_transpose(const unsigned long long* __restrict__ Z, int32_t W,
