@@ -653,6 +653,10 @@ const char* sdp_kernel_name(const SdpDispatch& d) {
 
 constexpr size_t kRemoteBytes = kRemSlots * 32 * sizeof(int64_t) + kRemSlots * sizeof(int) + 64;
 
+// Host tables from this size on are pre-faulted while the kernels run and (for
+// the 32-bit value class) copied out narrowed.
+static const size_t kHostCopyBig = (size_t)std::max(1, env_int("PIPEDP_HOST_COPY_BIG_KB", 2048)) << 10;
+
 // int64 -> int32 for a table whose values are proven to fit (the host widens
 // it back while copying out: half the device -> host bytes).
 __global__ void narrow_i64_i32(const int64_t* __restrict__ src, int32_t* __restrict__ dst, int64_t count) {
@@ -1291,7 +1295,7 @@ static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* 
       bytes < (64u << 20) ||
       env_int("PIPEDP_STREAM_D2H", 1) == 0) {
     const int bits = P->d.chunked ? P->dc.bits : P->d.bits;
-    const bool narrow = bits == 32 && P->d.method == PIPEDP_SDP_PIPELINE && bytes >= (16u << 20) &&
+    const bool narrow = bits == 32 && P->d.method == PIPEDP_SDP_PIPELINE && bytes >= kHostCopyBig &&
                         env_int("PIPEDP_D2H_NARROW", 1) != 0;
     if (P->d.chunked && narrow && P->G > sm_count() && env_int("PIPEDP_CHUNK_OVERLAP", 0) != 0) {
       // chunks in two launches (one per SM, then the rest): the first range's
@@ -1311,7 +1315,7 @@ static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* 
       return PIPEDP_OK;
     }
     TRY(sdp_execute(P, d_init, d_cells, W->stream, nullptr));
-    if (bytes >= (16u << 20)) pipedp_host::parallel_prefault(cells_out, bytes);  // overlaps the kernel
+    if (bytes >= kHostCopyBig) pipedp_host::parallel_prefault(cells_out, bytes);  // overlaps the kernel
     // 32-bit value class (min/max of int32 presets, normalised mod-add): every
     // table value fits int32 -- copy out half the bytes
     if (narrow) return d2h_narrowed(W, 4, cells_out, d_cells, P->batch * P->n);
@@ -1658,7 +1662,7 @@ static int32_t mcm_solve_host(int64_t batch, int64_t n, const int64_t* dims, int
   // first-touch the host outputs while the kernels run (execute may wait on
   // the device for the overflow check)
   std::thread touch;
-  if (sizeof(int64_t) * size >= (16u << 20))
+  if (sizeof(int64_t) * size >= kHostCopyBig)
     touch = std::thread([&] {
       pipedp_host::parallel_prefault(cells_out, sizeof(int64_t) * size);
       if (split_out) pipedp_host::parallel_prefault(split_out, sizeof(int64_t) * size);
@@ -1668,7 +1672,7 @@ static int32_t mcm_solve_host(int64_t batch, int64_t n, const int64_t* dims, int
   TRY(rc);
   // 32-bit run without the overflow flag: every cell < 2^30; split indices
   // always fit int32 -- copy out half the bytes
-  const bool narrow = sizeof(int64_t) * size >= (16u << 20) && env_int("PIPEDP_D2H_NARROW", 1) != 0;
+  const bool narrow = sizeof(int64_t) * size >= kHostCopyBig && env_int("PIPEDP_D2H_NARROW", 1) != 0;
   if (narrow && P->last_bits == 32) TRY(d2h_narrowed(W, 4, cells_out, (const int64_t*)d_cells, size));
   else CK(W->d2h(cells_out, d_cells, sizeof(int64_t) * size));
   if (split_out && narrow) {
