@@ -698,6 +698,7 @@ struct pipedp_sdp_plan {
   int64_t* d_cinit = nullptr;          // [G][a1] chunk preset cells
   int64_t* d_offs_rep = nullptr;       // [G][k]
   int64_t* d_pad = nullptr;            // [G][n_i] chunk tables
+  int32_t* d_perm = nullptr;           // batch warp kernel: instance order (dominance-form ones first)
   int64_t* d_offsets;  // device copy of the offsets, int64 [batch*k]
   void* d_remote;      // multi-CTA workspace: partial slots | ready flags | published
   int32_t* d_obg;      // remote producers: offsets as HBM-table byte offsets
@@ -1076,6 +1077,21 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
     e = cudaMalloc(&P->d_obg, sizeof(int32_t) * k);
     if (e == cudaSuccess) e = cudaMemcpy(P->d_obg, obg.data(), sizeof(int32_t) * k, cudaMemcpyHostToDevice);
   }
+  if (e == cudaSuccess && d.warp_kernel && batch > 1 && (op == PIPEDP_OP_MIN || op == PIPEDP_OP_MAX)) {
+    // group the instances that take the batch kernel's dominance form (offset 1,
+    // a_1 <= 128) ahead of the others
+    std::vector<int32_t> perm;
+    perm.reserve((size_t)batch);
+    for (int pass = 0; pass < 2; ++pass)
+      for (int64_t b = 0; b < batch; ++b) {
+        bool has1 = false;
+        for (int64_t j = 0; j < k; ++j) has1 = has1 || h_offsets[b * k + j] == 1;
+        const bool dom = has1 && a1 <= 128 && k >= 2;
+        if (dom == (pass == 0)) perm.push_back((int32_t)b);
+      }
+    e = cudaMalloc(&P->d_perm, sizeof(int32_t) * batch);
+    if (e == cudaSuccess) e = cudaMemcpy(P->d_perm, perm.data(), sizeof(int32_t) * batch, cudaMemcpyHostToDevice);
+  }
   if (e == cudaSuccess && d.chunked) {
     P->Lc = d.chunk_len;
     P->G = (n - a1 + P->Lc - 1) / P->Lc;
@@ -1275,6 +1291,11 @@ static int32_t sdp_execute(pipedp_sdp_plan_t P, const int64_t* d_init, int64_t* 
                        (cudaStream_t)stream));
   }
   if (armed) CK(cudaEventRecord(armed, (cudaStream_t)stream));
+  if (P->d_perm) {
+    SdpDispatch dd = P->d;
+    dd.shape.perm = P->d_perm;
+    return launch_sdp(dd, P->batch, P->d_offsets, d_init, d_cells, rm, (cudaStream_t)stream);
+  }
   return launch_sdp(P->d, P->batch, P->d_offsets, d_init, d_cells, rm, (cudaStream_t)stream);
 }
 
@@ -1389,6 +1410,7 @@ int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t P) {
   cudaFree(P->d_obg);
   cudaFree(P->d_bm);
   cudaFree(P->d_q);
+  cudaFree(P->d_perm);
   cudaFree(P->d_E);
   cudaFree(P->d_cinit);
   cudaFree(P->d_offs_rep);

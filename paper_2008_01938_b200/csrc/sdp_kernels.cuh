@@ -60,6 +60,7 @@ struct SdpShape {
   int32_t writers;       // finisher writer warps publishing progress (published[0..writers))
   int32_t j_rem;         // number of offsets >= a_remote (the producers' share)
   int32_t rem_look;      // batches between a producer batch and the newest cell it reads
+  const int32_t* perm;   // batch warp kernel: warp -> instance order (nullable), set at launch
 };
 
 // Global workspace of the multi-CTA mode (zeroed before every launch).
@@ -849,7 +850,7 @@ __global__ void __launch_bounds__(1024, 1)
 // -- offsets >= 32 straight from its private mirrored ring, offsets < 32
 // through chain_fold.  SMALL: a_1 < 64 (the first operand is assigned inside chain_fold).
 template <int OP, typename T, bool SMALL, bool ASSOC>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 5)
     sdp_batch_warp(const SdpShape S, int64_t batch, const int64_t* __restrict__ g_offsets,
                    const int64_t* __restrict__ g_init, int64_t* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -862,8 +863,11 @@ __global__ void __launch_bounds__(256)
   int32_t* offs = reinterpret_cast<int32_t*>(reinterpret_cast<T*>(smem) + (size_t)wpb * 2 * R) +
                   (size_t)warp * 2 * kpad;
   int32_t* ob = offs + kpad;
-  const int64_t inst = (int64_t)blockIdx.x * wpb + warp;
-  if (inst >= batch) return;
+  const int64_t gw = (int64_t)blockIdx.x * wpb + warp;
+  if (gw >= batch) return;
+  // instances grouped by path (dominance-form ones first): a block's warps
+  // take the same path and finish together
+  const int64_t inst = S.perm ? S.perm[gw] : gw;
   const int64_t a1 = S.a1, n = S.n;
   const int64_t* io = g_offsets + inst * S.k;
   const int64_t* ii = g_init + inst * a1;
@@ -886,13 +890,37 @@ __global__ void __launch_bounds__(256)
   constexpr bool kLA = !SMALL && ASSOC && !(OP == kModAdd && sizeof(T) == 8);
   const LaMasks lm = la_masks(offs, S.k, lane);
   const IdemMasks im = idem_masks(offs, S.k, lane);
+  // Dominance form (as in the single-instance chain, sdp_v2.cuh): min/max
+  // with offset 1 and a_1 <= 128 -- every finished batch is the prefix-(x) of
+  // its b vector, so the offsets [l+33, 128) a batch takes from the three
+  // batches before it fold to x at one lane each (three shuffles); only
+  // offsets >= 128 (a_1 itself) are read from the ring.  From batch 4 on;
+  // the first batches take the general path.
+  const bool dom = kLA && IsIdem<OP>::value && im.scan && a1 <= 128 && S.k >= 2;
+  int src2 = -1, src3 = -1, src4 = -1, j128 = 0;
+  if (dom) {
+    for (int j = S.k - 1; j >= 0; --j) {  // ascending d
+      const int d = offs[j];
+      if (d >= 128) break;
+      if (src2 < 0 && d >= lane + 33 && d <= lane + 64) src2 = lane + 64 - d;
+      if (src3 < 0 && d >= lane + 65 && d <= lane + 96) src3 = lane + 96 - d;
+      if (src4 < 0 && d >= lane + 97 && d <= lane + 128) src4 = lane + 128 - d;
+    }
+    while (j128 < S.k && offs[j128] >= 128) ++j128;
+  }
+  const T idv = SemiId<OP, T>::value();
+  T xm1 = idv, xm2 = idv, xm3 = idv, pre_cur = idv;
   T nxt = T(0);
   const int64_t nb = (n - a1 + 31) / 32;
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t c = a1 + 32 * b + lane;
     const uint32_t pos = ((uint32_t)c & (R - 1)) + R;
     T acc;
-    if (kLA) {
+    if (dom && b >= 4) {
+      // offsets >= 128 from the ring, [l+33, 128) as pre_cur, [l+1, l+32] as nxt
+      acc = SemiOp<OP, T>::apply(fold_range<OP, T, ASSOC>(pre_cur, true, ring + pos, ob, 0, j128), nxt);
+      idem_closure<OP, T>(acc, nxt, im);
+    } else if (kLA) {
       acc = fold_range<OP, T, ASSOC>(T(0), false, ring + pos, ob, 0, jn);
       if (b == 0) {
         bool h = true;
@@ -913,6 +941,18 @@ __global__ void __launch_bounds__(256)
       acc = chain_fold<OP, T, true, ASSOC>(acc, ring, pos, cm);
     } else {
       acc = chain_fold<OP, T, false, ASSOC>(T(0), ring, pos, cm);
+    }
+    if (dom) {  // batch b+1's [l+33, 128) terms from x of batches b-1, b-2, b-3
+      if (b >= 3) {
+        const T v2 = shfl_idx(xm1, src2 < 0 ? 0 : src2);
+        const T v3 = shfl_idx(xm2, src3 < 0 ? 0 : src3);
+        const T v4 = shfl_idx(xm3, src4 < 0 ? 0 : src4);
+        pre_cur = SemiOp<OP, T>::apply(SemiOp<OP, T>::apply(src2 < 0 ? idv : v2, src3 < 0 ? idv : v3),
+                                       src4 < 0 ? idv : v4);
+      }
+      xm3 = xm2;
+      xm2 = xm1;
+      xm1 = acc;
     }
     if (c < n) {
       ring[pos - R] = acc;
