@@ -306,3 +306,17 @@ def test_chunked_overlapped_copy_out(gpu, oracle, op, monkeypatch):
     n = 200 * 16384 + 512 + 99
     offs, init = oracle.generate_sdp(n, 50, 12, False, 512)
     _check(gpu, oracle, offs, init, n, op)
+
+
+@pytest.mark.parametrize("op", ["min", "max"])
+def test_chunked_int64_values(gpu, oracle, op):
+    # presets beyond int32: 64-bit chunk kernels, entry states and a full-width copy-out
+    rng = np.random.default_rng(77)
+    n = 2_500_000
+    offs, _ = oracle.generate_sdp(n, 40, 9, False, 300)
+    init = rng.integers(-(2**62), 2**62, len(_))
+    plan = gpu.SdpPlan(1, n, len(offs), len(init), offs, init, op)
+    name, bits, _l = plan.describe()
+    plan.close()
+    assert name.startswith("sdp_chunked") and bits == 64
+    _check(gpu, oracle, offs, init, n, op)
