@@ -871,13 +871,16 @@ int mcm_smem_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split
   const size_t sq = mcm_square_bytes(n, bits / 8);
   if (sq <= kSmemBudget && env_int("PIPEDP_MCM_SQUARE", 1) != 0) {
     // row-major square table: incremental operand addresses (mcm_smem_square)
+    // two warps for n <= 96: the short diagonals keep them busy (C5a: 3.96 ->
+    // 3.19 ms against four warps); more CTAs fit an SM
+    const int thr = std::max(32, std::min(128, env_int("PIPEDP_MCM_SQ_THREADS", n <= 96 ? 64 : 128))) / 32 * 32;
     if (bits == 32) {
       CK(cudaFuncSetAttribute(mcm_smem_square<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq));
-      mcm_smem_square<uint32_t><<<(unsigned)P->batch, 128, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
+      mcm_smem_square<uint32_t><<<(unsigned)P->batch, thr, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
                                                                       split, P->d_overflow);
     } else {
       CK(cudaFuncSetAttribute(mcm_smem_square<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq));
-      mcm_smem_square<int64_t><<<(unsigned)P->batch, 128, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
+      mcm_smem_square<int64_t><<<(unsigned)P->batch, thr, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
                                                                      split, P->d_overflow);
     }
     CK(cudaGetLastError());
