@@ -415,7 +415,8 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
       s.ring_log2 = ceil_log2((uint64_t)R);
       s.ring_cover = (int32_t)a1;
       s.mid_warps = s.far_warps = 0;
-      d->wpb = (int)std::max<int64_t>(1, std::min<int64_t>(8, (96 * 1024) / per_warp));
+      d->wpb = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(1, std::min(8, env_int("PIPEDP_SDP_WPB", 8))),
+                                                           (96 * 1024) / per_warp));
       d->threads = 32 * d->wpb;
       d->smem = per_warp * d->wpb;
       return PIPEDP_OK;
