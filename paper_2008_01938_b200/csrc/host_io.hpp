@@ -281,7 +281,14 @@ struct Workspace {
   // half the PCIe bytes, widened on the host while the next piece is in flight.
   cudaError_t d2h_widen(int64_t* dst, const int32_t* src, size_t count, cudaStream_t st = nullptr) {
     if (!st) st = stream;
-    const size_t per = kChunk / sizeof(int32_t);
+    // pieces of PIPEDP_WIDEN_PIECE_MB (default 16) MiB of int32: the DMA of piece
+    // i+1 overlaps the widening of piece i (the host side is the slower leg)
+    static const size_t piece_bytes = [] {
+      const char* v = getenv("PIPEDP_WIDEN_PIECE_MB");
+      const size_t mb = v && *v ? (size_t)atoi(v) : 16;
+      return std::min(kChunk, std::max<size_t>(1, mb) << 20);
+    }();
+    const size_t per = piece_bytes / sizeof(int32_t);
     const size_t nchunks = (count + per - 1) / per;
     auto issue = [&](size_t c) {
       const size_t off = c * per, len = std::min(per, count - off);
