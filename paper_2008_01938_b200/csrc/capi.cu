@@ -779,6 +779,8 @@ struct pipedp_mcm_plan {
   int64_t total_chunks;
   int launches;
   int last_bits;
+  bool packed_ok;     // tiled far tasks may fold packed keys (max_dim^3 < 2^25)
+  bool packed_now;    // this execute's tiled launch uses them
   // tiled kernel
   int32_t* d_pp;                 // dims, zero padded to N*T + 2
   uint32_t* d_tiles;
@@ -827,7 +829,7 @@ int mcm_tiled_launch(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStr
   CK(cudaMemsetAsync(split, 0, sizeof(int64_t) * (n + 1), st));
   McmTiled S{n, (int32_t)N, P->ntasks, P->d_pp, P->d_tiles, P->d_keys, P->d_tile_flags,
              P->d_tile_flags + ntiles, P->d_tasks, P->d_next, cells, split, P->d_overflow,
-             env_int("PIPEDP_MCM_BLOCKED", 0) ? 1 : env_int("PIPEDP_MCM_NEAR", 2)};
+             env_int("PIPEDP_MCM_BLOCKED", 0) ? 1 : env_int("PIPEDP_MCM_NEAR", 2), P->packed_now ? 1 : 0};
   if (P->d.tile == 32) {
     CK(cudaFuncSetAttribute(t32::mcm_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)t32::kTiledSmemBytes));
@@ -912,6 +914,10 @@ int mcm_execute(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t
     return PIPEDP_OK;
   }
   int bits = P->d.bits;
+  // packed far keys pay on the 64-wide tiles (ALU-bound far tasks); the 32-wide
+  // ones are latency-bound (C3 unchanged), so they keep the plain fold
+  P->packed_now = P->packed_ok && P->d.kernel == PIPEDP_MCM_TILED && P->d.tile == 64 &&
+                  env_int("PIPEDP_MCM_PACKED", 1) != 0;
   for (;;) {
     CK(cudaMemsetAsync(P->d_overflow, 0, sizeof(int), st));
     if (P->d.kernel == PIPEDP_MCM_SMEM) TRY(mcm_smem_launch(P, bits, cells, split, st));
@@ -923,6 +929,10 @@ int mcm_execute(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t
     CK(cudaMemcpyAsync(P->h_overflow, P->d_overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     if (*P->h_overflow == 0) return PIPEDP_OK;
+    if (*P->h_overflow == 2 && P->packed_now) {  // a cell reached 2^25: redo with unpacked far folds
+      P->packed_now = false;
+      continue;
+    }
     bits = 64;  // a value reached 2^30: redo exactly in 64-bit
     if (P->d.kernel == PIPEDP_MCM_SMEM && P->d.smem64 > 227 * 1024) {
       P->d.kernel = PIPEDP_MCM_WAVEFRONT;
@@ -1542,6 +1552,9 @@ int32_t pipedp_mcm_plan_create(int64_t batch, int64_t n, const int64_t* h_dims, 
     const int64_t T = d.tile, TC = T * T;
     const int64_t N = (n + T - 1) / T, ntiles = N * (N + 1) / 2;
     P->N = (int32_t)N;
+    int64_t maxd = 0;
+    for (int64_t i = 0; i <= n; ++i) maxd = std::max(maxd, h_dims[i]);
+    P->packed_ok = maxd * maxd * maxd < (int64_t)kMcmPackedLimit;
     std::vector<int32_t> pp((size_t)(N * T + 2), 0);
     for (int64_t i = 0; i <= n; ++i) pp[(size_t)i] = (int32_t)h_dims[i];
     const std::vector<unsigned long long> tasks = mcm_tiled_tasks((int)N);
@@ -1633,6 +1646,11 @@ int32_t pipedp_mcm_plan_destroy(pipedp_mcm_plan_t P) {
 // dispatch (the scratch tables are reused; only the dims-derived arrays change).
 static int mcm_plan_reload(pipedp_mcm_plan_t P, const int64_t* h_dims, const McmDispatch& d) {
   const int64_t cnt = P->batch * (P->n + 1);
+  {
+    int64_t maxd = 0;
+    for (int64_t i = 0; i < cnt; ++i) maxd = std::max(maxd, h_dims[i]);
+    P->packed_ok = maxd * maxd * maxd < (int64_t)kMcmPackedLimit;
+  }
   std::vector<int32_t> p32((size_t)cnt);
   for (int64_t i = 0; i < cnt; ++i) p32[(size_t)i] = (int32_t)h_dims[i];
   CK(cudaSetDevice(P->device));

@@ -57,6 +57,8 @@ struct McmTiled {
   int64_t* out_split;
   int* overflow;
   int32_t blocked;             // near in-tile pipeline: 0 CTA-wide folds per step, 1 8x8 sub-blocks, 2 pull
+  int32_t packed;              // far tasks fold (value << 5 | k-in-half) keys: every cell < 2^25 required
+                               // (a finished cell >= 2^25 raises overflow bit 2 -> unpacked rerun)
 };
 
 __host__ __device__ __forceinline__ int64_t tiled_index(int64_t I, int64_t J, int64_t N) {
@@ -88,6 +90,8 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 __device__ __forceinline__ void fence_proxy_async_shared() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
+constexpr uint32_t kMcmPackedLimit = 1u << 25;  // packed far keys: cells and weights below this
+
 __device__ __forceinline__ void spin_until_set(const int* flag) { spin_ge_gpu(flag, 1, 64); }
 __device__ __forceinline__ void spin_until_count(const int* ctr, int want) { spin_ge_gpu(ctr, want, 64); }
 

@@ -117,3 +117,13 @@ def test_tiled_blocked_variant(gpu, oracle, n, t32_maxn, monkeypatch):
     monkeypatch.setenv("PIPEDP_MCM_BLOCKED", "1")
     _check(gpu, oracle, oracle.generate_mcm(n, 5 + n, 1, 100), 4)
     _check(gpu, oracle, [7] * (n + 1), 4)
+
+
+@pytest.mark.parametrize("t32_maxn", ["0", "100000"])
+def test_tiled_packed_far_keys_fallback(gpu, oracle, t32_maxn, monkeypatch):
+    # dims <= 322 enable packed far keys (64-wide tiles); cells past 2^25 (but
+    # below 2^30) must trigger the unpacked 32-bit rerun, not a wrong table
+    monkeypatch.setenv("PIPEDP_MCM_T32_MAXN", t32_maxn)
+    dims = oracle.generate_mcm(300, 7, 100, 200)
+    _check(gpu, oracle, dims, 4)
+    _check(gpu, oracle, oracle.generate_mcm(700, 8, 1, 322), 4)  # packed, values small

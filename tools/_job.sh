@@ -1,1 +1,2 @@
-for pm in 64 16 8; do for w in c2 c4 c5b; do PIPEDP_WIDEN_PIECE_MB=$pm timeout 300 python bench.py --workload $w --no-cpu-baseline --steps 3 --warmup 3 --e2e-steps 5 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('piece $pm $w', round(d['ms_per_step'],2), round(d['e2e']['ms_per_step'],2))"; done; done
+timeout 900 python -m pytest tests/test_gpu_mcm.py -x -q 2>&1 | tail -2
+for w in c3 c4; do timeout 200 python bench.py --workload $w --no-cpu-baseline --e2e-steps 0 --steps 5 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$w', round(d['ms_per_step'],3), d['parity']['match'])"; done
