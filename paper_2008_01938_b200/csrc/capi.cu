@@ -779,7 +779,7 @@ struct pipedp_mcm_plan {
   int64_t total_chunks;
   int launches;
   int last_bits;
-  bool packed_ok;     // tiled far tasks may fold packed keys (max_dim^3 < 2^25)
+  int64_t maxd3;      // max_dim^3 over the plan's instances
   bool packed_now;    // this execute's tiled launch uses them
   // tiled kernel
   int32_t* d_pp;                 // dims, zero padded to N*T + 2
@@ -877,7 +877,11 @@ int mcm_smem_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split
     // two warps for n <= 96: the short diagonals keep them busy (C5a: 3.96 ->
     // 3.19 ms against four warps); more CTAs fit an SM
     const int thr = std::max(32, std::min(128, env_int("PIPEDP_MCM_SQ_THREADS", n <= 96 ? 64 : 128))) / 32 * 32;
-    if (bits == 32) {
+    if (bits == 32 && P->packed_now && n <= 64) {
+      CK(cudaFuncSetAttribute(mcm_smem_square<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq));
+      mcm_smem_square<uint32_t, true><<<(unsigned)P->batch, thr, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
+                                                                            split, P->d_overflow);
+    } else if (bits == 32) {
       CK(cudaFuncSetAttribute(mcm_smem_square<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq));
       mcm_smem_square<uint32_t><<<(unsigned)P->batch, thr, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
                                                                       split, P->d_overflow);
@@ -914,10 +918,14 @@ int mcm_execute(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t
     return PIPEDP_OK;
   }
   int bits = P->d.bits;
-  // packed far keys pay on the 64-wide tiles (ALU-bound far tasks); the 32-wide
-  // ones are latency-bound (C3 unchanged), so they keep the plain fold
-  P->packed_now = P->packed_ok && P->d.kernel == PIPEDP_MCM_TILED && P->d.tile == 64 &&
-                  env_int("PIPEDP_MCM_PACKED", 1) != 0;
+  // packed keys: the 64-wide tiles' far tasks (ALU-bound; the 32-wide ones are
+  // latency-bound and keep the plain fold) and the n <= 64 square-table batches
+  const bool tiled_pk = P->d.kernel == PIPEDP_MCM_TILED && P->d.tile == 64 && P->maxd3 < (int64_t)kMcmPackedLimit;
+  // (square batches: measured no faster -- lane occupancy, not the fold, bounds
+  // them -- so opt-in with PIPEDP_MCM_PACKED_SQUARE=1)
+  const bool square_pk = P->d.kernel == PIPEDP_MCM_SMEM && P->d.bits == 32 && P->n <= 64 &&
+                         P->maxd3 < (1ll << 24) && env_int("PIPEDP_MCM_PACKED_SQUARE", 0) != 0;
+  P->packed_now = (tiled_pk || square_pk) && env_int("PIPEDP_MCM_PACKED", 1) != 0;
   for (;;) {
     CK(cudaMemsetAsync(P->d_overflow, 0, sizeof(int), st));
     if (P->d.kernel == PIPEDP_MCM_SMEM) TRY(mcm_smem_launch(P, bits, cells, split, st));
@@ -1533,6 +1541,11 @@ int32_t pipedp_mcm_plan_create(int64_t batch, int64_t n, const int64_t* h_dims, 
   auto* P = new pipedp_mcm_plan{};
   P->batch = batch;
   P->n = n;
+  {
+    int64_t maxd = 0;
+    for (int64_t i = 0; i < batch * (n + 1); ++i) maxd = std::max(maxd, h_dims[i]);
+    P->maxd3 = maxd * maxd * maxd;  // dims validated <= 1e6: no overflow
+  }
   P->cc = n * (n + 1) / 2;
   P->d = d;
   auto cleanup = [&](cudaError_t e, const char* what) {
@@ -1552,9 +1565,6 @@ int32_t pipedp_mcm_plan_create(int64_t batch, int64_t n, const int64_t* h_dims, 
     const int64_t T = d.tile, TC = T * T;
     const int64_t N = (n + T - 1) / T, ntiles = N * (N + 1) / 2;
     P->N = (int32_t)N;
-    int64_t maxd = 0;
-    for (int64_t i = 0; i <= n; ++i) maxd = std::max(maxd, h_dims[i]);
-    P->packed_ok = maxd * maxd * maxd < (int64_t)kMcmPackedLimit;
     std::vector<int32_t> pp((size_t)(N * T + 2), 0);
     for (int64_t i = 0; i <= n; ++i) pp[(size_t)i] = (int32_t)h_dims[i];
     const std::vector<unsigned long long> tasks = mcm_tiled_tasks((int)N);
@@ -1649,7 +1659,7 @@ static int mcm_plan_reload(pipedp_mcm_plan_t P, const int64_t* h_dims, const Mcm
   {
     int64_t maxd = 0;
     for (int64_t i = 0; i < cnt; ++i) maxd = std::max(maxd, h_dims[i]);
-    P->packed_ok = maxd * maxd * maxd < (int64_t)kMcmPackedLimit;
+    P->maxd3 = maxd * maxd * maxd;
   }
   std::vector<int32_t> p32((size_t)cnt);
   for (int64_t i = 0; i < cnt; ++i) p32[(size_t)i] = (int32_t)h_dims[i];

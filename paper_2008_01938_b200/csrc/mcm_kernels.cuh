@@ -420,7 +420,13 @@ namespace pipedp_dev {
 // per cell G = 2^lg grows as the diagonal shortens; each lane scans its terms
 // j ascending with strict '<' and the G partials reduce lexicographically on
 // (value, j): the reference's first-min split (mcm.cpp:95-104).
-template <typename T>
+// PACKED (uint32 tables, n <= 64): terms fold as keys (cost << 6) | j with one
+// unsigned min -- exact while every cost < 2^26: every finished cell and every
+// weight < 2^24 (host-checked weights; a cell >= 2^24 sets overflow bit 2 and
+// the host reruns the launch unpacked; by induction over the diagonals no
+// candidate of an unflagged run wrapped).  Keys order as (cost, j): the first
+// minimum, as the reference.
+template <typename T, bool PACKED = false>
 __global__ void __launch_bounds__(128)
     mcm_smem_square(int32_t n, int64_t batch, const int64_t* __restrict__ g_dims,
                     int64_t* __restrict__ out_cells, int64_t* __restrict__ out_split,
@@ -443,7 +449,7 @@ __global__ void __launch_bounds__(128)
     os[i] = 0;
   }
   __syncthreads();
-  bool ovf = false;
+  bool ovf = false, ovf2 = false;
   int64_t db = 0;  // lin(r, r+D) = db(D) + r, db(D) = D*n - D(D-1)/2
   for (int D = 1; D < n; ++D) {
     db += n - (D - 1);
@@ -457,20 +463,36 @@ __global__ void __launch_bounds__(128)
       const bool live = tid < slots && t < ncell * G;
       const int r = 1 + (t >> lg), q = t & (G - 1), c = r + D;
       McmBest<T> best{mcm_max_value<T>(), 0};
-      if (live) {
-        const T prc = (T)p[r - 1] * (T)p[c];
-        const T* L = M + r * P + r - 1;  // m[r][r+j-1] at L[j]
-        const T* Rt = M + r * P + c;     // m[r+j][c]   at Rt[j*P]
-        const int32_t* pk = p + r - 1;   // p[r+j-1]    at pk[j]
-        for (int j = 1 + q; j <= D; j += G) {
-          const T cost = L[j] + Rt[j * P] + prc * (T)pk[j];
-          if (cost < best.v) {  // j ascending in this lane: first minimum
-            best.v = cost;
-            best.j = j;
+      if constexpr (PACKED) {
+        uint32_t key = 0xFFFFFFFFu;
+        if (live) {
+          const uint32_t prc = (uint32_t)p[r - 1] * (uint32_t)p[c];
+          const T* L = M + r * P + r - 1;
+          const T* Rt = M + r * P + c;
+          const int32_t* pk = p + r - 1;
+          for (int j = 1 + q; j <= D; j += G)
+            key = min(key, ((uint32_t)(L[j] + Rt[j * P] + prc * (uint32_t)pk[j]) << 6) | (uint32_t)j);
+        }
+        for (int sh = G >> 1; sh > 0; sh >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, sh));
+        best.v = (T)(key >> 6);
+        best.j = (int32_t)(key & 63u);
+        if (live && q == 0 && (uint32_t)best.v >= (1u << 24)) ovf2 = true;
+      } else {
+        if (live) {
+          const T prc = (T)p[r - 1] * (T)p[c];
+          const T* L = M + r * P + r - 1;  // m[r][r+j-1] at L[j]
+          const T* Rt = M + r * P + c;     // m[r+j][c]   at Rt[j*P]
+          const int32_t* pk = p + r - 1;   // p[r+j-1]    at pk[j]
+          for (int j = 1 + q; j <= D; j += G) {
+            const T cost = L[j] + Rt[j * P] + prc * (T)pk[j];
+            if (cost < best.v) {  // j ascending in this lane: first minimum
+              best.v = cost;
+              best.j = j;
+            }
           }
         }
+        if (G > 1) best = mcm_group_reduce(best, G);
       }
-      if (G > 1) best = mcm_group_reduce(best, G);
       if (live && q == 0) {
         M[r * P + c] = best.v;
         oc[db + r] = (int64_t)best.v;
@@ -481,6 +503,7 @@ __global__ void __launch_bounds__(128)
     __syncthreads();
   }
   if (ovf) atomicOr(overflow, 1);
+  if (ovf2) atomicOr(overflow, 2);
 }
 
 }  // namespace pipedp_dev

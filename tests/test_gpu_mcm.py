@@ -127,3 +127,13 @@ def test_tiled_packed_far_keys_fallback(gpu, oracle, t32_maxn, monkeypatch):
     dims = oracle.generate_mcm(300, 7, 100, 200)
     _check(gpu, oracle, dims, 4)
     _check(gpu, oracle, oracle.generate_mcm(700, 8, 1, 322), 4)  # packed, values small
+
+
+def test_batch_packed_square_and_fallback(gpu, oracle, monkeypatch):
+    # n <= 64 batches fold packed keys (opt-in); large dims (cells past 2^24) rerun unpacked
+    monkeypatch.setenv("PIPEDP_MCM_PACKED_SQUARE", "1")
+    for lo, hi in [(1, 100), (200, 255)]:
+        insts = [gpu.McmInstance(oracle.generate_mcm(64, 300 + i, lo, hi)) for i in range(24)]
+        for inst, (t, split) in zip(insts, gpu.solve_mcm_batch(insts)):
+            wc, _, ws = oracle.mcm_solve(inst.dims)
+            assert np.array_equal(t.cells, wc) and np.array_equal(split, ws)
