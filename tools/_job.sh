@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_mcm.py -x -q -k "packed" 2>&1 | tail -2
+PYTHONPATH=. timeout 600 python tools/fuzz.py 420 2>&1 | tail -15

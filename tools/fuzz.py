@@ -1,0 +1,61 @@
+"""Randomised S-DP / MCM parity sweep against the C oracle (test tooling; run on
+a GPU box: PYTHONPATH=. python tools/fuzz.py [seconds]).  Draws shapes that hit
+every dispatch (jump, serial, chunked, v2 pipeline, strict-order CTA, batches,
+tiled / square MCM) and reports any mismatch with its seed."""
+import sys
+import time
+
+import numpy as np
+
+import paper_2008_01938_b200 as pd
+from oracle import pyoracle
+
+orc = pyoracle.load_c()
+OPS = ["min", "max", "saturating-add", "modular-add"]
+budget = float(sys.argv[1]) if len(sys.argv) > 1 else 240.0
+t0 = time.time()
+rng = np.random.default_rng(int(time.time()))
+stats, bad = {}, 0
+it = 0
+while time.time() - t0 < budget:
+    it += 1
+    seed = int(rng.integers(1 << 31))
+    r = np.random.default_rng(seed)
+    kind = r.choice(["sdp_small", "sdp_mid", "sdp_big", "mcm"], p=[0.3, 0.35, 0.2, 0.15])
+    if kind == "mcm":
+        n = int(r.integers(2, 700))
+        dims = orc.generate_mcm(n, seed % 1000, 1, int(r.choice([100, 322, 1290])))
+        t, split = pd.solve_mcm_with_split(pd.McmInstance(dims), pd.MCM_AUTO)
+        wc, _, ws = orc.mcm_solve(dims)
+        ok = np.array_equal(t.cells, wc) and np.array_equal(split, ws)
+        name = f"mcm n={n}"
+    else:
+        op = OPS[int(r.integers(4))]
+        if kind == "sdp_small":
+            a1 = int(r.integers(2, 64))
+            n = int(r.integers(a1 + 1, 200000))
+        elif kind == "sdp_mid":
+            a1 = int(r.integers(64, 8192))
+            n = int(r.integers(a1 + 1, 600000))
+        else:
+            a1 = int(r.integers(64, 8192))
+            n = int(r.integers(1_000_000, 4_000_000))
+        k = int(r.integers(1, min(a1, 1024) + 1))
+        rest = r.choice(np.arange(1, a1), k - 1, replace=False) if k > 1 else np.array([], dtype=np.int64)
+        offs = np.concatenate([[a1], np.sort(rest)[::-1]]).astype(np.int64)
+        cls = int(r.integers(3))
+        init = (r.integers(0, 1 << 20, a1) if cls == 0 else
+                r.integers(-(1 << 40), 1 << 40, a1) if cls == 1 else r.integers(-(1 << 62), 1 << 62, a1))
+        if n * k > 4e9:
+            continue
+        t = pd.solve_sequential(pd.SdpInstance(n, offs, init, op))
+        want, _ = orc.sdp_solve(offs, init, n, op)
+        ok = np.array_equal(t.cells, want)
+        plan = pd.SdpPlan(1, n, k, a1, offs, init, op)
+        name = plan.describe()[0].split("[")[0]
+        plan.close()
+    stats[name.split(" ")[0]] = stats.get(name.split(" ")[0], 0) + 1
+    if not ok:
+        bad += 1
+        print(f"MISMATCH seed={seed} kind={kind} {name}", flush=True)
+print(f"fuzz: {it} cases in {time.time() - t0:.0f} s, {bad} mismatches; by kernel: {stats}")
