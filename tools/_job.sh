@@ -1,1 +1,3 @@
-PYTHONPATH=. timeout 600 python tools/fuzz.py 420 2>&1 | tail -15
+# scratch job script for ad-hoc gpurun calls (the round evidence runs via tools/evidence.sh)
+timeout 1200 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
