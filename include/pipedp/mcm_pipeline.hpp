@@ -31,4 +31,16 @@ struct McmPipelineResult {
 McmPipelineResult solve_mcm_pipeline(const McmInstance& instance,
                                      const McmScheduleConfig& config = {});
 
+/// Addresses of cells predicted to read a not-yet-final operand under the
+/// paper-literal schedule (reference mcm_pipeline.hpp:128-131): cell (r,c) on
+/// diagonal D is implicated iff some term j satisfies
+/// lin(r,c) - lin(r+j,c) <= D - 2j.  lin(r,c) - lin(r+j,c) depends on D and j
+/// only, so whole diagonals are in or out: O(n^2) for any n (the reference's
+/// per-cell scan is O(n^3) and is what limits the CPU study to small n).
+std::vector<std::int64_t> hazard_frontier(std::int64_t n);
+
+/// Cells implicated by a paper-literal hazard report: the reading lane's own
+/// cell, head - lane + 1.  Sorted, deduplicated (reference mcm_pipeline.cpp:96-103).
+std::vector<std::int64_t> hazard_cells(const HazardReport& report);
+
 }  // namespace pipedp

@@ -562,3 +562,17 @@ def op_latency_ns(op="min", value_bits=32, device=-1):
     ns, cyc = C.c_double(), C.c_double()
     _check(lib().pipedp_op_latency_ns(_op_index(op), value_bits, device, C.byref(ns), C.byref(cyc)))
     return ns.value, cyc.value
+
+
+def hazard_frontier(n: int):
+    """hazard_frontier (mcm_pipeline.hpp:128-131): addresses of the cells the
+    paper-literal MCM schedule reads before they are final.  Host logic; the
+    condition depends on the diagonal only (see include/pipedp/mcm_pipeline.hpp)."""
+    if n < 2:
+        raise Error(11, "InvalidParams: frontier needs n >= 2")
+    out = []
+    for D in range(1, n):
+        if any(j * n - j * (2 * D - j - 1) // 2 - j <= D - 2 * j for j in range(1, D + 1)):
+            base = D * n - D * (D - 1) // 2
+            out.extend(base + r for r in range(1, n - D + 1))
+    return out

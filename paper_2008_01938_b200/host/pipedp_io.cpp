@@ -7,6 +7,9 @@
 
 #include "pipedp/error.hpp"
 #include "pipedp/io.hpp"
+#include "pipedp/mcm_pipeline.hpp"
+
+#include <algorithm>
 
 namespace pipedp {
 
@@ -138,6 +141,30 @@ std::string mcm_parenthesization(const McmInstance& instance, const std::vector<
     }
   }
   return out;
+}
+
+std::vector<std::int64_t> hazard_frontier(std::int64_t n) {
+  if (n < 2) fail(errc::invalid_params, "frontier needs n >= 2");
+  std::vector<std::int64_t> out;
+  for (std::int64_t D = 1; D < n; ++D) {
+    // lin(r, r+D) - lin(r+j, r+D) = sum_{e = D-j+1}^{D} (n - e + 1) - j
+    //                             = j n - j (2D - j - 1) / 2 - j
+    bool hit = false;
+    for (std::int64_t j = 1; j <= D && !hit; ++j) hit = j * n - j * (2 * D - j - 1) / 2 - j <= D - 2 * j;
+    if (!hit) continue;
+    const std::int64_t base = D * n - D * (D - 1) / 2;  // lin(r, r+D) = base + r
+    for (std::int64_t r = 1; r + D <= n; ++r) out.push_back(base + r);
+  }
+  return out;
+}
+
+std::vector<std::int64_t> hazard_cells(const HazardReport& report) {
+  std::vector<std::int64_t> cells;
+  cells.reserve(report.hazards.size());
+  for (const HazardRecord& h : report.hazards) cells.push_back(h.head - h.lane + 1);
+  std::sort(cells.begin(), cells.end());
+  cells.erase(std::unique(cells.begin(), cells.end()), cells.end());
+  return cells;
 }
 
 }  // namespace pipedp

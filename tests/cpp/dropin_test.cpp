@@ -288,6 +288,20 @@ static int run_io() {
     std::int64_t rows, cols;
     EXPECT(paren_cost(pr, r.dims, i, rows, cols) == best && i == pr.size());
   }
+  // hazard_frontier against the reference's per-cell scan (mcm_pipeline.cpp:79-93)
+  for (std::int64_t n : {2, 3, 7, 33, 90}) {
+    std::vector<std::int64_t> want;
+    for (std::int64_t addr = n + 1; addr <= cell_count(n); ++addr) {
+      const TriCoord cc = coord(addr, n);
+      for (std::int64_t j = 1; j <= cc.diagonal(); ++j)
+        if (addr - lin(TriCoord{cc.row + j, cc.col}, n) <= cc.diagonal() - 2 * j) {
+          want.push_back(addr);
+          break;
+        }
+    }
+    EXPECT(hazard_frontier(n) == want);
+  }
+  EXPECT(throws_errc([] { hazard_frontier(1); }, errc::invalid_params, "InvalidParams: "));
   std::printf("%s\n", failures ? "FAILED" : "OK");
   return failures ? 1 : 0;
 }

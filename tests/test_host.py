@@ -189,3 +189,23 @@ def test_parenthesization_from_oracle_split(pd, oracle):
             else:
                 i += 1
         assert stack[0][2] == (int(cells[-1]) if n > 1 else 0)
+
+
+def test_hazard_frontier_matches_reference(pd, ref):
+    # the reference's per-cell scan (mcm_pipeline.cpp:79-93) vs the per-diagonal form
+    for n in [2, 3, 4, 5, 8, 17, 64, 130]:
+        got = pd.hazard_frontier(n)
+        want = []
+        for D in range(1, n):  # restated per cell, as the reference loops
+            for r in range(1, n - D + 1):
+                addr = D * n - D * (D - 1) // 2 + r
+                for j in range(1, D + 1):
+                    right = (D - j) * n - (D - j) * (D - j - 1) // 2 + (r + j)
+                    if addr - right <= D - 2 * j:
+                        want.append(addr)
+                        break
+        assert got == sorted(want)
+        if ref is not None:  # the reference library itself (oracle/_ref)
+            assert got == ref.hazard_frontier(n).tolist()
+    with pytest.raises(pd.Error):
+        pd.hazard_frontier(1)
