@@ -1399,9 +1399,25 @@ int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, in
   // product + transpose per squaring, state 0, the persistent chain, the batch
   if (launches) {
     int32_t nl = 1;
-    if (P->d.chunked) {  // build, 2 per squaring / multiply, state 0, 2 x 4 for Q^16, chain, batch
+    if (P->d.chunked) {  // the launches of sdp_chunked_run, counted by replaying its ladder
       const int top = 63 - __builtin_clzll((unsigned long long)P->Lc);
-      nl = 1 + 2 * (top + __builtin_popcountll((unsigned long long)P->Lc) - 1) + 1 + (P->G >= 64 ? 8 : 0) + 1 + 1;
+      auto prod = [&](int64_t t_new) { return 2 + (t_new < P->a1 ? 1 : 0); };  // mul + transpose (+ shift rows)
+      int64_t ex = 1, er = 0;
+      nl = 1;  // build
+      for (int i = 0; i <= top; ++i) {
+        if ((P->Lc >> i) & 1) {
+          if (er) nl += prod(er + ex);
+          er += ex;
+        }
+        if (i < top) {
+          nl += prod(2 * ex);
+          ex *= 2;
+        }
+      }
+      nl += 1;  // state 0
+      if (P->G >= 64)
+        for (int b = 1; b < 16; b *= 2) nl += prod(er * 2 * b);
+      nl += 1 + 1;  // chain, chunk batch
     }
     *launches = nl;
   }
