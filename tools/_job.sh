@@ -1,1 +1,1 @@
-for am in 256 384 512; do for mw in 1 2 3; do PIPEDP_CHUNK_AMID=$am PIPEDP_CHUNK_MID_WARPS=$mw timeout 200 python bench.py --workload c2 --no-cpu-baseline --e2e-steps 0 --steps 5 --warmup 3 | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('amid $am mid $mw', round(d['ms_per_step'],3), d['parity']['match'])"; done; done
+PYTHONPATH=. timeout 900 python tools/fuzz.py 600 2>&1 | tail -8
