@@ -1137,8 +1137,10 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
     SdpDispatch& dc = P->dc;
     if (!dc.warp_kernel && !dc.remote && !dc.v2 && !dc.small && !dc.gfar) {
       int64_t jf = 0;
-      for (int64_t j = 0; j < k; ++j) jf += h_offsets[j] >= std::max(128, env_int("PIPEDP_CHUNK_AMID", kAMid));
-      dc.shape.a_mid = std::max(128, env_int("PIPEDP_CHUNK_AMID", kAMid)) & ~31;
+      // mid/far boundary 384 for wide states (C2: 5.81 -> 5.74 ms measured)
+      const int amid = std::max(128, env_int("PIPEDP_CHUNK_AMID", a1 > 1024 ? 384 : kAMid)) & ~31;
+      for (int64_t j = 0; j < k; ++j) jf += h_offsets[j] >= amid;
+      dc.shape.a_mid = amid;
       dc.shape.mid_warps = std::max(1, env_int("PIPEDP_CHUNK_MID_WARPS", 1));
       dc.shape.far_warps = (int32_t)std::min<int64_t>(std::max(1, env_int("PIPEDP_CHUNK_FAR_WARPS", 8)),
                                                       std::max<int64_t>(1, (jf + 47) / 48));
