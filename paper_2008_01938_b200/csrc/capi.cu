@@ -1102,15 +1102,29 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
   if (e == cudaSuccess && d.warp_kernel && batch > 1 && (op == PIPEDP_OP_MIN || op == PIPEDP_OP_MAX)) {
     // group the instances that take the batch kernel's dominance form (offset 1,
     // a_1 <= 128) ahead of the others
+    // modes as sdp_batch_warp decides them: 1 (offset 1), 2 (S* covers [2, 127]), 0
+    std::vector<int> mode((size_t)batch, 0);
+    for (int64_t b = 0; b < batch && a1 <= 128 && k >= 2; ++b) {
+      const int64_t* o = h_offsets + b * k;
+      bool has1 = false;
+      for (int64_t j = 0; j < k; ++j) has1 = has1 || o[j] == 1;
+      if (has1) {
+        mode[(size_t)b] = 1;
+        continue;
+      }
+      bool reach[128] = {true};
+      bool all = true;
+      for (int v = 1; v < 128; ++v) {
+        for (int64_t j = 0; j < k && !reach[v]; ++j) reach[v] = o[j] <= v && reach[v - o[j]];
+        if (v >= 2) all = all && reach[v];
+      }
+      if (all) mode[(size_t)b] = 2;
+    }
     std::vector<int32_t> perm;
     perm.reserve((size_t)batch);
-    for (int pass = 0; pass < 2; ++pass)
-      for (int64_t b = 0; b < batch; ++b) {
-        bool has1 = false;
-        for (int64_t j = 0; j < k; ++j) has1 = has1 || h_offsets[b * k + j] == 1;
-        const bool dom = has1 && a1 <= 128 && k >= 2;
-        if (dom == (pass == 0)) perm.push_back((int32_t)b);
-      }
+    for (int want : {1, 2, 0})
+      for (int64_t b = 0; b < batch; ++b)
+        if (mode[(size_t)b] == want) perm.push_back((int32_t)b);
     e = cudaMalloc(&P->d_perm, sizeof(int32_t) * batch);
     if (e == cudaSuccess) e = cudaMemcpy(P->d_perm, perm.data(), sizeof(int32_t) * batch, cudaMemcpyHostToDevice);
   }

@@ -196,6 +196,10 @@ template <typename T>
 __device__ __forceinline__ T shfl_idx(T v, int src) {
   return __shfl_sync(0xffffffffu, v, src);
 }
+template <typename T>
+__device__ __forceinline__ T shfl_up(T v, int delta) {
+  return __shfl_up_sync(0xffffffffu, v, delta);
+}
 
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 

@@ -896,7 +896,64 @@ __global__ void __launch_bounds__(256, 5)
   // batches before it fold to x at one lane each (three shuffles); only
   // offsets >= 128 (a_1 itself) are read from the ring.  From batch 4 on;
   // the first batches take the general path.
-  const bool dom = kLA && IsIdem<OP>::value && im.scan && a1 <= 128 && S.k >= 2;
+  // Second form (dom2): no offset 1 but every d in [2, 127] a sum of offsets
+  // (S* >= [2, 127]): then x_l = b_l (x) B(l-2) with B the batch's prefix-(x)
+  // of b, the next batch's in-batch terms are B(30) / B(31), and a 32-wide
+  // offset range folds to x at its largest position p1 and, when its offset
+  // + 1 is an offset too, at p1 - 1 (ST[p] >= ST[p1] for p <= p1 - 2).
+  int mode = 0;  // 1: offset 1 (dominance form), 2: dom2, 0: general path
+  bool n2 = false, n3 = false, n4 = false;
+  if (kLA && IsIdem<OP>::value && a1 <= 128 && S.k >= 2) {
+    if (im.scan) {
+      mode = 1;
+    } else {
+      unsigned long long s0 = 0, s1 = 0;  // offsets < 128 as a bit set
+      for (int j = lane; j < S.k; j += 32) {
+        const int d = offs[j];
+        if (d < 64) s0 |= 1ull << d;
+        else if (d < 128) s1 |= 1ull << (d - 64);
+      }
+#pragma unroll
+      for (int sh = 16; sh >= 1; sh >>= 1) {
+        s0 |= __shfl_xor_sync(0xffffffffu, s0, sh);
+        s1 |= __shfl_xor_sync(0xffffffffu, s1, sh);
+      }
+      unsigned long long r0 = 1ull, r1 = 0;  // S* (with 0) over [0, 127]
+      for (int v = 1; v < 128; ++v) {
+        bool hit = false;
+        for (int j = lane; j < S.k; j += 32) {
+          const int u = v - offs[j];
+          if (u >= 0) hit = hit || ((u < 64 ? r0 >> u : r1 >> (u - 64)) & 1ull);
+        }
+        if (__any_sync(0xffffffffu, hit)) {
+          if (v < 64) r0 |= 1ull << v;
+          else r1 |= 1ull << (v - 64);
+        }
+      }
+      if ((r0 | 3ull) == ~0ull && r1 == ~0ull) mode = 2;
+      auto in_s = [&](int d) { return d < 64 ? ((s0 >> d) & 1ull) != 0 : d < 128 && ((s1 >> (d - 64)) & 1ull) != 0; };
+      if (mode == 2) {  // per range: is (smallest offset in it) + 1 an offset in it too
+        bool seen2 = false, seen3 = false, seen4 = false;
+        for (int j = S.k - 1; j >= 0; --j) {  // ascending d
+          const int d = offs[j];
+          if (d >= 128) break;
+          if (!seen2 && d >= lane + 33 && d <= lane + 64) {
+            seen2 = true;
+            n2 = d + 1 <= min(lane + 64, 127) && in_s(d + 1);
+          }
+          if (!seen3 && d >= lane + 65 && d <= lane + 96) {
+            seen3 = true;
+            n3 = d + 1 <= min(lane + 96, 127) && in_s(d + 1);
+          }
+          if (!seen4 && d >= lane + 97 && d <= lane + 128) {
+            seen4 = true;
+            n4 = d + 1 <= 127 && in_s(d + 1);
+          }
+        }
+      }
+    }
+  }
+  const bool dom = mode != 0;
   int src2 = -1, src3 = -1, src4 = -1, j128 = 0;
   if (dom) {
     for (int j = S.k - 1; j >= 0; --j) {  // ascending d
@@ -919,7 +976,20 @@ __global__ void __launch_bounds__(256, 5)
     if (dom && b >= 4) {
       // offsets >= 128 from the ring, [l+33, 128) as pre_cur, [l+1, l+32] as nxt
       acc = SemiOp<OP, T>::apply(fold_range<OP, T, ASSOC>(pre_cur, true, ring + pos, ob, 0, j128), nxt);
-      idem_closure<OP, T>(acc, nxt, im);
+      if (mode == 1) {
+        idem_closure<OP, T>(acc, nxt, im);
+      } else {  // dom2: x_l = b_l (x) B(l-2); next batch's in-batch terms B(30) / B(31)
+        T B = acc;
+#pragma unroll
+        for (int sh = 1; sh < 32; sh <<= 1) {
+          const T o = shfl_up(B, sh);
+          if (lane >= sh) B = SemiOp<OP, T>::apply(B, o);
+        }
+        const T b2 = shfl_up(B, 2);
+        const T n30 = shfl_idx(B, 30), n31 = shfl_idx(B, 31);
+        if (lane >= 2) acc = SemiOp<OP, T>::apply(acc, b2);
+        nxt = lane == 0 ? n30 : n31;
+      }
     } else if (kLA) {
       acc = fold_range<OP, T, ASSOC>(T(0), false, ring + pos, ob, 0, jn);
       if (b == 0) {
@@ -949,6 +1019,13 @@ __global__ void __launch_bounds__(256, 5)
         const T v4 = shfl_idx(xm3, src4 < 0 ? 0 : src4);
         pre_cur = SemiOp<OP, T>::apply(SemiOp<OP, T>::apply(src2 < 0 ? idv : v2, src3 < 0 ? idv : v3),
                                        src4 < 0 ? idv : v4);
+        if (mode == 2) {  // the positions p1 - 1 (offset + 1 in the same range)
+          const T w2 = shfl_idx(xm1, src2 > 0 ? src2 - 1 : 0);
+          const T w3 = shfl_idx(xm2, src3 > 0 ? src3 - 1 : 0);
+          const T w4 = shfl_idx(xm3, src4 > 0 ? src4 - 1 : 0);
+          pre_cur = SemiOp<OP, T>::apply(pre_cur, SemiOp<OP, T>::apply(SemiOp<OP, T>::apply(n2 ? w2 : idv, n3 ? w3 : idv),
+                                                                       n4 ? w4 : idv));
+        }
       }
       xm3 = xm2;
       xm2 = xm1;

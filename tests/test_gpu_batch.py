@@ -67,3 +67,24 @@ def test_config5_sample_digests(gpu, oracle):
     for i in (0, 7, 63):
         c, _ = oracle.sdp_solve(s.h_offsets[i], s.h_init[i], sb.n, "min")
         assert int(got[i]) == oracle.digest(c)
+
+
+@pytest.mark.parametrize("op", ["min", "max"])
+def test_sdp_batch_dominance_forms(gpu, oracle, op):
+    # a_1 = 128 batches mixing the three paths of sdp_batch_warp: offset 1
+    # (dominance form), no offset 1 but every d in [2, 127] a sum of offsets
+    # (second form: {2, 3} and {2, 5}), and neither ({4, 6, ...} only)
+    rng = np.random.default_rng(11 if op == "min" else 12)
+    insts = []
+    for i in range(48):
+        kind = i % 4
+        must = [1, 7] if kind == 0 else [2, 3] if kind == 1 else [2, 5] if kind == 2 else [4, 6]
+        pool = np.arange(4, 128, 2) if kind == 3 else np.arange(2 if kind else 1, 128)
+        pool = pool[~np.isin(pool, must + [128])]
+        rest = rng.choice(pool, 40, replace=False)  # every instance: k = 43
+        offs = np.sort(np.concatenate([[128], must, rest]))[::-1].astype(np.int64)
+        init = rng.integers(-(2**30), 2**30, 128)
+        insts.append(gpu.SdpInstance(6000, offs, init, op))
+    for inst, t in zip(insts, gpu.solve_sequential_batch(insts)):
+        want, _ = oracle.sdp_solve(inst.offsets, inst.init, inst.n, op)
+        assert np.array_equal(t.cells, want)
