@@ -1,1 +1,1 @@
-timeout 900 python -m pytest tests/test_gpu_batch.py -x -q 2>&1 | tail -3
+PYTHONPATH=. timeout 900 python tools/fuzz.py 480 2>&1 | tail -8

@@ -21,8 +21,30 @@ while time.time() - t0 < budget:
     it += 1
     seed = int(rng.integers(1 << 31))
     r = np.random.default_rng(seed)
-    kind = r.choice(["sdp_small", "sdp_mid", "sdp_big", "mcm"], p=[0.3, 0.35, 0.2, 0.15])
-    if kind == "mcm":
+    kind = r.choice(["sdp_small", "sdp_mid", "sdp_big", "mcm", "sdp_batch"], p=[0.25, 0.3, 0.15, 0.15, 0.15])
+    if kind == "sdp_batch":
+        # warp-per-instance batches (a_1 <= 128): the three sdp_batch_warp paths
+        op = ["min", "max", "saturating-add", "modular-add"][int(r.integers(4))]
+        a1 = int(r.integers(2, 129))
+        k = int(r.integers(2, min(a1, 64) + 1))
+        n = int(r.integers(a1 + 1, 20000))
+        count = int(r.integers(2, 40))
+        insts = []
+        for _ in range(count):
+            lo = int(r.integers(1, 4))
+            pool = np.arange(lo, a1)
+            if len(pool) < k - 1:
+                pool = np.arange(1, a1)
+            rest = r.choice(pool, k - 1, replace=False)
+            offs = np.concatenate([[a1], np.sort(rest)[::-1]]).astype(np.int64)
+            init = r.integers(-(1 << 30), 1 << 30, a1) if op != "modular-add" else r.integers(0, 2**31 - 1, a1)
+            insts.append(pd.SdpInstance(n, offs, init, op))
+        ok = True
+        for inst, t in zip(insts, pd.solve_sequential_batch(insts)):
+            want, _ = orc.sdp_solve(inst.offsets, inst.init, inst.n, op)
+            ok = ok and np.array_equal(t.cells, want)
+        name = "sdp_batch"
+    elif kind == "mcm":
         n = int(r.integers(2, 700))
         dims = orc.generate_mcm(n, seed % 1000, 1, int(r.choice([100, 322, 1290])))
         t, split = pd.solve_mcm_with_split(pd.McmInstance(dims), pd.MCM_AUTO)
