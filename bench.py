@@ -3,17 +3,24 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2] [--impl ours|reference]
 
-One process per GPU (torchrun for N > 1, NCCL only for the barrier and the
-max-over-ranks timing reduction; the data path has no collective).
+One process per GPU.  Under torchrun (WORLD_SIZE set) every process is one
+rank; `--gpus N` without torchrun starts the N ranks itself (127.0.0.1
+rendezvous).  NCCL carries only the barrier, the max-over-ranks timing
+reduction and the post-timing digest gather (gloo when ranks share a GPU);
+the data path has no collective.
+
+Default workload: c2 at N = 1 (BASELINE's headline single instance), the
+sharded c5b batch at N > 1 (the only configuration that shards, SURVEY.md
+8e), with a c5a companion measurement in the same line.
 
 Workloads (BASELINE.json configs; inputs from the reference's own seeded
 generators, generate.cpp:21-60, restated bit-exactly in the C ABI):
   c1   S-DP Fibonacci n=2^20, offsets {2,1}, saturating-add, init {1,1}
-  c2   S-DP n=2^24, k=1024, a_1=4096, min, seed 1           (DEFAULT, the headline)
+  c2   S-DP n=2^24, k=1024, a_1=4096, min, seed 1           (default at N = 1, the headline)
   c3   MCM n=1024, dims U[1,100], seed 1 (pipeline kernel; --mcm-kernel tournament for the paper's method)
   c4   MCM n=8192, dims U[1,100], seed 1 (table in HBM)
   c5a  65,536 x MCM n=64 (batch, sharded over ranks)
-  c5b  65,536 x S-DP n=2^16, k=64, min (batch, sharded over ranks)
+  c5b  65,536 x S-DP n=2^16, k=64, min (batch, sharded over ranks; default at N > 1)
 Single-instance workloads (c1-c4) cannot be split (every cell depends on its
 predecessors): at N > 1 every rank solves its own instance
 (seed 1 + rank), i.e. a batch of N independent instances, one per GPU -- weak
@@ -195,6 +202,8 @@ class Batch:
         spec = B.McmBatchSpec() if name == "c5a" else B.SdpBatchSpec()
         self.spec = spec
         self.shard = B.BatchShard(spec, rank, world, dev)
+        self.shard.upload(torch.cuda.current_stream())  # the shard's init cells into HBM (once)
+        torch.cuda.synchronize()
         self.relax = self.shard.relaxations()
         n = spec.n
         if name == "c5a":
@@ -298,23 +307,189 @@ def traffic_for(name):
     return e.get("dram_bytes_per_launch") if isinstance(e, dict) else None
 
 
+# ------------------------------------------------------------ launching ---
+def spawn_ranks(n):
+    """`--gpus N` without torchrun: start N ranks of this script (one per GPU,
+    or sharing the visible GPUs round-robin) with a 127.0.0.1 rendezvous; only
+    rank 0's stdout is the bench line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n), LOCAL_WORLD_SIZE=str(n),
+                   MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__), *sys.argv[1:]], env=env,
+                                      stdout=None if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
+
+
 # --------------------------------------------------------------------- main ---
+class Ranks:
+    """Process-group plumbing: barrier and scalar reductions.  NCCL when every
+    rank has its own GPU, gloo when ranks share one (a 1-GPU box running
+    `--gpus 2`)."""
+
+    def __init__(self, torch, world, rank, device):
+        import torch.distributed as dist
+        self.torch, self.dist, self.world, self.rank = torch, dist, world, rank
+        self.backend = None
+        if world > 1:
+            shared = torch.cuda.device_count() < world
+            self.backend = "gloo" if shared else "nccl"
+            kw = {} if shared else {"device_id": torch.device("cuda", device)}
+            dist.init_process_group(self.backend, **kw)
+        self.dev = "cpu" if self.backend == "gloo" else "cuda"
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def reduce(self, x, op):
+        if self.world == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64, device=self.dev)
+        self.dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    def max(self, x):
+        return self.reduce(x, self.dist.ReduceOp.MAX) if self.world > 1 else x
+
+    def sum(self, x):
+        return self.reduce(x, self.dist.ReduceOp.SUM) if self.world > 1 else x
+
+    def gather_digests(self, local, total):
+        """Per-instance digests of every rank in global instance order (rank 0)."""
+        import numpy as np
+        from paper_2008_01938_b200 import batch as B
+        if self.world == 1:
+            return local.cpu().numpy().view(np.uint64).copy()
+        src = local.cpu() if self.dev == "cpu" else local
+        out = B.gather_digests(src, total)
+        return None if out is None else np.asarray(out).view(np.uint64)
+
+    def close(self):
+        if self.world > 1:
+            self.dist.destroy_process_group()
+
+
+def golden_batch_digests(name):
+    import numpy as np
+    here = os.path.join(ROOT, "tests", "golden")
+    try:
+        if name == "c5a":
+            return np.load(os.path.join(here, "c5a_cells.npy")), np.load(os.path.join(here, "c5a_split.npy"))
+        return np.load(os.path.join(here, "c5b_cells.npy")), None
+    except OSError:
+        return None, None
+
+
+def measure(pd, torch, R, name, args, rank, world, local, flush, with_e2e=True):
+    """Warm up, time K steps (device events, max over ranks), check parity,
+    then the end-to-end C-ABI leg.  Returns the per-workload record."""
+    single = name not in BATCH
+    W = Batch(pd, torch, name, rank, world, local) if not single else Single(pd, torch, name, rank, local,
+                                                                               args.mcm_kernel)
+    stream = torch.cuda.current_stream()
+    for _ in range(max(args.warmup, 0)):
+        flush.zero_()
+        W.execute(stream)
+    torch.cuda.synchronize()
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    R.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for e0, e1 in ev:
+            flush.zero_()
+            e0.record(stream)
+            W.execute(stream)
+            e1.record(stream)
+        torch.cuda.synchronize()
+    R.barrier()
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    kernel_ms = sum(step_ms)
+    kernel_ms_max = R.max(kernel_ms)
+    relax_total = R.sum(float(W.relax))
+    value = relax_total * K / (kernel_ms_max / 1e3)
+
+    # parity of the benchmarked output (after timing): single instances by the
+    # reference's table digest of the seed-1 instance, batches by every
+    # instance's device digest against the reference-generated lists
+    parity = None
+    if single:
+        if rank == 0:
+            golden = load_json(os.path.join(ROOT, "tests", "golden", "golden.json")) or {}
+            want = {"c1": golden.get("configs", {}).get("c1_saturating-add", {}).get("digest"),
+                    "c2": golden.get("configs", {}).get("c2", {}).get("digest"),
+                    "c3": "9e31907a82260f66", "c4": "cc41fd2d4975b51b"}.get(name)
+            got = f"{W.digest():016x}"
+            parity = {"cells_digest": got, "golden": want, "match": (got == want) if want else None}
+    else:
+        import numpy as np
+        cells = R.gather_digests(W.shard.digests(stream), W.spec.total)
+        split = R.gather_digests(W.shard.digests(stream, split=True), W.spec.total) if name == "c5a" else None
+        if rank == 0:
+            want_c, want_s = golden_batch_digests(name)
+            if want_c is None:
+                parity = {"match": None, "note": "golden digest lists absent"}
+            else:
+                bad = int(np.count_nonzero(cells != want_c))
+                if split is not None:
+                    bad += int(np.count_nonzero(split != want_s))
+                parity = {"instances": int(cells.size), "tables_checked": int(cells.size) * (2 if split is not None else 1),
+                          "mismatches": bad, "match": bad == 0,
+                          "golden": "tests/golden/%s (reference, make_c5_digests.py)" %
+                                    ("c5a_cells.npy+c5a_split.npy" if name == "c5a" else "c5b_cells.npy")}
+
+    e2e = None
+    if with_e2e:
+        ek = args.e2e_steps if args.e2e_steps is not None else min(K, 3)
+        if ek:
+            W.e2e_step()  # warm-up: staging buffers, copy pool, cached plan / device buffers
+        R.barrier()
+        t0 = time.perf_counter()
+        for _ in range(ek):
+            W.e2e_step()
+        e2e_s = R.max(time.perf_counter() - t0)
+        h2d, d2h = W.e2e_bytes()
+        e2e = {"value": relax_total * ek / e2e_s if ek else None, "unit": UNIT,
+               "h2d_bytes_per_step": int(R.sum(h2d)), "d2h_bytes_per_step": int(R.sum(d2h)),
+               "steps": ek, "ms_per_step": e2e_s * 1e3 / max(ek, 1),
+               "call": "pipedp_sdp_solve / pipedp_mcm_solve (C ABI, host buffers)" if single
+               else "pipedp_sdp_solve_batch / pipedp_mcm_solve_batch (C ABI, host buffers)"}
+    rec = {"W": W, "value": value, "kernel_ms": kernel_ms, "kernel_ms_max": kernel_ms_max, "K": K,
+           "step_ms": step_ms, "parity": parity, "e2e": e2e, "clocks": clk.summary(),
+           "launches": W.launches() * K, "kernel": W.kernel_name(), "bits": W.value_bits()}
+    return rec
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: c2 at N = 1, c5b (+ c5a companion) at N > 1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mcm-kernel", default="pipeline", choices=["pipeline", "tiled", "wavefront", "tournament"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-companion", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=None)
     args = ap.parse_args()
+
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args.gpus))
 
     world = env_int("WORLD_SIZE", 1)
     rank = env_int("RANK", 0)
     local = env_int("LOCAL_RANK", 0)
-    name = args.workload
+    name = args.workload or ("c2" if world == 1 else "c5b")
     single = name not in BATCH
     config = {"workload": f"{name}: {WORKLOADS[name]}", "n_instances": world if single else 65536,
               "parallelism": (f"replicas{world}" if single else f"shard{world}"),
@@ -325,12 +500,11 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        import os as _os
-        cores = _os.cpu_count() or 1
+        cores = os.cpu_count() or 1
         thr = 1 if single else cores
         cpu_reference_sample(name, thr, 1)  # warm-up sample
         v, thr, kind, sample, dt = cpu_reference_sample(name, thr, max(1, args.steps))
-        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": dt * 1e3 / max(1, args.steps),
                 "higher_is_better": True, "scaling": "weak" if single else "strong",
                 "vs_baseline": None, "dtype": "int64", "data": "synthetic (reference generators)",
@@ -341,87 +515,28 @@ def main():
         return
 
     import torch
-    import torch.distributed as dist
     import paper_2008_01938_b200 as pd
 
+    ndev = max(torch.cuda.device_count(), 1)
+    local = local % ndev
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-
-    def barrier():
-        if world > 1:
-            dist.barrier()
-
-    def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    def sum_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
-
-    W = Batch(pd, torch, name, rank, world, local) if not single else Single(pd, torch, name, rank, local,
-                                                                               args.mcm_kernel)
-    stream = torch.cuda.current_stream()
+    R = Ranks(torch, world, rank, local)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    for _ in range(max(args.warmup, 0)):
-        flush.zero_()
-        W.execute(stream)
-    torch.cuda.synchronize()
 
-    K = args.steps
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
-    barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clk:
-        for e0, e1 in ev:
-            flush.zero_()
-            e0.record(stream)
-            W.execute(stream)
-            e1.record(stream)
-        torch.cuda.synchronize()
-    barrier()
-    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
-    kernel_ms = sum(step_ms)
-    kernel_ms_max = max_over_ranks(kernel_ms)
-    relax_total = sum_over_ranks(float(W.relax))
-    value = relax_total * K / (kernel_ms_max / 1e3)
-
-    # parity spot check of the benchmarked output (rank 0, seed-1 instance)
-    parity = None
-    if rank == 0 and single:
-        golden = load_json(os.path.join(ROOT, "tests", "golden", "golden.json")) or {}
-        want = {"c1": golden.get("configs", {}).get("c1_saturating-add", {}).get("digest"),
-                "c2": golden.get("configs", {}).get("c2", {}).get("digest"),
-                "c3": "9e31907a82260f66", "c4": "cc41fd2d4975b51b"}.get(name)
-        got = f"{W.digest():016x}"
-        parity = {"cells_digest": got, "golden": want, "match": (got == want) if want else None}
-
-    # end to end through the reference-facing C ABI with host buffers
-    ek = args.e2e_steps if args.e2e_steps is not None else min(K, 3)
-    if ek:
-        W.e2e_step()  # warm-up: staging buffers, copy pool, cached plan / device buffers
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(ek):
-        W.e2e_step()
-    e2e_s = max_over_ranks(time.perf_counter() - t0)
-    h2d, d2h = W.e2e_bytes()
-    e2e = {"value": relax_total * ek / e2e_s if ek else None, "unit": UNIT,
-           "h2d_bytes_per_step": int(sum_over_ranks(h2d)), "d2h_bytes_per_step": int(sum_over_ranks(d2h)),
-           "steps": ek, "ms_per_step": e2e_s * 1e3 / max(ek, 1),
-           "call": "pipedp_sdp_solve / pipedp_mcm_solve (C ABI, host buffers)" if single
-           else "pipedp_sdp_solve_batch / pipedp_mcm_solve_batch (C ABI, host buffers)"}
+    rec = measure(pd, torch, R, name, args, rank, world, local, flush)
+    companion = None
+    if world > 1 and args.workload is None and not args.no_companion:
+        del rec["W"].shard  # free the c5b tables before the companion batch
+        torch.cuda.empty_cache()
+        c = measure(pd, torch, R, "c5a", args, rank, world, local, flush, with_e2e=False)
+        companion = {"workload": f"c5a: {WORKLOADS['c5a']}", "value": c["value"], "unit": UNIT,
+                     "ms_per_step": c["kernel_ms_max"] / c["K"], "kernel": c["kernel"],
+                     "parity": c["parity"], "gpu_launches": c["launches"]}
+    W, K = rec["W"], rec["K"]
+    kernel_ms, kernel_ms_max = rec["kernel_ms"], rec["kernel_ms_max"]
 
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
+        R.close()
         return
 
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
@@ -433,7 +548,7 @@ def main():
     achieved = alg_bytes / (avg_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                 "frac": achieved / hbm_peak, "traffic": traffic_for(name), "peak_source": peak_src,
-                "kernel": W.kernel_name(), "algorithmic_bytes_per_launch": alg_bytes,
+                "kernel": rec["kernel"], "algorithmic_bytes_per_launch": alg_bytes,
                 "avg_launch_ms": avg_ms}
     extra = {}
     if name in ("c1", "c2"):
@@ -441,19 +556,30 @@ def main():
         bits = W.value_bits()
         op_ns, op_cyc = pd.op_latency_ns(i.op, bits, local)
         hand_ns, _ = pd.chain_step_ns(i.op, bits, local) if (i.op, bits) != ("saturating-add", 32) else (None, None)
-        kname = W.kernel_name()
+        kname = rec["kernel"]
+        # north_star's dependency-chain bound: one output per step (a_k = 1),
+        # n - a_1 steps, each the measured latency of one dependent (x).  The
+        # chunked / jump paths regroup the recurrence algebraically, so they
+        # are not bound by it (frac > 1 = faster than any one-cell-per-step
+        # pipeline); their own critical path is reported next to it.
+        steps = i.n - i.a1
+        floor_ms = steps * op_ns / 1e6
+        extra["chain_roofline"] = {
+            "definition": "(n - a_1) dependent steps x latency of one dependent (x) (north_star)",
+            "steps": steps, "t_op_ns": op_ns, "t_op_cycles": op_cyc, "floor_ms": floor_ms,
+            "achieved_ms": avg_ms, "frac": floor_ms / avg_ms, "t_warp_handoff_ns": hand_ns,
+            "value_bits": bits}
         if kname.startswith("sdp_chunked"):
-            # chunked: the longest dependent chains are one chunk's cells and
-            # the chunk entry-state chain (G matrix-vector steps)
             import re
             m = re.search(r"L=(\d+),G=(\d+)", kname)
             L, G = (int(m.group(1)), int(m.group(2))) if m else (i.n - i.a1, 1)
-            steps = L + G
-            definition = ("sdp_chunked: one chunk (L cells) + G entry-state steps, "
-                          "each x latency of one dependent (x)")
-            # relaxation phase: one 4-byte shared-memory operand read per relaxation
+            extra["chain_roofline"]["critical_path"] = {
+                "definition": "sdp_chunked: one chunk (L cells) + G entry-state steps", "steps": L + G,
+                "floor_ms": (L + G) * op_ns / 1e6}
+            # the binding resource of the chunk batch: one 4-byte shared-memory
+            # operand read per relaxation at 128 B/cycle/SM
             sms = torch.cuda.get_device_properties(0).multi_processor_count
-            smem_gbs = sms * 128 * 1.965e9 / 1e9  # 128 B/cycle/SM at the max SM clock
+            smem_gbs = sms * 128 * 1.965e9 / 1e9
             relax_bytes = (i.n - i.a1) * i.k * 4
             extra["relaxation_roofline"] = {
                 "bound": "shared-memory bandwidth, one 4-byte operand read per relaxation",
@@ -461,42 +587,34 @@ def main():
                 "achieved_ms": avg_ms, "frac": relax_bytes / smem_gbs / 1e6 / avg_ms,
                 "chunks": G, "chunk_cells": L}
         elif kname == "sdp_jump":
-            # jump-ahead segments: the longest dependent chain is one 64-cell
-            # segment after its entry state (log2(segments) matrix levels)
             nseg = -(-(i.n - i.a1) // 64)
-            steps = 64 + max(1, (nseg - 1).bit_length())
-            definition = ("sdp_jump: 64-cell segment chain + log2(segments) entry-state levels, "
-                          "each x latency of one dependent (x)")
-        else:
-            steps = i.n - i.a1  # a_k = 1: one cell per step
-            definition = "(n - a_1) dependent steps x latency of one dependent (x) in a register chain"
-        floor_ms = steps * op_ns / 1e6
-        extra["chain_roofline"] = {
-            "definition": definition,
-            "steps": steps, "t_op_ns": op_ns, "t_op_cycles": op_cyc, "floor_ms": floor_ms,
-            "achieved_ms": avg_ms, "frac": floor_ms / avg_ms,
-            "t_warp_handoff_ns": hand_ns, "value_bits": bits}
+            cp = 64 + max(1, (nseg - 1).bit_length())
+            extra["chain_roofline"]["critical_path"] = {
+                "definition": "sdp_jump: 64-cell segment chain + log2(segments) entry-state levels",
+                "steps": cp, "floor_ms": cp * op_ns / 1e6}
     if name in ("c3", "c4"):
         n = W.inst.n
         extra["mcm_steps"] = {"cells": n * (n - 1) // 2, "ns_per_cell": avg_ms * 1e6 / (n * (n - 1) // 2),
                               "diagonals": n - 1, "us_per_diagonal": avg_ms * 1e3 / (n - 1)}
+    if companion:
+        extra["companion"] = companion
 
+    R.close()  # the CPU baseline below runs on rank 0 alone, after every collective
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         v, thr, kind, sample, _ = cpu_reference_sample(name, 1 if single else cores, 1)
         cpu = {"value": v, "unit": UNIT, "cores": thr, "kind": kind, "sample": sample}
 
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+    line = {"metric": METRIC, "value": rec["value"], "unit": UNIT, "n_gpus": world, "steps": K,
             "warmup": args.warmup, "ms_per_step": kernel_ms_max / K, "higher_is_better": True,
             "scaling": "weak" if single else "strong", "vs_baseline": None, "dtype": "int64",
             "data": "synthetic (the reference's seeded generators, generate.cpp:21-60)",
-            "config": config, "e2e": e2e, "gpu_launches": W.launches() * K,
-            "roofline": roofline, "cpu_baseline": cpu, "clocks": clk.summary(),
-            "kernel_value_bits": W.value_bits(), "parity": parity, "step_ms": step_ms, **extra}
+            "config": config, "e2e": rec["e2e"], "gpu_launches": rec["launches"],
+            "roofline": roofline, "cpu_baseline": cpu, "clocks": rec["clocks"],
+            "kernel_value_bits": rec["bits"], "parity": rec["parity"], "step_ms": rec["step_ms"],
+            "process_group": R.backend, **extra}
     print(json.dumps(line), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
 
 
 if __name__ == "__main__":

@@ -86,8 +86,9 @@ class BatchShard:
                                             False, spec.a1_cap)
             self.a1 = init.shape[1]
             self.h_offsets, self.h_init = offs, init
+            # an empty shard (world > total) has no plan: execute/digests skip it
             self.plan = SdpPlan(self.count, spec.n, spec.k, self.a1, offs.reshape(-1), init.reshape(-1),
-                                spec.op, device)
+                                spec.op, device) if self.count else None
             self.h_in = torch.from_numpy(init.reshape(-1)).pin_memory()
             self.d_in = torch.empty_like(self.h_in, device=self.dev)
             self.d_cells = torch.empty(self.count * spec.n, dtype=torch.int64, device=self.dev)
@@ -95,7 +96,7 @@ class BatchShard:
         else:
             dims = generate_mcm_batch(spec.n, spec.seed0 + self.lo, self.count, spec.dims_min, spec.dims_max)
             self.h_dims = dims
-            self.plan = McmPlan(self.count, spec.n, dims.reshape(-1), device=device)
+            self.plan = McmPlan(self.count, spec.n, dims.reshape(-1), device=device) if self.count else None
             size = self.count * spec.table_size()
             self.h_in = torch.from_numpy(dims.reshape(-1)).pin_memory()
             self.d_in = None

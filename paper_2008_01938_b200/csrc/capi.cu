@@ -795,27 +795,32 @@ struct pipedp_mcm_plan {
 namespace {
 
 int mcm_wave_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split, cudaStream_t st) {
-  const int64_t n = P->n;
-  CK(cudaMemsetAsync(P->d_done, 0, sizeof(int) * std::max<int64_t>(P->total_chunks, 1), st));
-  CK(cudaMemsetAsync(P->d_next, 0, sizeof(unsigned long long), st));
-  CK(cudaMemsetAsync(cells, 0, sizeof(int64_t) * (n + 1), st));
-  CK(cudaMemsetAsync(split, 0, sizeof(int64_t) * (n + 1), st));
-  McmWave W{n, P->total_chunks, P->d_chunk_base, P->d_done, P->d_next};
+  // one dataflow wavefront per instance (a batch runs them back to back on the
+  // stream; the done/next/value scratch is reset for each)
+  const int64_t n = P->n, cc = P->cc;
   int dev = 0, sms = 148;
   CK(cudaGetDevice(&dev));
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   const int threads = 256;
   int64_t grid = std::min<int64_t>((int64_t)sms * 8, (P->total_chunks + 7) / 8);
   grid = std::max<int64_t>(grid, 1);
-  if (bits == 32) {
-    CK(cudaMemsetAsync(P->d_v32, 0, sizeof(uint32_t) * (n + 1), st));
-    mcm_wavefront<uint32_t><<<(unsigned)grid, threads, 0, st>>>(W, P->d_p, P->d_v32, cells, split,
-                                                                 P->d_overflow);
-  } else {
-    mcm_wavefront<int64_t><<<(unsigned)grid, threads, 0, st>>>(W, P->d_p, cells, cells, split,
-                                                                P->d_overflow);
+  for (int64_t b = 0; b < P->batch; ++b) {
+    int64_t* cb = cells + b * (cc + 1);
+    int64_t* sb = split + b * (cc + 1);
+    const int32_t* pb = P->d_p + b * (n + 1);
+    CK(cudaMemsetAsync(P->d_done, 0, sizeof(int) * std::max<int64_t>(P->total_chunks, 1), st));
+    CK(cudaMemsetAsync(P->d_next, 0, sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(cb, 0, sizeof(int64_t) * (n + 1), st));
+    CK(cudaMemsetAsync(sb, 0, sizeof(int64_t) * (n + 1), st));
+    McmWave W{n, P->total_chunks, P->d_chunk_base, P->d_done, P->d_next};
+    if (bits == 32) {
+      CK(cudaMemsetAsync(P->d_v32, 0, sizeof(uint32_t) * (n + 1), st));
+      mcm_wavefront<uint32_t><<<(unsigned)grid, threads, 0, st>>>(W, pb, P->d_v32, cb, sb, P->d_overflow);
+    } else {
+      mcm_wavefront<int64_t><<<(unsigned)grid, threads, 0, st>>>(W, pb, cb, cb, sb, P->d_overflow);
+    }
+    CK(cudaGetLastError());
   }
-  CK(cudaGetLastError());
   return PIPEDP_OK;
 }
 
@@ -926,12 +931,13 @@ int mcm_execute(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t
   const bool square_pk = P->d.kernel == PIPEDP_MCM_SMEM && P->d.bits == 32 && P->n <= 64 &&
                          P->maxd3 < (1ll << 24) && env_int("PIPEDP_MCM_PACKED_SQUARE", 0) != 0;
   P->packed_now = (tiled_pk || square_pk) && env_int("PIPEDP_MCM_PACKED", 1) != 0;
+  int kernel = P->d.kernel;  // this execute's kernel (the plan itself is never changed)
   for (;;) {
     CK(cudaMemsetAsync(P->d_overflow, 0, sizeof(int), st));
-    if (P->d.kernel == PIPEDP_MCM_SMEM) TRY(mcm_smem_launch(P, bits, cells, split, st));
-    else if (P->d.kernel == PIPEDP_MCM_TILED && bits == 32) TRY(mcm_tiled_launch(P, cells, split, st));
+    if (kernel == PIPEDP_MCM_SMEM) TRY(mcm_smem_launch(P, bits, cells, split, st));
+    else if (kernel == PIPEDP_MCM_TILED && bits == 32) TRY(mcm_tiled_launch(P, cells, split, st));
     else TRY(mcm_wave_launch(P, bits, cells, split, st));
-    ++P->launches;
+    P->launches += kernel == PIPEDP_MCM_WAVEFRONT ? (int)P->batch : 1;
     P->last_bits = bits;
     if (bits == 64) return PIPEDP_OK;
     CK(cudaMemcpyAsync(P->h_overflow, P->d_overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
@@ -942,11 +948,9 @@ int mcm_execute(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t
       continue;
     }
     bits = 64;  // a value reached 2^30: redo exactly in 64-bit
-    if (P->d.kernel == PIPEDP_MCM_SMEM && P->d.smem64 > 227 * 1024) {
-      P->d.kernel = PIPEDP_MCM_WAVEFRONT;
-      if (P->batch > 1)
-        return fail(PIPEDP_ERR_UNSUPPORTED, "batched instance overflowed 32-bit and n too large for 64-bit smem");
-    }
+    // a 64-bit square/triangle table that no longer fits shared memory: the
+    // exact int64 wavefront, instance by instance
+    if (kernel == PIPEDP_MCM_SMEM && P->d.smem64 > 227 * 1024) kernel = PIPEDP_MCM_WAVEFRONT;
   }
 }
 
@@ -1368,7 +1372,9 @@ static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* 
       TRY(P->d.op == PIPEDP_OP_MAX ? sdp_chunked_run<kMax>(P, d_init, d_cells, W->stream, gs, W->armed)
                                    : sdp_chunked_run<kMin>(P, d_init, d_cells, W->stream, gs, W->armed));
       pipedp_host::parallel_prefault(cells_out, bytes);  // overlaps the kernels
-      const int64_t cut = P->a1 + gs * P->Lc;             // cells [0, cut) final at `armed`
+      // cells [0, cut) are final at `armed`; cut is even so both halves stay
+      // 16-byte aligned for narrow_i64_i32's int4 loads
+      const int64_t cut = (P->a1 + gs * P->Lc) & ~(int64_t)1;
       CK(cudaStreamWaitEvent(W->side, W->armed, 0));
       TRY(d2h_narrowed(W, 4, cells_out, d_cells, cut, W->side));
       TRY(d2h_narrowed(W, 5, cells_out + cut, d_cells + cut, P->n - cut, W->stream));

@@ -88,3 +88,73 @@ def test_sdp_batch_dominance_forms(gpu, oracle, op):
     for inst, t in zip(insts, gpu.solve_sequential_batch(insts)):
         want, _ = oracle.sdp_solve(inst.offsets, inst.init, inst.n, op)
         assert np.array_equal(t.cells, want)
+
+
+# --- BASELINE config 5 at full size: every instance against the reference ----
+# tests/golden/c5*_cells.npy / c5a_split.npy hold table_digest of all 65,536
+# instances, produced by the reference library itself (make_c5_digests.py).
+
+def _golden(name):
+    import os
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", name))
+
+
+def _full_batch_digests(spec, split=False):
+    st = torch.cuda.current_stream()
+    s = B.BatchShard(spec, 0, 1, 0)
+    s.upload(st)
+    s.execute(st)
+    cells = s.digests(st).cpu().numpy().view(np.uint64).copy()
+    sp = s.digests(st, split=True).cpu().numpy().view(np.uint64).copy() if split else None
+    torch.cuda.synchronize()
+    del s
+    torch.cuda.empty_cache()
+    return cells, sp
+
+
+def test_config5a_full_batch_bit_exact(gpu):
+    cells, split = _full_batch_digests(B.McmBatchSpec(), split=True)
+    want_c, want_s = _golden("c5a_cells.npy"), _golden("c5a_split.npy")
+    bad = np.nonzero(cells != want_c)[0]
+    assert bad.size == 0, f"{bad.size} C5a cell tables differ, first instance {bad[:8]}"
+    bad = np.nonzero(split != want_s)[0]
+    assert bad.size == 0, f"{bad.size} C5a split tables differ, first instance {bad[:8]}"
+
+
+def test_config5b_full_batch_bit_exact(gpu):
+    cells, _ = _full_batch_digests(B.SdpBatchSpec())
+    want = _golden("c5b_cells.npy")
+    bad = np.nonzero(cells != want)[0]
+    assert bad.size == 0, f"{bad.size} C5b tables differ, first instance {bad[:8]}"
+
+
+def test_config5b_sharded_full_batch(gpu):
+    # the strong-scaling shards of the bench (W = 8), solved one after another
+    spec = B.SdpBatchSpec()
+    want = _golden("c5b_cells.npy")
+    st = torch.cuda.current_stream()
+    for r in (0, 5, 7):
+        s = B.BatchShard(spec, r, 8, 0)
+        s.upload(st)
+        s.execute(st)
+        got = s.digests(st).cpu().numpy().view(np.uint64)
+        assert np.array_equal(got, want[s.lo:s.hi]), f"shard {r} of 8 differs"
+        del s
+        torch.cuda.empty_cache()
+
+
+def test_bench_two_ranks_share_one_gpu(gpu):
+    # bench.py --gpus 2 starts its own ranks (gloo when they share the GPU);
+    # the gathered digest list of the sharded C5b batch equals the reference's
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--workload", "c5b",
+                          "--steps", "1", "--warmup", "1", "--no-cpu-baseline", "--e2e-steps", "0"],
+                         capture_output=True, text=True, timeout=900, cwd=root)
+    assert out.returncode == 0, out.stderr[-3000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "shard2"
+    assert line["parity"]["match"] is True and line["parity"]["instances"] == 65536

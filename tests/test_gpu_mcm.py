@@ -137,3 +137,30 @@ def test_batch_packed_square_and_fallback(gpu, oracle, monkeypatch):
         for inst, (t, split) in zip(insts, gpu.solve_mcm_batch(insts)):
             wc, _, ws = oracle.mcm_solve(inst.dims)
             assert np.array_equal(t.cells, wc) and np.array_equal(split, ws)
+
+
+@pytest.mark.parametrize("n,lo,hi", [(330, 1, 100),     # 32-bit table too big for shared memory
+                                     (250, 1300, 2000),  # 64-bit values from the start
+                                     (300, 1000, 1290)])  # 32-bit square, overflows -> exact int64 rerun
+def test_batch_beyond_shared_memory(gpu, oracle, n, lo, hi):
+    # batches whose tables do not fit one CTA's shared memory run the dataflow
+    # wavefront instance by instance; every instance is checked
+    insts = [gpu.generate_mcm(n=n, seed=s, dims_min=lo, dims_max=hi) for s in (1, 2, 3)]
+    for inst, (t, split) in zip(insts, gpu.solve_mcm_batch(insts)):
+        wc, _, ws = oracle.mcm_solve(inst.dims)
+        assert np.array_equal(t.cells, wc) and np.array_equal(split, ws)
+    # the same plan executed twice keeps its dispatch (the overflow rerun must
+    # not rewrite the plan)
+    import torch
+    dims = np.concatenate([i.dims for i in insts])
+    plan = gpu.McmPlan(3, n, dims, device=0)
+    size = gpu.cell_count(n) + 1
+    for _ in range(2):
+        c = torch.full((3 * size,), -1, dtype=torch.int64, device="cuda")
+        s = torch.full((3 * size,), -1, dtype=torch.int64, device="cuda")
+        plan.execute(c.data_ptr(), s.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        c, s = c.cpu().numpy(), s.cpu().numpy()
+        for b, inst in enumerate(insts):
+            wc, _, ws = oracle.mcm_solve(inst.dims)
+            assert np.array_equal(c[b * size:(b + 1) * size], wc)
+            assert np.array_equal(s[b * size:(b + 1) * size], ws)

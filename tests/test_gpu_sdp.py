@@ -320,3 +320,23 @@ def test_chunked_int64_values(gpu, oracle, op):
     plan.close()
     assert name.startswith("sdp_chunked") and bits == 64
     _check(gpu, oracle, offs, init, n, op)
+
+
+def test_config2_full_table_digest(gpu):
+    # BASELINE config 2 at full size (n = 2^24, k = 1024, a_1 = 4096, min,
+    # seed 1): the whole 128 MiB table against the reference's table_digest,
+    # through the drop-in call (host buffers) and the device-resident plan
+    import json
+    import os
+    import torch
+    g = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))["configs"]["c2"]
+    inst = gpu.generate_sdp(n=1 << 24, k=1024, op="min", seed=1, a1_cap=4096)
+    t = gpu.solve_sequential(inst)
+    assert f"{gpu.table_digest(t.cells):016x}" == g["digest"] and int(t.cells[-1]) == g["last"]
+    plan = gpu.SdpPlan(1, inst.n, inst.k, inst.a1, inst.offsets, inst.init, inst.op, 0)
+    d_init = torch.tensor(inst.init, dtype=torch.int64, device="cuda")
+    d_cells = torch.empty(inst.n, dtype=torch.int64, device="cuda")
+    for _ in range(2):  # plan reuse
+        d_cells.fill_(-1)
+        plan.execute(d_init.data_ptr(), d_cells.data_ptr(), torch.cuda.current_stream().cuda_stream)
+        assert f"{gpu.table_digest(d_cells.cpu().numpy()):016x}" == g["digest"]

@@ -216,3 +216,20 @@ def test_ref_apply_random(oracle, ref):
     for op in OPS:
         for a, b in zip(xs, np.roll(xs, 17)):
             assert oracle.apply(op, int(a), int(b)) == ref.apply(op, int(a), int(b))
+
+
+def test_c5_golden_digest_lists(oracle):
+    # tests/golden/c5*.npy (all 65,536 instances, written by the reference via
+    # make_c5_digests.py) agree with the C restatement on a spread sample
+    import os
+    here = os.path.join(os.path.dirname(__file__), "golden")
+    c5a_c = np.load(os.path.join(here, "c5a_cells.npy"))
+    c5a_s = np.load(os.path.join(here, "c5a_split.npy"))
+    c5b = np.load(os.path.join(here, "c5b_cells.npy"))
+    assert c5a_c.shape == c5a_s.shape == c5b.shape == (65536,) and c5b.dtype == np.uint64
+    for i in (0, 1, 2, 777, 40000, 65535):
+        c, _, s = oracle.mcm_solve(oracle.generate_mcm(64, i, 1, 100))
+        assert oracle.digest(c) == int(c5a_c[i]) and oracle.digest(s) == int(c5a_s[i])
+    for i in (0, 9, 65535):
+        offs, init = oracle.generate_sdp(1 << 16, 64, i, False, 0)
+        assert oracle.digest(oracle.sdp_solve(offs, init, 1 << 16, "min")[0]) == int(c5b[i])
