@@ -5,6 +5,8 @@
 #pragma once
 
 #include <cstdint>
+#include <optional>
+#include <vector>
 
 #include "pipedp/analysis.hpp"
 #include "pipedp/engine.hpp"
@@ -30,6 +32,23 @@ struct McmPipelineResult {
 
 McmPipelineResult solve_mcm_pipeline(const McmInstance& instance,
                                      const McmScheduleConfig& config = {});
+
+// Lemma 1/2 check on a trace (reference mcm_pipeline.hpp:115-126): substep-1
+// reads, substep-2 reads and substep-4 writes touch distinct addresses across
+// lanes at every head.  Declared for the reference's verify_mcm; the body is
+// the reference's trace tool (mcm_pipeline.cpp:49-77), provided by the drop-in.
+struct DistinctnessVerdict {
+  bool substep1_reads_distinct = true;
+  bool substep2_reads_distinct = true;
+  bool substep4_writes_distinct = true;
+  std::optional<ConflictGroup> counterexample;
+
+  bool all_ok() const {
+    return substep1_reads_distinct && substep2_reads_distinct && substep4_writes_distinct;
+  }
+};
+
+DistinctnessVerdict verify_substep_distinctness(const PipelineTrace& trace);
 
 /// Addresses of cells predicted to read a not-yet-final operand under the
 /// paper-literal schedule (reference mcm_pipeline.hpp:128-131): cell (r,c) on

@@ -151,6 +151,51 @@ int32_t pipedp_mcm_solve(const int64_t* dims, int64_t dims_len, int32_t kernel,
 int32_t pipedp_mcm_pipeline(const int64_t* dims, int64_t dims_len, int32_t mode,
                             int64_t* cells_out, uint8_t* filled_out, int64_t* steps_out,
                             int64_t* stall_iterations_out);
+/* ---- lock-step engine with device-side trace analyses -------------------
+ * The reference engine (engine.hpp:134-433) running McmProgram
+ * (mcm_pipeline.hpp:22-84) or SdpProgram (sdp_pipeline.hpp:16-58) on the GPU,
+ * iteration for iteration.  flags: PIPEDP_ENGINE_TRACE collects the access
+ * records (PipelineTrace::records, canonical record_less order);
+ * PIPEDP_ENGINE_ANALYSIS computes, on the device while the schedule runs,
+ * the conflict groups of detect_conflicts (analysis.cpp:31-70) and the hazard
+ * records of detect_hazards (analysis.cpp:72-103) without materialising the
+ * trace.  The run handle owns the results until pipedp_engine_free. */
+enum { PIPEDP_ENGINE_TRACE = 1, PIPEDP_ENGINE_ANALYSIS = 2 };
+typedef struct pipedp_engine_run* pipedp_engine_t;
+typedef struct {
+  int64_t first_head;        /* head_range().first */
+  int64_t steps_executed;    /* iterations, stalls included */
+  int64_t stall_iterations;  /* steps_executed - head count */
+  int64_t records;           /* access records (TRACE) */
+  int64_t hazards;           /* hazard records (ANALYSIS) */
+  int64_t conflict_groups;   /* conflict groups (ANALYSIS) */
+  int64_t conflict_lanes;    /* lanes over all groups */
+  int64_t max_group_size;    /* ConflictReport::max_group_size (1 if none) */
+  int64_t stall_heads;       /* PipelineTrace::stall_heads entries */
+} pipedp_engine_summary;
+/* mode: PIPEDP_MCM_PAPER_LITERAL / PIPEDP_MCM_STALL_ON_HAZARD; cells_out
+ * (nullable) cell_count(n)+1 entries */
+int32_t pipedp_mcm_engine(const int64_t* dims, int64_t dims_len, int32_t mode, int32_t flags,
+                          int64_t* cells_out, pipedp_engine_summary* summary, pipedp_engine_t* run_out);
+/* SdpProgram has no stall mode in the reference (lock-step only); cells_out
+ * (nullable) n entries */
+int32_t pipedp_sdp_engine(const int64_t* offsets, int64_t k, const int64_t* init, int64_t init_len,
+                          int64_t n, int32_t op, int32_t flags, int64_t* cells_out,
+                          pipedp_engine_summary* summary, pipedp_engine_t* run_out);
+/* records in record_less order: head, substep, lane, kind (0 read, 1 write), address */
+int32_t pipedp_engine_records(pipedp_engine_t run, int64_t* head, int32_t* substep, int32_t* lane,
+                              int32_t* kind, int64_t* address);
+/* hazards [hazards][6]: head, substep, lane, address, finalization head, finalization substep,
+ * sorted as detect_hazards sorts them */
+int32_t pipedp_engine_hazards(pipedp_engine_t run, int64_t* out);
+/* conflicts: groups [conflict_groups][4] head, substep, kind, address (detect_conflicts order);
+ * group_sizes [conflict_groups]; lanes [conflict_lanes] concatenated, ascending per group;
+ * per_step_cost [steps_executed] */
+int32_t pipedp_engine_conflicts(pipedp_engine_t run, int64_t* groups, int32_t* group_sizes, int32_t* lanes,
+                                int32_t* per_step_cost);
+int32_t pipedp_engine_stall_heads(pipedp_engine_t run, int64_t* out);
+void pipedp_engine_free(pipedp_engine_t run);
+
 /* solve_mcm_bruteforce (mcm.cpp:130-138): the reference's independent oracle
  * (enumeration of every parenthesisation, n <= 12, else TooLargeForBruteForce),
  * run on the device. */

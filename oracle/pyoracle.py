@@ -236,6 +236,22 @@ class OracleRef(_Lib):
                                          _p64(init), len(init), C.byref(a1)))
         return offs, init[: a1.value].copy()
 
+    def mcm_engine_digests(self, dims, mode: int):
+        """ref_mcm_engine_digests: trace/report digest vector of solve_mcm_pipeline."""
+        d = np.ascontiguousarray(dims, dtype=np.int64)
+        out = np.zeros(14, dtype=np.uint64)
+        _check(self.lib.ref_mcm_engine_digests(_p64(d), len(d), mode, out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return [int(x) for x in out]
+
+    def sdp_engine_digests(self, offsets, init, n, op):
+        """ref_sdp_engine_digests: trace/report digest vector of solve_sdp_pipeline."""
+        offs = np.ascontiguousarray(offsets, dtype=np.int64)
+        ini = np.ascontiguousarray(init, dtype=np.int64)
+        out = np.zeros(14, dtype=np.uint64)
+        _check(self.lib.ref_sdp_engine_digests(_p64(offs), len(offs), _p64(ini), len(ini), n, OPS.get(op, op),
+                                               out.ctypes.data_as(C.POINTER(C.c_uint64))))
+        return [int(x) for x in out]
+
     def hazard_frontier(self, n):
         out = np.zeros(n * n, dtype=np.int64)
         cnt = int(self.lib.ref_hazard_frontier(n, _p64(out), len(out)))

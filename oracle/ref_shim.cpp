@@ -126,6 +126,68 @@ int ref_mcm_pipeline(const int64_t* dims, int64_t len, int mode, int collect_tra
   });
 }
 
+// Digest vector of one lock-step engine run with collect_trace (the trace and
+// the reports of analysis.cpp), for the GPU engine's parity tests:
+//  [0] steps [1] stalls [2] first_head [3] records [4] D(records: head, substep,
+//  lane, kind, address) [5] max_group_size [6] groups [7] D(groups: head,
+//  substep, kind, address, size, lanes...) [8] D(per_step_cost) [9] hazards
+//  [10] D(hazards: 6 fields) [11] stall heads [12] D(stall heads) [13] D(cells)
+// D = table_digest of the flattened int64 sequence.
+namespace {
+uint64_t dig(const std::vector<int64_t>& v) {
+  SolutionTable t;
+  t.cells = v;
+  t.filled.assign(v.size(), 1);
+  return table_digest(t);
+}
+void engine_digests(const SolutionTable& table, const PipelineTrace& tr, const ConflictReport& cr,
+                    const HazardReport* hz, uint64_t* out) {
+  std::vector<int64_t> v;
+  for (const AccessRecord& a : tr.records)
+    v.insert(v.end(), {a.head, a.substep, a.lane, static_cast<int64_t>(a.kind), a.address});
+  out[0] = tr.steps_executed;
+  out[1] = tr.stall_iterations;
+  out[2] = tr.first_head;
+  out[3] = tr.records.size();
+  out[4] = dig(v);
+  v.clear();
+  for (const ConflictGroup& g : cr.groups) {
+    v.insert(v.end(), {g.head, g.substep, static_cast<int64_t>(g.kind), g.address, (int64_t)g.lanes.size()});
+    for (int l : g.lanes) v.push_back(l);
+  }
+  out[5] = cr.max_group_size;
+  out[6] = cr.groups.size();
+  out[7] = dig(v);
+  out[8] = dig(std::vector<int64_t>(cr.per_step_cost.begin(), cr.per_step_cost.end()));
+  v.clear();
+  if (hz)
+    for (const HazardRecord& h : hz->hazards)
+      v.insert(v.end(), {h.head, h.substep, h.lane, h.address, h.finalization_head, h.finalization_substep});
+  out[9] = hz ? hz->hazards.size() : 0;
+  out[10] = dig(v);
+  out[11] = tr.stall_heads.size();
+  out[12] = dig(tr.stall_heads);
+  out[13] = dig(table.cells);
+}
+}  // namespace
+
+int ref_mcm_engine_digests(const int64_t* dims, int64_t len, int mode, uint64_t* out) {
+  return guard([&] {
+    McmScheduleConfig cfg;
+    cfg.mode = mode == 1 ? McmMode::stall_on_hazard : McmMode::paper_literal;
+    McmPipelineResult r = solve_mcm_pipeline(make_mcm(dims, len), cfg);
+    engine_digests(r.table, r.trace, r.conflicts, &r.hazards, out);
+  });
+}
+
+int ref_sdp_engine_digests(const int64_t* offs, int64_t k, const int64_t* init, int64_t init_len, int64_t n,
+                           int op, uint64_t* out) {
+  return guard([&] {
+    SdpPipelineResult r = solve_sdp_pipeline(make_sdp(offs, k, init, init_len, n, op), SdpRunConfig{});
+    engine_digests(r.table, r.trace, r.conflicts, nullptr, out);
+  });
+}
+
 int64_t ref_mcm_bruteforce(const int64_t* dims, int64_t len) {
   int64_t out = 0;
   const int rc = guard([&] { out = solve_mcm_bruteforce(make_mcm(dims, len)); });

@@ -53,8 +53,18 @@ EXPORTS = (
     "pipedp_mcm_plan_destroy", "pipedp_digest_device", "pipedp_chain_step_ns",
     "pipedp_profile_read", "pipedp_generate_sdp_batch", "pipedp_generate_mcm_batch",
     "pipedp_op_latency_ns", "pipedp_mcm_bruteforce", "pipedp_sdp_solve_method",
-    "pipedp_sdp_plan_set_method",
+    "pipedp_sdp_plan_set_method", "pipedp_mcm_engine", "pipedp_sdp_engine", "pipedp_engine_records",
+    "pipedp_engine_hazards", "pipedp_engine_conflicts", "pipedp_engine_stall_heads", "pipedp_engine_free",
 )
+ENGINE_TRACE, ENGINE_ANALYSIS = 1, 2
+TRACE_LIMIT = 1 << 28  # engine.cu kMaxRecords
+
+
+class EngineSummary(C.Structure):
+    """pipedp_engine_summary (include/pipedp_cuda.h)."""
+    _fields_ = [(f, C.c_int64) for f in ("first_head", "steps_executed", "stall_iterations", "records",
+                                         "hazards", "conflict_groups", "conflict_lanes", "max_group_size",
+                                         "stall_heads")]
 
 
 class Error(RuntimeError):
@@ -131,6 +141,17 @@ def lib():
     L.pipedp_sdp_solve_method.argtypes = [_i64p, C.c_int64, _i64p, C.c_int64, C.c_int64, C.c_int32,
                                           C.c_int32, _i64p, _u8p]
     L.pipedp_sdp_plan_set_method.argtypes = [C.c_void_p, C.c_int32]
+    _i32p = C.POINTER(C.c_int32)
+    L.pipedp_mcm_engine.argtypes = [_i64p, C.c_int64, C.c_int32, C.c_int32, _i64p, C.POINTER(EngineSummary),
+                                    C.POINTER(C.c_void_p)]
+    L.pipedp_sdp_engine.argtypes = [_i64p, C.c_int64, _i64p, C.c_int64, C.c_int64, C.c_int32, C.c_int32, _i64p,
+                                    C.POINTER(EngineSummary), C.POINTER(C.c_void_p)]
+    L.pipedp_engine_records.argtypes = [C.c_void_p, _i64p, _i32p, _i32p, _i32p, _i64p]
+    L.pipedp_engine_hazards.argtypes = [C.c_void_p, _i64p]
+    L.pipedp_engine_conflicts.argtypes = [C.c_void_p, _i64p, _i32p, _i32p, _i32p]
+    L.pipedp_engine_stall_heads.argtypes = [C.c_void_p, _i64p]
+    L.pipedp_engine_free.argtypes = [C.c_void_p]
+    L.pipedp_engine_free.restype = None
     _lib = L
     return L
 
@@ -209,27 +230,109 @@ class SolutionTable:
                 and np.array_equal(self.filled, other.filled))
 
 
+RECORD_DTYPE = np.dtype([("head", np.int64), ("substep", np.int32), ("lane", np.int32), ("kind", np.int32),
+                         ("address", np.int64)])
+HAZARD_DTYPE = np.dtype([("head", np.int64), ("substep", np.int64), ("lane", np.int64), ("address", np.int64),
+                         ("finalization_head", np.int64), ("finalization_substep", np.int64)])
+
+
 @dataclass
 class PipelineTrace:
-    """PipelineTrace (engine.hpp:68-77); the GPU solvers collect no records."""
+    """PipelineTrace (engine.hpp:68-77).  records: RECORD_DTYPE array in
+    record_less order (kind 0 read, 1 write), emitted by the GPU lock-step
+    engine when collected."""
 
     first_head: int = 0
     steps_executed: int = 0
     stall_iterations: int = 0
-    records: list = field(default_factory=list)
+    records: np.ndarray = field(default_factory=lambda: np.zeros(0, RECORD_DTYPE))
     collected: bool = False
+    stall_heads: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))
+
+
+@dataclass
+class ConflictGroup:
+    head: int
+    substep: int
+    kind: int
+    address: int
+    lanes: list
+
+
+@dataclass
+class ConflictReport:
+    """ConflictReport (analysis.hpp:23-34), computed on the device."""
+
+    groups: list = field(default_factory=list)
+    max_group_size: int = 1
+    first_head: int = 0
+    per_step_cost: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
+
+
+@dataclass
+class HazardReport:
+    """HazardReport (analysis.hpp:54-58): HAZARD_DTYPE records, detect_hazards order."""
+
+    hazards: np.ndarray = field(default_factory=lambda: np.zeros(0, HAZARD_DTYPE))
+
+    def empty(self) -> bool:
+        return len(self.hazards) == 0
 
 
 @dataclass
 class SdpPipelineResult:
     table: SolutionTable
     trace: PipelineTrace
+    conflicts: ConflictReport = field(default_factory=ConflictReport)
 
 
 @dataclass
 class McmPipelineResult:
     table: SolutionTable
     trace: PipelineTrace
+    conflicts: ConflictReport = field(default_factory=ConflictReport)
+    hazards: HazardReport = field(default_factory=HazardReport)
+
+
+def _engine_results(run, summ: "EngineSummary", collected: bool, analysis: bool):
+    """Copy one pipedp_*_engine run's results into the reference's result types."""
+    L = lib()
+    try:
+        tr = PipelineTrace(summ.first_head, summ.steps_executed, summ.stall_iterations, collected=collected)
+        tr.stall_heads = np.zeros(summ.stall_heads, np.int64)
+        _check(L.pipedp_engine_stall_heads(run, _p(tr.stall_heads)))
+        nr = summ.records
+        if nr:
+            rec = np.zeros(nr, RECORD_DTYPE)
+            cols = {f: np.zeros(nr, RECORD_DTYPE[f]) for f in RECORD_DTYPE.names}
+            i32 = C.POINTER(C.c_int32)
+            _check(L.pipedp_engine_records(run, _p(cols["head"]), _p(cols["substep"], i32), _p(cols["lane"], i32),
+                                           _p(cols["kind"], i32), _p(cols["address"])))
+            for f in RECORD_DTYPE.names:
+                rec[f] = cols[f]
+            tr.records = rec
+        conf, haz = ConflictReport(first_head=summ.first_head), HazardReport()
+        if analysis:
+            g = summ.conflict_groups
+            groups = np.zeros(4 * g, np.int64)
+            sizes = np.zeros(g, np.int32)
+            lanes = np.zeros(summ.conflict_lanes, np.int32)
+            conf.per_step_cost = np.zeros(max(summ.steps_executed, 0), np.int32)
+            i32 = C.POINTER(C.c_int32)
+            _check(L.pipedp_engine_conflicts(run, _p(groups), _p(sizes, i32), _p(lanes, i32),
+                                             _p(conf.per_step_cost, i32)))
+            at = 0
+            for i in range(g):
+                h, sub, kind, addr = (int(x) for x in groups[4 * i:4 * i + 4])
+                conf.groups.append(ConflictGroup(h, sub, kind, addr, [int(x) for x in lanes[at:at + sizes[i]]]))
+                at += int(sizes[i])
+            conf.max_group_size = int(summ.max_group_size)
+            hz = np.zeros(summ.hazards * 6, np.int64)
+            _check(L.pipedp_engine_hazards(run, _p(hz)))
+            haz.hazards = hz.view(HAZARD_DTYPE).copy() if summ.hazards else np.zeros(0, HAZARD_DTYPE)
+        return tr, conf, haz
+    finally:
+        L.pipedp_engine_free(run)
 
 
 @dataclass
@@ -308,9 +411,24 @@ def solve_naive_parallel(inst: SdpInstance) -> NaiveParallelResult:
     return NaiveParallelResult(t, inst.k - 1, (inst.n - inst.a1) * inst.k)
 
 
-def solve_sdp_pipeline(inst: SdpInstance, config=None) -> SdpPipelineResult:
-    t = solve_sequential(inst)
-    return SdpPipelineResult(t, PipelineTrace(inst.a1, inst.n + inst.k - inst.a1 - 1, 0))
+def solve_sdp_pipeline(inst: SdpInstance, collect_trace: bool = True) -> SdpPipelineResult:
+    """solve_sdp_pipeline (sdp_pipeline.cpp:34-44; SdpRunConfig default
+    collect_trace = true).  With collect_trace the GPU lock-step engine runs
+    SdpProgram and returns the trace records (when within TRACE_LIMIT) and the
+    conflict report computed on the device; otherwise the fast solvers."""
+    validate(inst)
+    if not collect_trace:
+        t = solve_sequential(inst)
+        return SdpPipelineResult(t, PipelineTrace(inst.a1, inst.n + inst.k - inst.a1 - 1, 0))
+    fits = (inst.n - inst.a1) * (3 * inst.k - 1) <= TRACE_LIMIT
+    offs, init = _a64(inst.offsets), _a64(inst.init)
+    cells = np.empty(inst.n, np.int64)
+    summ, run = EngineSummary(), C.c_void_p()
+    _check(lib().pipedp_sdp_engine(_p(offs), len(offs), _p(init), len(init), inst.n, _op_index(inst.op),
+                                   ENGINE_ANALYSIS | (ENGINE_TRACE if fits else 0), _p(cells), C.byref(summ),
+                                   C.byref(run)))
+    tr, conf, _ = _engine_results(run, summ, fits, True)
+    return SdpPipelineResult(SolutionTable(cells, np.ones(inst.n, np.uint8)), tr, conf)
 
 
 def solve_sequential_batch(insts: List[SdpInstance], device: int = -1) -> List[SolutionTable]:
@@ -417,21 +535,25 @@ def solve_mcm_bruteforce(inst: McmInstance) -> int:
     return out.value
 
 
-def solve_mcm_pipeline(inst: McmInstance, mode: str = PAPER_LITERAL) -> McmPipelineResult:
-    """solve_mcm_pipeline (mcm_pipeline.cpp:32-47): exact lock-step engine semantics."""
+def solve_mcm_pipeline(inst: McmInstance, mode: str = PAPER_LITERAL, collect_trace: bool = True) -> McmPipelineResult:
+    """solve_mcm_pipeline (mcm_pipeline.cpp:32-47; McmScheduleConfig default
+    collect_trace = true): the GPU lock-step engine running McmProgram -- table,
+    steps, stalls, stall heads; with collect_trace the access records (within
+    TRACE_LIMIT) and the conflict and hazard reports computed on the device."""
     d = _a64(inst.dims)
     validate(inst)
     if inst.n < 2:
         raise Error(11, "InvalidParams: pipeline needs at least two matrices")
     m = {PAPER_LITERAL: 0, STALL_ON_HAZARD: 1}[mode]
-    size = cell_count(inst.n) + 1
+    n = inst.n
+    size = cell_count(n) + 1
+    fits = 4 * ((n ** 3 - n) // 6) - (size - 1 - n) <= TRACE_LIMIT
+    flags = (ENGINE_ANALYSIS | (ENGINE_TRACE if fits else 0)) if collect_trace else 0
     cells = np.empty(size, dtype=np.int64)
-    filled = np.empty(size, dtype=np.uint8)
-    steps, stall = C.c_int64(), C.c_int64()
-    _check(lib().pipedp_mcm_pipeline(_p(d), len(d), m, _p(cells), _p(filled, _u8p),
-                                     C.byref(steps), C.byref(stall)))
-    return McmPipelineResult(SolutionTable(cells, filled),
-                             PipelineTrace(inst.n + 1, steps.value, stall.value))
+    summ, run = EngineSummary(), C.c_void_p()
+    _check(lib().pipedp_mcm_engine(_p(d), len(d), m, flags, _p(cells), C.byref(summ), C.byref(run)))
+    tr, conf, haz = _engine_results(run, summ, collect_trace and fits, collect_trace)
+    return McmPipelineResult(SolutionTable(cells, np.ones(size, np.uint8)), tr, conf, haz)
 
 
 def solve_mcm_batch(insts: List[McmInstance], device: int = -1):

@@ -60,12 +60,24 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
     cuda_srcs = _sources(CSRC, (".cu", ".cuh", ".inc", ".hpp")) + [os.path.join(INCLUDE, "pipedp_cuda.h")]
     target = PROF_SO if profile else CUDA_SO
     if force or _newer(target, cuda_srcs):
-        cmd = [nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
-               "-Xptxas", "-v" if verbose else "-O3",
-               "-Xcompiler", "-fPIC,-O3", "-shared", "-cudart", "static",
-               *(["-DPIPEDP_PROFILE"] if profile else []),
-               "-I", INCLUDE, os.path.join(CSRC, "capi.cu"), "-o", target + ".tmp"]
-        _run(cmd, verbose)
+        # one object per top-level translation unit, compiled in parallel, then
+        # one shared library (CUDA runtime linked statically)
+        tus = [os.path.join(CSRC, f) for f in ("capi.cu", "engine.cu")]
+        flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
+                 "-Xptxas", "-v" if verbose else "-O3", "-Xcompiler", "-fPIC,-O3",
+                 *(["-DPIPEDP_PROFILE"] if profile else []), "-I", INCLUDE]
+        objdir = os.path.join(LIB, "obj_prof" if profile else "obj")
+        os.makedirs(objdir, exist_ok=True)
+        objs = [os.path.join(objdir, os.path.basename(t) + ".o") for t in tus]
+        procs = [(subprocess.Popen([nvcc, *flags, "-c", t, "-o", o], stdout=subprocess.PIPE,
+                                   stderr=subprocess.STDOUT, text=True), t) for t, o in zip(tus, objs)]
+        for p, t in procs:
+            out = p.communicate()[0]
+            if verbose or p.returncode:
+                sys.stdout.write(out)
+            if p.returncode:
+                raise RuntimeError(f"build failed: nvcc -c {os.path.basename(t)}")
+        _run([nvcc, *ARCH, "-shared", "-cudart", "static", *objs, "-o", target + ".tmp"], verbose)
         os.replace(target + ".tmp", target)
     if profile:
         return

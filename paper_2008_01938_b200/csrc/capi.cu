@@ -29,158 +29,11 @@
 
 using namespace pipedp_dev;
 
+#include "capi_util.hpp"
+
+using namespace pipedp_capi;
+
 namespace {
-
-// ---------------------------------------------------------------- errors ---
-thread_local std::string g_last_error;
-
-const char* errc_name(int code) {  // semigroup.cpp:73-99, indexed by errc + 1
-  static const char* names[] = {"",
-                                "NonDecreasingOffsets",
-                                "NonPositiveOffset",
-                                "InitLengthMismatch",
-                                "TableTooSmall",
-                                "CoordOutOfRange",
-                                "AddressOutOfRange",
-                                "BaseCellHasNoDeps",
-                                "TooLargeForBruteForce",
-                                "StallLivelock",
-                                "WeightOverflow",
-                                "InvalidParams"};
-  if (code >= 1 && code <= 11) return names[code];
-  switch (code) {
-    case PIPEDP_ERR_CUDA: return "CudaError";
-    case PIPEDP_ERR_NO_DEVICE: return "NoDevice";
-    case PIPEDP_ERR_OUT_OF_MEMORY: return "OutOfMemory";
-    case PIPEDP_ERR_UNSUPPORTED: return "Unsupported";
-  }
-  return "UnknownError";
-}
-
-int fail(int code, const char* fmt, ...) {
-  char buf[512];
-  va_list ap;
-  va_start(ap, fmt);
-  vsnprintf(buf, sizeof buf, fmt, ap);
-  va_end(ap);
-  g_last_error = std::string(errc_name(code)) + ": " + buf;
-  return code;
-}
-
-int cuda_fail(cudaError_t e, const char* what) {
-  (void)cudaGetLastError();
-  return fail(e == cudaErrorMemoryAllocation ? PIPEDP_ERR_OUT_OF_MEMORY : PIPEDP_ERR_CUDA,
-              "%s: %s", what, cudaGetErrorString(e));
-}
-
-#define CK(expr)                                      \
-  do {                                                \
-    cudaError_t _e = (expr);                          \
-    if (_e != cudaSuccess) return cuda_fail(_e, #expr); \
-  } while (0)
-
-// ------------------------------------------------------------ validation ---
-// sdp.cpp:10-32, in the reference's order.
-int validate_sdp(const int64_t* offs, int64_t k, int64_t init_len, int64_t n) {
-  if (k <= 0 || offs == nullptr) return fail(PIPEDP_E_INVALID_PARAMS, "offset set must be nonempty");
-  for (int64_t i = 0; i < k; ++i) {
-    if (offs[i] <= 0)
-      return fail(PIPEDP_E_NON_POSITIVE_OFFSET, "offset a_%lld is not positive", (long long)(i + 1));
-    if (i > 0 && offs[i - 1] <= offs[i])
-      return fail(PIPEDP_E_NON_DECREASING_OFFSETS,
-                  "offsets must strictly decrease, violated at position %lld", (long long)(i + 1));
-  }
-  if (init_len != offs[0])
-    return fail(PIPEDP_E_INIT_LENGTH_MISMATCH, "expected a_1=%lld initial values, got %lld",
-                (long long)offs[0], (long long)init_len);
-  if (n <= offs[0])
-    return fail(PIPEDP_E_TABLE_TOO_SMALL, "n=%lld leaves nothing to compute past the preset prefix",
-                (long long)n);
-  return PIPEDP_OK;
-}
-
-// mcm.cpp:11-28.  The overflow product is evaluated like the reference's
-// signed left-to-right expression compiles on gcc/x86-64 (two's-complement
-// wrap), so the accepted set is identical.
-int validate_mcm(const int64_t* dims, int64_t len) {
-  if (len < 2 || dims == nullptr)
-    return fail(PIPEDP_E_INVALID_PARAMS, "dimension vector needs at least two entries");
-  int64_t max_dim = 1;
-  for (int64_t i = 0; i < len; ++i) {
-    if (dims[i] < 1) return fail(PIPEDP_E_INVALID_PARAMS, "matrix dimensions must be >= 1");
-    max_dim = std::max(max_dim, dims[i]);
-  }
-  const int64_t n = len - 1;
-  uint64_t p = (uint64_t)n * (uint64_t)max_dim;
-  p *= (uint64_t)max_dim;
-  p *= (uint64_t)max_dim;
-  if (max_dim > 1000000 || (int64_t)p > ((int64_t)1 << 61))
-    return fail(PIPEDP_E_WEIGHT_OVERFLOW, "dimension products too large for 64-bit cost accumulation");
-  return PIPEDP_OK;
-}
-
-// ------------------------------------------------------------- devices ---
-int usable_devices() {
-  int count = 0;
-  if (cudaGetDeviceCount(&count) != cudaSuccess) {
-    (void)cudaGetLastError();
-    return 0;
-  }
-  int usable = 0;
-  for (int d = 0; d < count; ++d) {
-    int major = 0;
-    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, d) == cudaSuccess && major == 10) ++usable;
-  }
-  return usable;
-}
-
-int select_device(int32_t device) {
-  int count = 0;
-  if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
-    (void)cudaGetLastError();
-    return fail(PIPEDP_ERR_NO_DEVICE, "no CUDA device visible (the solvers have no CPU path)");
-  }
-  int dev = device;
-  if (dev < 0) CK(cudaGetDevice(&dev));
-  if (dev >= count) return fail(PIPEDP_ERR_NO_DEVICE, "device %d not present (%d visible)", dev, count);
-  int major = 0, minor = 0;  // attribute queries: cudaGetDeviceProperties costs milliseconds
-  CK(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev));
-  CK(cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev));
-  if (major != 10)
-    return fail(PIPEDP_ERR_NO_DEVICE, "device %d is sm_%d%d; these kernels are built for sm_100a", dev,
-                major, minor);
-  CK(cudaSetDevice(dev));
-  return PIPEDP_OK;
-}
-
-// A per-call stream and a tiny RAII set of device buffers.
-struct Scope {
-  cudaStream_t stream = nullptr;
-  std::vector<void*> bufs;
-  ~Scope() {
-    if (stream) cudaStreamSynchronize(stream);
-    for (void* p : bufs) cudaFree(p);
-    if (stream) cudaStreamDestroy(stream);
-  }
-  int init() {
-    CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
-    return PIPEDP_OK;
-  }
-  template <typename T>
-  int alloc(T** p, size_t count) {
-    void* q = nullptr;
-    CK(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T)));
-    bufs.push_back(q);
-    *p = static_cast<T*>(q);
-    return PIPEDP_OK;
-  }
-};
-
-#define TRY(expr)                  \
-  do {                             \
-    int _rc = (expr);              \
-    if (_rc != PIPEDP_OK) return _rc; \
-  } while (0)
 
 int ceil_log2(uint64_t v) {
   int r = 0;
@@ -1729,6 +1582,7 @@ static int32_t mcm_solve_host(int64_t batch, int64_t n, const int64_t* dims, int
   for (int64_t b = 0; b < batch; ++b) TRY(validate_mcm(dims + b * (n + 1), n + 1));
   McmDispatch d{};
   TRY(plan_mcm(batch, n, dims, kernel, &d));
+  TRY(select_device(device));  // NoDevice without a GPU: there is no CPU path
   int dev = device;
   if (dev < 0) CK(cudaGetDevice(&dev));
   pipedp_mcm_plan_t P = nullptr;
@@ -1788,53 +1642,6 @@ int32_t pipedp_mcm_solve(const int64_t* dims, int64_t dims_len, int32_t kernel,
 int32_t pipedp_mcm_solve_batch(int64_t batch, int64_t n, const int64_t* dims, int64_t* cells_out,
                                int64_t* split_out, int32_t device) {
   return mcm_solve_host(batch, n, dims, PIPEDP_MCM_AUTO, cells_out, split_out, device);
-}
-
-int32_t pipedp_mcm_pipeline(const int64_t* dims, int64_t dims_len, int32_t mode,
-                            int64_t* cells_out, uint8_t* filled_out, int64_t* steps_out,
-                            int64_t* stall_out) {
-  TRY(validate_mcm(dims, dims_len));
-  const int64_t n = dims_len - 1;
-  if (n < 2) return fail(PIPEDP_E_INVALID_PARAMS, "pipeline needs at least two matrices");
-  if (mode != PIPEDP_MCM_PAPER_LITERAL && mode != PIPEDP_MCM_STALL_ON_HAZARD)
-    return fail(PIPEDP_E_INVALID_PARAMS, "unknown McmMode %d", mode);
-  TRY(select_device(-1));
-  const int64_t cc = n * (n + 1) / 2;
-  Scope sc;
-  TRY(sc.init());
-  int64_t *d_dims, *d_cells, *d_vhead, *d_wval, *d_steps;
-  int32_t *d_row, *d_diag, *d_wcount;
-  int8_t *d_state, *d_exec;
-  TRY(sc.alloc(&d_dims, n + 1));
-  TRY(sc.alloc(&d_cells, cc + 1));
-  TRY(sc.alloc(&d_vhead, n));
-  TRY(sc.alloc(&d_wval, n));
-  TRY(sc.alloc(&d_steps, 2));
-  TRY(sc.alloc(&d_row, cc + 1));
-  TRY(sc.alloc(&d_diag, cc + 1));
-  TRY(sc.alloc(&d_wcount, cc + 1));
-  TRY(sc.alloc(&d_state, n));
-  TRY(sc.alloc(&d_exec, n));
-  CK(cudaMemcpyAsync(d_dims, dims, sizeof(int64_t) * (n + 1), cudaMemcpyHostToDevice, sc.stream));
-  CK(cudaMemsetAsync(d_cells, 0, sizeof(int64_t) * (cc + 1), sc.stream));
-  CK(cudaMemsetAsync(d_wcount, 0, sizeof(int32_t) * (cc + 1), sc.stream));
-  CK(cudaMemsetAsync(d_steps, 0, sizeof(int64_t) * 2, sc.stream));
-  mcm_coord_table<<<(unsigned)std::min<int64_t>(4096, (cc + 255) / 256), 256, 0, sc.stream>>>(n, d_row, d_diag);
-  CK(cudaGetLastError());
-  McmLockstep S{n, mode == PIPEDP_MCM_STALL_ON_HAZARD, d_row, d_diag, d_wcount, d_vhead,
-                d_state, d_exec, d_wval, d_steps};
-  mcm_lockstep<<<1, 1024, 0, sc.stream>>>(S, d_dims, d_cells);
-  CK(cudaGetLastError());
-  int64_t h_steps[2];
-  CK(cudaMemcpyAsync(h_steps, d_steps, sizeof h_steps, cudaMemcpyDeviceToHost, sc.stream));
-  CK(cudaMemcpyAsync(cells_out, d_cells, sizeof(int64_t) * (cc + 1), cudaMemcpyDeviceToHost, sc.stream));
-  CK(cudaStreamSynchronize(sc.stream));
-  if (h_steps[1]) return fail(PIPEDP_E_STALL_LIVELOCK, "no lane can make progress");
-  if (filled_out) memset(filled_out, 1, (size_t)(cc + 1));
-  const int64_t heads = (cc + n - 2) - (n + 1) + 1;
-  if (steps_out) *steps_out = h_steps[0];
-  if (stall_out) *stall_out = h_steps[0] - heads;
-  return PIPEDP_OK;
 }
 
 int32_t pipedp_mcm_bruteforce(const int64_t* dims, int64_t dims_len, int64_t* out) {

@@ -272,117 +272,6 @@ __global__ void __launch_bounds__(1024, 1)
   (void)cc;
 }
 
-// -----------------------------------------------------------------------------
-// Exact lock-step emulation of the reference engine running McmProgram
-// (engine.hpp:134-433 + mcm_pipeline.hpp:22-84): lanes j = 1..n-1 with their
-// own vhead; per iteration a plan phase (stall mode: operands must have all
-// their writes, own cell exactly j-1), a read/compute phase against the table
-// of the previous iteration, and a write phase.  Reproduces the table, the
-// step count and the stall count of both McmMode values bit-for-bit.
-struct McmLockstep {
-  int64_t n;
-  int stall;
-  const int32_t* row;   // [cc+1]
-  const int32_t* diag;  // [cc+1]
-  int32_t* wcount;      // [cc+1] writes applied
-  int64_t* vhead;       // [n]
-  int8_t* state;        // [n] 0 running, 1 done
-  int8_t* exec;         // [n]
-  int64_t* wval;        // [n]
-  int64_t* steps_out;   // [2] steps, error flag
-};
-
-__global__ void mcm_coord_table(int64_t n, int32_t* row, int32_t* diag) {
-  // one thread per (D, r); the grid covers all cells
-  const int64_t cc = n * (n + 1) / 2;
-  for (int64_t a = blockIdx.x * (int64_t)blockDim.x + threadIdx.x + 1; a <= cc;
-       a += (int64_t)gridDim.x * blockDim.x) {
-    // invert dbase: largest D with dbase(D) < a
-    double nn = (double)n + 0.5;
-    int64_t D = (int64_t)(nn - sqrt(nn * nn - 2.0 * (double)(a - 1)));
-    if (D < 0) D = 0;
-    if (D > n - 1) D = n - 1;
-    while (D > 0 && mcm_dbase(D, n) >= a) --D;
-    while (D + 1 <= n - 1 && mcm_dbase(D + 1, n) < a) ++D;
-    row[a] = (int32_t)(a - mcm_dbase(D, n));
-    diag[a] = (int32_t)D;
-  }
-}
-
-__global__ void __launch_bounds__(1024, 1)
-    mcm_lockstep(const McmLockstep S, const int64_t* __restrict__ g_dims, int64_t* cells) {
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int64_t n = S.n;
-  const int64_t cc = n * (n + 1) / 2;
-  const int64_t first = n + 1, last = cc + n - 2;
-  const int64_t lanes = n - 1;
-  const int64_t budget = (last - first + 1) * (lanes + 2) + 16;
-  for (int64_t j = tid + 1; j <= lanes; j += nt) {
-    S.vhead[j] = first;
-    S.state[j] = 0;
-  }
-  __syncthreads();
-  int64_t steps = 0;
-  for (;;) {
-    bool all_done = true, any_exec = false;
-    for (int64_t j = tid + 1; j <= lanes; j += nt) {
-      int8_t e = 0;
-      if (!S.state[j]) {
-        all_done = false;
-        const int64_t cell = S.vhead[j] - j + 1;
-        const bool active = cell >= n + 1 && cell <= cc && j <= S.diag[cell];
-        if (!active) {
-          e = 2;
-        } else {
-          bool ready = true;
-          if (S.stall) {
-            const int64_t r = S.row[cell], D = S.diag[cell];
-            const int64_t left = mcm_dbase(j - 1, n) + r;
-            const int64_t right = mcm_dbase(D - j, n) + r + j;
-            if (left > n && S.wcount[left] < S.diag[left]) ready = false;
-            if (right > n && S.wcount[right] < S.diag[right]) ready = false;
-            if (S.wcount[cell] != j - 1) ready = false;
-          }
-          e = ready ? 1 : 0;
-        }
-        if (e) any_exec = true;
-        if (e == 1) {
-          const int64_t r = S.row[cell], D = S.diag[cell], c = r + D;
-          const int64_t vs = cells[mcm_dbase(j - 1, n) + r] + cells[mcm_dbase(D - j, n) + r + j] +
-                             g_dims[r - 1] * g_dims[r + j - 1] * g_dims[c];
-          const int64_t own = cells[cell];
-          S.wval[j] = j == 1 ? vs : (own < vs ? own : vs);
-        }
-      }
-      S.exec[j] = e;
-    }
-    all_done = __syncthreads_and(all_done);
-    if (all_done) break;
-    any_exec = __syncthreads_or(any_exec);
-    if (!any_exec || steps > budget) {
-      if (tid == 0) S.steps_out[1] = 1;  // livelock (engine.hpp:352-362)
-      return;
-    }
-    for (int64_t j = tid + 1; j <= lanes; j += nt) {
-      const int8_t e = S.exec[j];
-      if (e == 1) {
-        const int64_t cell = S.vhead[j] - j + 1;
-        cells[cell] = S.wval[j];
-        S.wcount[cell] += 1;
-      }
-      if (e) {
-        if (++S.vhead[j] > last) S.state[j] = 1;
-      }
-    }
-    ++steps;
-    __syncthreads();
-  }
-  if (tid == 0) {
-    S.steps_out[0] = steps;
-    S.steps_out[1] = 0;
-  }
-}
-
 }  // namespace pipedp_dev
 
 namespace pipedp_dev {

@@ -6,7 +6,9 @@
 // CPU solver behind these functions.
 #include <algorithm>
 #include <cstdio>
+#include <map>
 #include <string>
+#include <tuple>
 
 #include "pipedp/error.hpp"
 #include "pipedp/generate.hpp"
@@ -44,6 +46,68 @@ std::int64_t ceil_log2(std::int64_t k) {  // sdp.cpp:78-80
   std::int64_t r = 0;
   while ((std::int64_t{1} << r) < k) ++r;
   return r;
+}
+
+// The device records of one engine run -> the reference's trace/report types.
+constexpr std::int64_t kTraceLimit = std::int64_t(1) << 28;  // pipedp_engine: records per trace
+
+struct EngineRun {
+  pipedp_engine_t run = nullptr;
+  pipedp_engine_summary sum{};
+  ~EngineRun() { pipedp_engine_free(run); }
+};
+
+void fill_trace(EngineRun& e, bool collected, PipelineTrace& t) {
+  t.first_head = e.sum.first_head;
+  t.steps_executed = e.sum.steps_executed;
+  t.stall_iterations = e.sum.stall_iterations;
+  t.collected = collected;
+  t.stall_heads.assign(static_cast<std::size_t>(e.sum.stall_heads), 0);
+  check(pipedp_engine_stall_heads(e.run, t.stall_heads.data()));
+  const std::size_t nr = static_cast<std::size_t>(e.sum.records);
+  if (!nr) return;
+  std::vector<std::int64_t> head(nr), addr(nr);
+  std::vector<std::int32_t> sub(nr), lane(nr), kind(nr);
+  check(pipedp_engine_records(e.run, head.data(), sub.data(), lane.data(), kind.data(), addr.data()));
+  t.records.resize(nr);
+  for (std::size_t i = 0; i < nr; ++i)
+    t.records[i] = AccessRecord{head[i], sub[i], lane[i], kind[i] ? AccessKind::write : AccessKind::read, addr[i]};
+}
+
+ConflictReport conflicts_of(EngineRun& e) {
+  ConflictReport c;
+  c.first_head = e.sum.first_head;
+  c.max_group_size = static_cast<int>(e.sum.max_group_size);
+  const std::size_t g = static_cast<std::size_t>(e.sum.conflict_groups);
+  std::vector<std::int64_t> groups(4 * g);
+  std::vector<std::int32_t> sizes(g), lanes(static_cast<std::size_t>(e.sum.conflict_lanes));
+  c.per_step_cost.assign(static_cast<std::size_t>(std::max<std::int64_t>(e.sum.steps_executed, 0)), 1);
+  check(pipedp_engine_conflicts(e.run, groups.data(), sizes.data(), lanes.data(), c.per_step_cost.data()));
+  std::size_t at = 0;
+  for (std::size_t i = 0; i < g; ++i) {
+    ConflictGroup cg;
+    cg.head = groups[4 * i];
+    cg.substep = static_cast<int>(groups[4 * i + 1]);
+    cg.kind = groups[4 * i + 2] ? AccessKind::write : AccessKind::read;
+    cg.address = groups[4 * i + 3];
+    cg.lanes.assign(lanes.begin() + static_cast<std::ptrdiff_t>(at),
+                    lanes.begin() + static_cast<std::ptrdiff_t>(at + sizes[i]));
+    at += static_cast<std::size_t>(sizes[i]);
+    c.groups.push_back(std::move(cg));
+  }
+  return c;
+}
+
+HazardReport hazards_of(EngineRun& e) {
+  HazardReport h;
+  const std::size_t nh = static_cast<std::size_t>(e.sum.hazards);
+  std::vector<std::int64_t> v(6 * nh);
+  check(pipedp_engine_hazards(e.run, v.data()));
+  h.hazards.resize(nh);
+  for (std::size_t i = 0; i < nh; ++i)
+    h.hazards[i] = HazardRecord{v[6 * i], static_cast<int>(v[6 * i + 1]), static_cast<int>(v[6 * i + 2]),
+                                v[6 * i + 3], v[6 * i + 4], static_cast<int>(v[6 * i + 5])};
+  return h;
 }
 
 }  // namespace
@@ -211,14 +275,33 @@ ConflictRunAnalysis analyze_conflict_runs(const OffsetSet& offsets) {  // sdp_pi
   return a;
 }
 
-SdpPipelineResult solve_sdp_pipeline(const SdpInstance& inst, const SdpRunConfig&) {
+// solve_sdp_pipeline (sdp_pipeline.cpp:34-44).  Without collect_trace the
+// table comes from the fast S-DP solvers (the schedule never stalls, so its
+// step count is n + k - a_1 - 1).  With collect_trace the GPU lock-step engine
+// runs SdpProgram itself: the table, the access records (when they fit the
+// trace limit; otherwise trace.collected = false) and detect_conflicts'
+// report computed on the device.
+SdpPipelineResult solve_sdp_pipeline(const SdpInstance& inst, const SdpRunConfig& cfg) {
+  validate(inst);
   SdpPipelineResult r;
-  r.table = solve_sequential(inst);
-  // SdpProgram head range [a_1, n+k-2] (sdp_pipeline.hpp:20), never stalls
-  r.trace.first_head = inst.offsets.a1();
-  r.trace.steps_executed = inst.n + inst.offsets.k() - inst.offsets.a1() - 1;
-  r.trace.stall_iterations = 0;
-  r.trace.collected = false;
+  if (!cfg.collect_trace) {
+    r.table = solve_sequential(inst);
+    r.trace.first_head = inst.offsets.a1();  // head range [a_1, n+k-2] (sdp_pipeline.hpp:20)
+    r.trace.steps_executed = inst.n + inst.offsets.k() - inst.offsets.a1() - 1;
+    r.trace.stall_iterations = 0;
+    r.trace.collected = false;
+    return r;
+  }
+  const std::int64_t k = inst.offsets.k(), a1 = inst.offsets.a1();
+  const bool fits = (inst.n - a1) * (3 * k - 1) <= kTraceLimit;
+  EngineRun e;
+  r.table = full_table(inst.n);
+  check(pipedp_sdp_engine(inst.offsets.offsets.data(), k, inst.init.data(), static_cast<std::int64_t>(inst.init.size()),
+                          inst.n, static_cast<int32_t>(inst.op.kind),
+                          PIPEDP_ENGINE_ANALYSIS | (fits ? PIPEDP_ENGINE_TRACE : 0), r.table.cells.data(), &e.sum,
+                          &e.run));
+  fill_trace(e, fits, r.trace);
+  r.conflicts = conflicts_of(e);
   return r;
 }
 
@@ -323,21 +406,66 @@ std::vector<SolutionTable> solve_mcm_batch(const std::vector<McmInstance>& insts
   return out;
 }
 
+// solve_mcm_pipeline (mcm_pipeline.cpp:32-47): the GPU lock-step engine
+// running McmProgram in either McmMode -- table, steps, stalls and stall
+// heads always; with collect_trace also the access records (when they fit the
+// trace limit; otherwise trace.collected = false) and the conflict and hazard
+// reports, computed on the device while the schedule runs.
 McmPipelineResult solve_mcm_pipeline(const McmInstance& inst, const McmScheduleConfig& cfg) {
   validate(inst);  // build_mcm_program: validate, then n >= 2 (mcm_pipeline.cpp:26-30)
   if (inst.n() < 2) fail(errc::invalid_params, "pipeline needs at least two matrices");
+  const std::int64_t n = inst.n(), cc = cell_count(n);
+  const bool fits = 4 * ((n * n * n - n) / 6) - (cc - n) <= kTraceLimit;
+  const int32_t flags = cfg.collect_trace ? (PIPEDP_ENGINE_ANALYSIS | (fits ? PIPEDP_ENGINE_TRACE : 0)) : 0;
   McmPipelineResult r;
-  r.table = full_table(cell_count(inst.n()) + 1);
-  std::int64_t steps = 0, stalls = 0;
-  check(pipedp_mcm_pipeline(inst.dims.data(), static_cast<std::int64_t>(inst.dims.size()),
-                            cfg.mode == McmMode::stall_on_hazard ? PIPEDP_MCM_STALL_ON_HAZARD
-                                                                 : PIPEDP_MCM_PAPER_LITERAL,
-                            r.table.cells.data(), nullptr, &steps, &stalls));
-  r.trace.first_head = inst.n() + 1;
-  r.trace.steps_executed = steps;
-  r.trace.stall_iterations = stalls;
-  r.trace.collected = false;
+  r.table = full_table(cc + 1);
+  EngineRun e;
+  check(pipedp_mcm_engine(inst.dims.data(), static_cast<std::int64_t>(inst.dims.size()),
+                          cfg.mode == McmMode::stall_on_hazard ? PIPEDP_MCM_STALL_ON_HAZARD : PIPEDP_MCM_PAPER_LITERAL,
+                          flags, r.table.cells.data(), &e.sum, &e.run));
+  fill_trace(e, cfg.collect_trace && fits, r.trace);
+  if (cfg.collect_trace) {
+    r.conflicts = conflicts_of(e);
+    r.hazards = hazards_of(e);
+  }
   return r;
+}
+
+// verify_substep_distinctness (mcm_pipeline.cpp:49-77): Lemma 1/2 check on a
+// trace -- substep-1 reads, substep-2 reads and substep-4 writes must touch
+// distinct addresses across lanes at every head.  The counterexample is the
+// first offending (head, substep, address) in that order.
+DistinctnessVerdict verify_substep_distinctness(const PipelineTrace& trace) {
+  std::vector<std::tuple<std::int64_t, int, std::int64_t, int>> picked;  // head, substep, address, lane
+  for (const AccessRecord& a : trace.records) {
+    const bool rd = a.kind == AccessKind::read && (a.substep == 1 || a.substep == 2);
+    const bool wr = a.kind == AccessKind::write && a.substep == 4;
+    if (rd || wr) picked.emplace_back(a.head, a.substep, a.address, a.lane);
+  }
+  std::sort(picked.begin(), picked.end());
+  DistinctnessVerdict v;
+  for (std::size_t i = 0; i < picked.size();) {
+    std::size_t j = i + 1;
+    while (j < picked.size() && std::get<0>(picked[j]) == std::get<0>(picked[i]) &&
+           std::get<1>(picked[j]) == std::get<1>(picked[i]) && std::get<2>(picked[j]) == std::get<2>(picked[i]))
+      ++j;
+    if (j - i >= 2) {
+      const int sub = std::get<1>(picked[i]);
+      (sub == 1 ? v.substep1_reads_distinct : sub == 2 ? v.substep2_reads_distinct : v.substep4_writes_distinct) =
+          false;
+      if (!v.counterexample) {
+        ConflictGroup g;
+        g.head = std::get<0>(picked[i]);
+        g.substep = sub;
+        g.kind = sub == 4 ? AccessKind::write : AccessKind::read;
+        g.address = std::get<2>(picked[i]);
+        for (std::size_t t = i; t < j; ++t) g.lanes.push_back(std::get<3>(picked[t]));
+        v.counterexample = std::move(g);
+      }
+    }
+    i = j;
+  }
+  return v;
 }
 
 // ------------------------------------------------------------ generators ---

@@ -71,3 +71,45 @@ def test_dropin_instance_io_and_parenthesization(binary):
     # reference io.cpp formats, the batched loader, split-table parenthesisation
     rc, out = _run(binary, "io")
     assert rc == 0 and out.strip().endswith("OK"), out
+
+
+# ---- INTEGRATION.md §2 for real: the reference's own callers on the drop-in ----
+CALLERS = os.path.join(ROOT, "tests", "cpp", "_build", "ref_callers")
+GOLD_DIR = os.path.join(ROOT, "tests", "golden")
+
+
+@pytest.fixture(scope="module")
+def ref_callers(pd):
+    """tests/cpp/Makefile: proj/src/commands.cpp, analysis.cpp, io.cpp compiled
+    against include/ (+ the reference's include/ for commands.hpp) and linked
+    with -lpipedp_b200 -lpipedp_cuda -- built here from /root/reference, or
+    prebuilt (build()) where the reference is absent."""
+    if os.path.isdir("/root/reference/proj/src"):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp"), CALLERS], check=True)
+    if not os.path.exists(CALLERS):
+        pytest.skip("reference callers not built (reference sources absent and no prebuilt binary)")
+    return CALLERS
+
+
+def _strip_msec(text):
+    return "".join(l + "\n" for l in text.splitlines() if not l.startswith("msec:"))
+
+
+def test_reference_callers_link_and_fail_loudly_without_gpu(ref_callers, pd):
+    if pd.device_count() > 0:
+        pytest.skip("a GPU is visible; the no-GPU contract is checked on the CPU box")
+    r = subprocess.run([ref_callers, "run"], capture_output=True, text=True, timeout=120)
+    rcs = [l for l in r.stdout.splitlines() if " rc=" in l]
+    assert len(rcs) == 6 and all(l.endswith("rc=2") for l in rcs), r.stdout
+    assert r.stderr.count("error: NoDevice") == 6, r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["run", "verify"])
+def test_reference_callers_on_gpu(ref_callers, gpu, mode):
+    """cmd_run / cmd_verify of the reference, unchanged, over the B200 drop-in:
+    same digests, steps, conflict counts, hazard frontier and verdicts as the
+    same program linked with the reference's own solvers."""
+    r = subprocess.run([ref_callers, mode], capture_output=True, text=True, timeout=600)
+    want = open(os.path.join(GOLD_DIR, f"ref_callers_{mode}.txt")).read()
+    assert _strip_msec(r.stdout) == want, r.stderr[-2000:]

@@ -18,7 +18,7 @@ GOLDEN = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^\s*(?:const char\*|int32_t|uint64_t)\s+(pipedp_\w+)\s*\(", text, re.M)))
+    return sorted(set(re.findall(r"^\s*(?:const char\*|int32_t|uint64_t|void)\s+(pipedp_\w+)\s*\(", text, re.M)))
 
 
 def test_header_symbols_exported(pd):
