@@ -153,7 +153,10 @@ static int run_solve() {
   EXPECT(m.cells.back() == 15125 && split.back() == 3 && m.all_filled());
   // the reference's defaults (collect_trace = true, paper_literal) must be accepted
   McmPipelineResult pr = solve_mcm_pipeline(McmInstance{{10, 20, 30, 40, 30}});
-  EXPECT(pr.trace.steps_executed == 4 * 5 / 2 - 2 && !pr.trace.collected);
+  // -> trace collected by the GPU engine; n = 4 is hazardous at address 10
+  EXPECT(pr.trace.steps_executed == 4 * 5 / 2 - 2 && pr.trace.collected && pr.trace.records.size() == 34);
+  EXPECT(hazard_cells(pr.hazards) == std::vector<std::int64_t>{10} && pr.conflicts.max_group_size == 1);
+  EXPECT(verify_substep_distinctness(pr.trace).all_ok());
   McmScheduleConfig sc;
   sc.mode = McmMode::stall_on_hazard;
   McmPipelineResult ps = solve_mcm_pipeline(McmInstance{{10, 20, 30, 40, 30}}, sc);
