@@ -26,6 +26,7 @@
 #include "sdp_chunked.cuh"
 #include "sdp_v2.cuh"
 #include "host_io.hpp"
+#include "sdp_rank.hpp"
 
 using namespace pipedp_dev;
 
@@ -556,6 +557,11 @@ struct pipedp_sdp_plan {
   int64_t* d_offsets;  // device copy of the offsets, int64 [batch*k]
   void* d_remote;      // multi-CTA workspace: partial slots | ready flags | published
   int32_t* d_obg;      // remote producers: offsets as HBM-table byte offsets
+  // chunked min / max on 16-bit ranks (sdp_rank.cu); null: the generic chunk batch
+  pipedp_rank::ChunkRankParams* rank = nullptr;
+  int rank_threads = 0;
+  size_t rank_smem = 0;
+  int64_t* d_sorted = nullptr;  // [a1] init ascending: rank -> value
 };
 
 // ================================================================== MCM ===
@@ -1026,6 +1032,16 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
     if (e == cudaSuccess) e = cudaMalloc(&P->d_pad, sizeof(int64_t) * P->G * P->n_i);
     if (e == cudaSuccess)
       e = cudaMemcpy(P->d_offs_rep, orep.data(), sizeof(int64_t) * P->G * k, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && env_int("PIPEDP_SDP_RANK", 1) != 0) {
+      auto* rp = new pipedp_rank::ChunkRankParams();
+      if (pipedp_rank::chunk_rank_plan(h_offsets, P->d_offsets, (int)k, (int)a1, n, P->Lc, P->G,
+                                       op == PIPEDP_OP_MAX ? 1 : 0, rp, &P->rank_threads, &P->rank_smem)) {
+        P->rank = rp;
+        e = cudaMalloc(&P->d_sorted, sizeof(int64_t) * a1);
+      } else {
+        delete rp;
+      }
+    }
   }
   if (e != cudaSuccess) {
     pipedp_sdp_plan_destroy(P);
@@ -1143,8 +1159,21 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
   // chunks [0, gs) then [gs, G), each gathered into the instance's table; an
   // event after the first range lets the host copy it out while the second runs
   const int64_t gs = split_at > 0 && split_at < P->G ? split_at : P->G;
+  if (P->rank) {  // rank-compressed chunk batch: chunks write the table directly
+    CK(pipedp_rank::chunk_rank_sort(d_init, a1, P->d_sorted, st));
+    P->rank->cinit = P->d_cinit;
+    P->rank->sorted = P->d_sorted;
+    P->rank->out = d_cells;
+  }
   for (int64_t g0 = 0; g0 < P->G; g0 = gs == P->G ? P->G : (g0 == 0 ? gs : P->G)) {
     const int64_t g1 = g0 == 0 ? gs : P->G;
+    if (P->rank) {
+      P->rank->g0 = g0;
+      P->rank->G = g1;
+      CK(pipedp_rank::chunk_rank_launch(*P->rank, P->rank_threads, P->rank_smem, st));
+      if (g0 == 0 && split_event) CK(cudaEventRecord(split_event, st));
+      continue;
+    }
     TRY(launch_sdp(P->dc, g1 - g0, P->d_offs_rep + g0 * P->k, P->d_cinit + g0 * a1, P->d_pad + g0 * P->n_i,
                    SdpRemote{}, st));
     const int64_t full = std::min(g1, P->G - 1) - g0;  // whole chunks in the range
@@ -1267,7 +1296,8 @@ int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, in
   if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
   if (name && cap) {
     if (P->d.chunked)
-      snprintf(name, cap, "sdp_chunked[L=%lld,G=%lld,%s]", (long long)P->Lc, (long long)P->G, sdp_kernel_name(P->dc));
+      snprintf(name, cap, "sdp_chunked[L=%lld,G=%lld,%s]", (long long)P->Lc, (long long)P->G,
+               P->rank ? "chunk_rank_kernel" : sdp_kernel_name(P->dc));
     else snprintf(name, cap, "%s", sdp_kernel_name(P->d));
   }
   if (bits) *bits = P->d.chunked ? P->dc.bits : P->d.bits;
@@ -1294,6 +1324,7 @@ int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, in
       if (P->G >= 64)
         for (int b = 1; b < 16; b *= 2) nl += prod(er * 2 * b);
       nl += 1 + 1;  // chain, chunk batch
+      if (P->rank) nl += 1;  // rank sort
     }
     *launches = nl;
   }
@@ -1329,6 +1360,8 @@ int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t P) {
   cudaFree(P->d_cinit);
   cudaFree(P->d_offs_rep);
   cudaFree(P->d_pad);
+  cudaFree(P->d_sorted);
+  delete P->rank;
   delete P;
   return PIPEDP_OK;
 }
