@@ -27,6 +27,7 @@
 #include "sdp_v2.cuh"
 #include "host_io.hpp"
 #include "sdp_rank.hpp"
+#include "sdp_batch_dom.hpp"
 
 using namespace pipedp_dev;
 
@@ -562,6 +563,10 @@ struct pipedp_sdp_plan {
   int rank_threads = 0;
   size_t rank_smem = 0;
   int64_t* d_sorted = nullptr;  // [a1] init ascending: rank -> value
+  // batched min / max: instances perm[0, n_dom) take the dominance kernel
+  // (sdp_batch_dom.cu), the rest sdp_batch_warp
+  int64_t n_dom = 0;
+  pipedp_bdom::DomInfo* d_dinfo = nullptr;
 };
 
 // ================================================================== MCM ===
@@ -983,11 +988,24 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
       }
       if (all) mode[(size_t)b] = 2;
     }
+    // the dominance kernel first (device-classified: g <= 32), then the rest by mode
+    std::vector<pipedp_bdom::DomInfo> info;
+    if (d.bits == 32 && a1 >= 64 && a1 <= 128 && env_int("PIPEDP_SDP_BDOM", 1) != 0) {
+      e = cudaMalloc(&P->d_dinfo, sizeof(pipedp_bdom::DomInfo) * batch);
+      if (e == cudaSuccess) e = pipedp_bdom::classify(batch, (int32_t)k, (int32_t)a1, P->d_offsets, P->d_dinfo, 0);
+      if (e == cudaSuccess) {
+        info.resize((size_t)batch);
+        e = cudaMemcpy(info.data(), P->d_dinfo, sizeof(pipedp_bdom::DomInfo) * batch, cudaMemcpyDeviceToHost);
+      }
+    }
     std::vector<int32_t> perm;
     perm.reserve((size_t)batch);
+    for (int64_t b = 0; b < (int64_t)info.size(); ++b)
+      if (info[(size_t)b].g != 0) perm.push_back((int32_t)b);
+    P->n_dom = (int64_t)perm.size();
     for (int want : {1, 2, 0})
       for (int64_t b = 0; b < batch; ++b)
-        if (mode[(size_t)b] == want) perm.push_back((int32_t)b);
+        if (mode[(size_t)b] == want && (info.empty() || info[(size_t)b].g == 0)) perm.push_back((int32_t)b);
     e = cudaMalloc(&P->d_perm, sizeof(int32_t) * batch);
     if (e == cudaSuccess) e = cudaMemcpy(P->d_perm, perm.data(), sizeof(int32_t) * batch, cudaMemcpyHostToDevice);
   }
@@ -1217,9 +1235,13 @@ static int32_t sdp_execute(pipedp_sdp_plan_t P, const int64_t* d_init, int64_t* 
   }
   if (armed) CK(cudaEventRecord(armed, (cudaStream_t)stream));
   if (P->d_perm) {
+    if (P->n_dom > 0)
+      CK(pipedp_bdom::launch(P->d.op == PIPEDP_OP_MAX ? 1 : 0, P->n_dom, P->d_perm, P->n, (int32_t)P->k,
+                             (int32_t)P->a1, P->d_offsets, d_init, d_cells, P->d_dinfo, (cudaStream_t)stream));
+    if (P->n_dom == P->batch) return PIPEDP_OK;
     SdpDispatch dd = P->d;
-    dd.shape.perm = P->d_perm;
-    return launch_sdp(dd, P->batch, P->d_offsets, d_init, d_cells, rm, (cudaStream_t)stream);
+    dd.shape.perm = P->d_perm + P->n_dom;
+    return launch_sdp(dd, P->batch - P->n_dom, P->d_offsets, d_init, d_cells, rm, (cudaStream_t)stream);
   }
   return launch_sdp(P->d, P->batch, P->d_offsets, d_init, d_cells, rm, (cudaStream_t)stream);
 }
@@ -1298,6 +1320,9 @@ int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, in
     if (P->d.chunked)
       snprintf(name, cap, "sdp_chunked[L=%lld,G=%lld,%s]", (long long)P->Lc, (long long)P->G,
                P->rank ? "chunk_rank_kernel" : sdp_kernel_name(P->dc));
+    else if (P->n_dom > 0)
+      snprintf(name, cap, "sdp_batch_dom[%lld/%lld]%s", (long long)P->n_dom, (long long)P->batch,
+               P->n_dom < P->batch ? "+sdp_batch_warp" : "");
     else snprintf(name, cap, "%s", sdp_kernel_name(P->d));
   }
   if (bits) *bits = P->d.chunked ? P->dc.bits : P->d.bits;
@@ -1325,6 +1350,8 @@ int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, in
         for (int b = 1; b < 16; b *= 2) nl += prod(er * 2 * b);
       nl += 1 + 1;  // chain, chunk batch
       if (P->rank) nl += 1;  // rank sort
+    } else if (P->n_dom > 0) {
+      nl = 1 + (P->n_dom < P->batch ? 1 : 0);  // dominance kernel (+ sdp_batch_warp for the rest)
     }
     *launches = nl;
   }
@@ -1361,6 +1388,7 @@ int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t P) {
   cudaFree(P->d_offs_rep);
   cudaFree(P->d_pad);
   cudaFree(P->d_sorted);
+  cudaFree(P->d_dinfo);
   delete P->rank;
   delete P;
   return PIPEDP_OK;

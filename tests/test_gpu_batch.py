@@ -158,3 +158,46 @@ def test_bench_two_ranks_share_one_gpu(gpu):
     line = json.loads(out.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "shard2"
     assert line["parity"]["match"] is True and line["parity"]["instances"] == 65536
+
+
+def _mk(rng, a1, must, nrest, lo, n, op, step=1):
+    pool = np.arange(lo, a1, step)
+    pool = pool[~np.isin(pool, must)]
+    rest = rng.choice(pool, min(nrest, len(pool)), replace=False)
+    offs = np.unique(np.concatenate([[a1], must, rest]))[::-1].astype(np.int64)
+    return offs, rng.integers(-(2**30), 2**30, a1)
+
+
+@pytest.mark.parametrize("op", ["min", "max"])
+@pytest.mark.parametrize("a1", [64, 97, 128])
+def test_sdp_batch_dominance_kernel(gpu, oracle, op, a1):
+    """sdp_batch_dom (window + closure form) on the shapes that stress it: F
+    non-empty below g (in-step D terms), g near 32, odd a_1 (window start lane
+    shuffles), and instances with g > 32 that must fall back to sdp_batch_warp
+    in the same plan."""
+    rng = np.random.default_rng(a1 * 7 + (op == "max"))
+    kinds = [([1], 1), ([2, 3], 2), ([3, 5], 3), ([4, 6, 9], 4), ([7, 11], 6), ([5, 8], 3),
+             ([13, 17, 19], 12), ([20, 25, 31], 20), ([33, 34], 33), ([40], 40)]
+    n, k = 5000, None
+    insts = []
+    for i in range(60):
+        must, lo = kinds[i % len(kinds)]
+        offs, init = _mk(rng, a1, [m for m in must if m < a1], 24, max(lo, 1), n, op)
+        insts.append((offs, init))
+    k = min(len(o) for o, _ in insts)  # the batch API needs one k: trim each to its k largest + must
+    batch = []
+    for offs, init in insts:
+        o = np.concatenate([offs[:k - 1], offs[-1:]]) if len(offs) > k else offs
+        o = np.unique(o)[::-1].astype(np.int64)
+        if len(o) < k:  # pad with fresh large offsets
+            extra = [d for d in range(a1 - 1, 0, -1) if d not in o][: k - len(o)]
+            o = np.unique(np.concatenate([o, extra]))[::-1].astype(np.int64)
+        batch.append(gpu.SdpInstance(n, o, init, op))
+    offs = np.stack([b.offsets for b in batch]).reshape(-1)
+    init = np.stack([b.init for b in batch]).reshape(-1)
+    plan = gpu.SdpPlan(len(batch), n, k, a1, offs, init, op, device=0)
+    name = plan.describe()[0]
+    assert name.startswith("sdp_batch_dom"), name
+    for inst, t in zip(batch, gpu.solve_sequential_batch(batch)):
+        want, _ = oracle.sdp_solve(inst.offsets, inst.init, inst.n, op)
+        assert np.array_equal(t.cells, want), (list(inst.offsets[-6:]), op, a1)
