@@ -49,6 +49,18 @@ def _newer(target: str, sources) -> bool:
     return any(os.path.getmtime(s) > t for s in sources)
 
 
+def _deps(path, seen=None):
+    """path plus every file it #includes with quotes, recursively."""
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    import re
+    for inc in re.findall(r'^\s*#\s*include\s+"([^"]+)"', open(path).read(), re.M):
+        _deps(os.path.normpath(os.path.join(os.path.dirname(path), inc)), seen)
+    return seen
+
+
 def _sources(d, exts):
     return sorted(os.path.join(d, f) for f in os.listdir(d) if f.endswith(exts))
 
@@ -69,8 +81,9 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
         objdir = os.path.join(LIB, "obj_prof" if profile else "obj")
         os.makedirs(objdir, exist_ok=True)
         objs = [os.path.join(objdir, os.path.basename(t) + ".o") for t in tus]
+        todo = [(t, o) for t, o in zip(tus, objs) if force or _newer(o, sorted(_deps(t)))]
         procs = [(subprocess.Popen([nvcc, *flags, "-c", t, "-o", o], stdout=subprocess.PIPE,
-                                   stderr=subprocess.STDOUT, text=True), t) for t, o in zip(tus, objs)]
+                                   stderr=subprocess.STDOUT, text=True), t) for t, o in todo]
         for p, t in procs:
             out = p.communicate()[0]
             if verbose or p.returncode:

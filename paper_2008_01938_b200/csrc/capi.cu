@@ -567,6 +567,9 @@ struct pipedp_sdp_plan {
   // (sdp_batch_dom.cu), the rest sdp_batch_warp
   int64_t n_dom = 0;
   pipedp_bdom::DomInfo* d_dinfo = nullptr;
+  // the fallback instances run beside the dominance kernel (fork / join)
+  cudaStream_t side = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // ================================================================== MCM ===
@@ -1235,13 +1238,26 @@ static int32_t sdp_execute(pipedp_sdp_plan_t P, const int64_t* d_init, int64_t* 
   }
   if (armed) CK(cudaEventRecord(armed, (cudaStream_t)stream));
   if (P->d_perm) {
-    if (P->n_dom > 0)
-      CK(pipedp_bdom::launch(P->d.op == PIPEDP_OP_MAX ? 1 : 0, P->n_dom, P->d_perm, P->n, (int32_t)P->k,
-                             (int32_t)P->a1, P->d_offsets, d_init, d_cells, P->d_dinfo, (cudaStream_t)stream));
-    if (P->n_dom == P->batch) return PIPEDP_OK;
     SdpDispatch dd = P->d;
     dd.shape.perm = P->d_perm + P->n_dom;
-    return launch_sdp(dd, P->batch - P->n_dom, P->d_offsets, d_init, d_cells, rm, (cudaStream_t)stream);
+    if (P->n_dom == 0)
+      return launch_sdp(dd, P->batch, P->d_offsets, d_init, d_cells, rm, (cudaStream_t)stream);
+    const bool rest = P->n_dom < P->batch;
+    if (rest) {  // the few sdp_batch_warp instances run beside the dominance kernel
+      if (!P->side) {
+        CK(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&P->ev_fork, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&P->ev_join, cudaEventDisableTiming));
+      }
+      CK(cudaEventRecord(P->ev_fork, (cudaStream_t)stream));
+      CK(cudaStreamWaitEvent(P->side, P->ev_fork, 0));
+      TRY(launch_sdp(dd, P->batch - P->n_dom, P->d_offsets, d_init, d_cells, rm, P->side));
+      CK(cudaEventRecord(P->ev_join, P->side));
+    }
+    CK(pipedp_bdom::launch(P->d.op == PIPEDP_OP_MAX ? 1 : 0, P->n_dom, P->d_perm, P->n, (int32_t)P->k,
+                           (int32_t)P->a1, P->d_offsets, d_init, d_cells, P->d_dinfo, (cudaStream_t)stream));
+    if (rest) CK(cudaStreamWaitEvent((cudaStream_t)stream, P->ev_join, 0));
+    return PIPEDP_OK;
   }
   return launch_sdp(P->d, P->batch, P->d_offsets, d_init, d_cells, rm, (cudaStream_t)stream);
 }
@@ -1389,6 +1405,9 @@ int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t P) {
   cudaFree(P->d_pad);
   cudaFree(P->d_sorted);
   cudaFree(P->d_dinfo);
+  if (P->side) cudaStreamDestroy(P->side);
+  if (P->ev_fork) cudaEventDestroy(P->ev_fork);
+  if (P->ev_join) cudaEventDestroy(P->ev_join);
   delete P->rank;
   delete P;
   return PIPEDP_OK;

@@ -54,16 +54,15 @@ __global__ void dom_classify(int64_t batch, int32_t k, int32_t a1, const int64_t
     if (d < 64) A0 |= 1ull << d;
     else if (d < 128) A1 |= 1ull << (d - 64);
   }
-  uint64_t R0 = 1, R1 = 0;  // S* (with 0)
+  // S* (with 0) in increasing v: W holds reach[v - d] at bit d (d = 1..127),
+  // so reach[v] = (W & A) != 0 -- a 128-bit shift and test per v
+  uint64_t R0 = 1, R1 = 0, W0 = 0, W1 = 0;
+  bool last = true;  // reach[v - 1]
   for (int v = 1; v < a1; ++v) {
-    bool hit = false;
-    for (int d = 1; d <= v && !hit; ++d) {
-      const bool ina = d < 64 ? (A0 >> d) & 1 : (A1 >> (d - 64)) & 1;
-      if (!ina) continue;
-      const int u = v - d;
-      hit = u < 64 ? (R0 >> u) & 1 : (R1 >> (u - 64)) & 1;
-    }
-    if (hit) {
+    W1 = (W1 << 1) | (W0 >> 63);
+    W0 = (W0 << 1) | (last ? 2ull : 0ull);  // bit 1 = reach[v - 1]
+    last = ((W0 & A0) | (W1 & A1)) != 0;
+    if (last) {
       if (v < 64) R0 |= 1ull << v;
       else R1 |= 1ull << (v - 64);
     }
@@ -121,6 +120,98 @@ __device__ __forceinline__ int32_t warp_all(int32_t v) {
   return OP == kMin ? __reduce_min_sync(0xffffffffu, v) : __reduce_max_sync(0xffffffffu, v);
 }
 
+struct DomCtx {
+  int j0, L0, g, lg, h, lane;
+  uint32_t F, D;
+};
+
+// One step of 32 cells.  s2, s3, s4: suffix minima of steps b-2, b-3, b-4;
+// m1..m3 whole-step minima of steps b-1..b-3; p1 / x1: step b-1's prefix
+// minima and values (updated to step b's).  Returns step b's suffix minima.
+// MODE 1: g = 1 (x = prefix minimum of b); MODE 2: F = D = {} (one window
+// term per lane); MODE 0: general.  A128: a_1 = 128 (window start = lane l of
+// step b-4).
+template <int OP, bool A128, int MODE>
+__device__ __forceinline__ int32_t dom_step(const DomCtx& cx, int32_t s2, int32_t s3, int32_t s4, int32_t m1,
+                                            int32_t m2, int32_t m3, int32_t& p1, int32_t& x1) {
+  using S = Sel<OP>;
+  const int lane = cx.lane;
+  int32_t r;
+  if (A128) {
+    r = S::f(S::f(s4, m3), m2);
+  } else {
+    const int32_t t2 = __shfl_sync(0xffffffffu, s2, cx.L0);
+    const int32_t t3 = __shfl_sync(0xffffffffu, s3, cx.L0);
+    const int32_t t4 = __shfl_sync(0xffffffffu, s4, cx.L0);
+    r = cx.j0 == 2 ? t2 : (cx.j0 == 3 ? t3 : t4);
+    if (cx.j0 > 2) r = S::f(r, m2);
+    if (cx.j0 > 3) r = S::f(r, m3);
+  }
+  const int32_t t1 = __shfl_sync(0xffffffffu, p1, cx.lg);
+  r = S::f(r, lane < cx.g ? t1 : m1);
+  if (MODE == 0) {  // F-terms reaching step b-1
+    for (uint32_t f = cx.F; f; f &= f - 1) {
+      const int a = __ffs(f) - 1;
+      const int32_t v = __shfl_sync(0xffffffffu, x1, (32 + lane - a) & 31);
+      if (a > lane) r = S::f(r, v);
+    }
+  }
+  const int32_t Bp = scan_prefix<OP>(r, lane);
+  int32_t x;
+  if (MODE == 1) {
+    x = Bp;
+  } else {
+    x = r;
+    if (cx.h < 32) {
+      const int32_t v = __shfl_sync(0xffffffffu, Bp, (lane - cx.h) & 31);
+      if (lane >= cx.h) x = S::f(x, v);
+    }
+    if (MODE == 0) {
+      for (uint32_t dm = cx.D; dm; dm &= dm - 1) {
+        const int d = __ffs(dm) - 1;
+        const int32_t v = __shfl_sync(0xffffffffu, r, (lane - d) & 31);
+        if (d <= lane) x = S::f(x, v);
+      }
+    }
+  }
+  p1 = Bp;
+  x1 = x;
+  return scan_suffix<OP>(x, lane);
+}
+
+template <int OP, bool A128, int MODE>
+__device__ __forceinline__ void dom_loop(const DomCtx& cx, int64_t nfull, int64_t cells, int64_t* op, int32_t x1,
+                                         int32_t p1, int32_t q0, int32_t q1, int32_t q2, int32_t q3, int32_t mq0,
+                                         int32_t mq1, int32_t mq2, int32_t mq3) {
+  // slots hold steps (b-1, b-2, b-3, b-4) = (q0, q1, q2, q3) at the top of
+  // each unrolled group; each step overwrites the oldest slot
+  int64_t b = 0;
+#define DOM_STEP(A, B, C, Dq, MA, MB, MC, MD)                                    \
+  Dq = dom_step<OP, A128, MODE>(cx, B, C, Dq, MA, MB, MC, p1, x1);             \
+  MD = __shfl_sync(0xffffffffu, Dq, 0);                                         \
+  op[32 * b] = (int64_t)x1;                                                     \
+  ++b;
+  for (; b + 4 <= nfull;) {
+    DOM_STEP(q0, q1, q2, q3, mq0, mq1, mq2, mq3)  // step b:   new in q3
+    DOM_STEP(q3, q0, q1, q2, mq3, mq0, mq1, mq2)  // step b+1: new in q2
+    DOM_STEP(q2, q3, q0, q1, mq2, mq3, mq0, mq1)  // step b+2: new in q1
+    DOM_STEP(q1, q2, q3, q0, mq1, mq2, mq3, mq0)  // step b+3: new in q0
+  }
+#undef DOM_STEP
+  for (; 32 * b < cells; ++b) {  // the rest (and a partial last step)
+    const int32_t sf = dom_step<OP, A128, MODE>(cx, q1, q2, q3, mq0, mq1, mq2, p1, x1);
+    q3 = q2;
+    q2 = q1;
+    q1 = q0;
+    q0 = sf;
+    mq3 = mq2;
+    mq2 = mq1;
+    mq1 = mq0;
+    mq0 = __shfl_sync(0xffffffffu, sf, 0);
+    if (32 * b + cx.lane < cells) op[32 * b] = (int64_t)x1;
+  }
+}
+
 constexpr int kWarps = 8;
 constexpr int kRing = 256;  // exact-phase ring per warp: a_1 presets + a_1 computed cells
 
@@ -167,61 +258,34 @@ __global__ void __launch_bounds__(32 * kWarps, 4) sdp_batch_dom(int64_t count, c
   for (int64_t c = a1 + lane; c < e0; c += 32) o[c] = (int64_t)ring[c];
   if (e0 >= n) return;
 
-  // register state: steps b-1 .. b-4 relative to the first fast step B0 = 2 a1
+  // register state: suffix minima of steps b-1 .. b-4 (slots q0..q3, rotated
+  // by unrolling four steps), their whole-step minima, step b-1's prefix
+  // minima and values; the first fast step is B0 = 2 a1
   const int B0 = 2 * a1;
   int32_t x1 = ring[B0 - 32 + lane];
-  int32_t sf1 = scan_suffix<OP>(x1, lane), sf2 = scan_suffix<OP>(ring[B0 - 64 + lane], lane);
-  int32_t sf3 = scan_suffix<OP>(ring[B0 - 96 + lane], lane), sf4 = scan_suffix<OP>(ring[B0 - 128 + lane], lane);
+  int32_t q0 = scan_suffix<OP>(x1, lane), q1 = scan_suffix<OP>(ring[B0 - 64 + lane], lane);
+  int32_t q2 = scan_suffix<OP>(ring[B0 - 96 + lane], lane), q3 = scan_suffix<OP>(ring[B0 - 128 + lane], lane);
+  int32_t mq0 = __shfl_sync(0xffffffffu, q0, 0), mq1 = __shfl_sync(0xffffffffu, q1, 0);
+  int32_t mq2 = __shfl_sync(0xffffffffu, q2, 0), mq3 = 0;
   int32_t p1 = scan_prefix<OP>(x1, lane);
-  int32_t m1 = __shfl_sync(0xffffffffu, sf1, 0), m2 = __shfl_sync(0xffffffffu, sf2, 0),
-          m3 = __shfl_sync(0xffffffffu, sf3, 0);
-  // window start c - a1 = B + l - a1: step j0 back, lane L0
-  const int j0 = (a1 - lane + 31) / 32;  // 2..4 (a1 >= 64)
-  const int L0 = (lane - a1) & 31;
-  const int lg = (32 + lane - g) & 31;   // lane of step b-1 where the window ends (l < g)
-
-  const int64_t nb = (n - B0 + 31) / 32;
+  DomCtx cx;
+  cx.j0 = (a1 - lane + 31) / 32;  // window start c - a1: step j0 back (2..4), lane L0
+  cx.L0 = (lane - a1) & 31;
+  cx.g = __shfl_sync(0xffffffffu, g, 0);
+  cx.lg = (32 + lane - cx.g) & 31;  // lane of step b-1 where the window ends (l < g)
+  cx.h = __shfl_sync(0xffffffffu, h, 0);
+  cx.F = __shfl_sync(0xffffffffu, F, 0);
+  cx.D = __shfl_sync(0xffffffffu, D, 0);
+  cx.lane = lane;
+  const int64_t nfull = (n - B0) / 32;  // whole steps; then at most one partial step
   int64_t* op = o + B0 + lane;
-  for (int64_t b = 0; b < nb; ++b, op += 32) {
-    // window part in earlier steps
-    const int32_t s2 = __shfl_sync(0xffffffffu, sf2, L0);
-    const int32_t s3 = __shfl_sync(0xffffffffu, sf3, L0);
-    const int32_t s4 = __shfl_sync(0xffffffffu, sf4, L0);
-    int32_t r = j0 == 2 ? s2 : (j0 == 3 ? s3 : s4);
-    if (j0 > 2) r = S::f(r, m2);
-    if (j0 > 3) r = S::f(r, m3);
-    const int32_t t1 = __shfl_sync(0xffffffffu, p1, lg);
-    r = S::f(r, lane < g ? t1 : m1);
-    // F-terms reaching step b-1
-    for (uint32_t f = F; f; f &= f - 1) {
-      const int a = __ffs(f) - 1;
-      const int32_t v = __shfl_sync(0xffffffffu, x1, (32 + lane - a) & 31);
-      if (a > lane) r = S::f(r, v);
-    }
-    // in-step closure
-    const int32_t Bp = scan_prefix<OP>(r, lane);
-    int32_t x = r;
-    if (h < 32) {
-      const int32_t v = __shfl_sync(0xffffffffu, Bp, (lane - h) & 31);
-      if (lane >= h) x = S::f(x, v);
-    }
-    for (uint32_t dm = D; dm; dm &= dm - 1) {
-      const int d = __ffs(dm) - 1;
-      const int32_t v = __shfl_sync(0xffffffffu, r, (lane - d) & 31);
-      if (d <= lane) x = S::f(x, v);
-    }
-    // shift the register window
-    const int32_t sf = scan_suffix<OP>(x, lane);
-    sf4 = sf3;
-    sf3 = sf2;
-    sf2 = sf1;
-    sf1 = sf;
-    m3 = m2;
-    m2 = m1;
-    m1 = __shfl_sync(0xffffffffu, sf, 0);
-    p1 = Bp;
-    x1 = x;
-    if (B0 + 32 * b + lane < n) *op = (int64_t)x;
+  const int mode = cx.g == 1 ? 1 : (cx.F == 0 && cx.D == 0 ? 2 : 0);
+  if (a1 == 128) {
+    if (mode == 1) dom_loop<OP, true, 1>(cx, nfull, n - B0, op, x1, p1, q0, q1, q2, q3, mq0, mq1, mq2, mq3);
+    else if (mode == 2) dom_loop<OP, true, 2>(cx, nfull, n - B0, op, x1, p1, q0, q1, q2, q3, mq0, mq1, mq2, mq3);
+    else dom_loop<OP, true, 0>(cx, nfull, n - B0, op, x1, p1, q0, q1, q2, q3, mq0, mq1, mq2, mq3);
+  } else {
+    dom_loop<OP, false, 0>(cx, nfull, n - B0, op, x1, p1, q0, q1, q2, q3, mq0, mq1, mq2, mq3);
   }
 }
 
