@@ -28,6 +28,7 @@
 #include "host_io.hpp"
 #include "sdp_rank.hpp"
 #include "sdp_batch_dom.hpp"
+#include "mcm_tournament.hpp"
 
 using namespace pipedp_dev;
 
@@ -170,7 +171,7 @@ bool plan_sdp_v2(int64_t n, int64_t k, int64_t a1, const int64_t* offs, SdpDispa
   // preference: enough fetchers (a fetcher serialises poll + L2 read per
   // batch), then near groups, then combiners (cheap per batch)
   const int nf_max = std::max(1, env_int("PIPEDP_SDP2_FETCH", 4));
-  const int nw_max = std::max(1, std::min(8, env_int("PIPEDP_SDP2_WRITERS", 1)));
+  const int nw_max = std::max(1, std::min(4, env_int("PIPEDP_SDP2_WRITERS", 1)));  // <= 4 progress counters
   const int ng_max = std::max(1, env_int("PIPEDP_SDP2_NEAR_GROUP", 2));
   const int nc_min = std::max(1, env_int("PIPEDP_SDP2_COMB", 2));
   int NWR = 1;
@@ -782,9 +783,8 @@ int mcm_smem_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split
 
 int mcm_execute(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t st) {
   P->launches = 0;
-  if (P->d.kernel == PIPEDP_MCM_TOURNAMENT) {
-    mcm_tournament<<<1, 1024, 0, st>>>(P->n, P->d_dims, cells, split);
-    CK(cudaGetLastError());
+  if (P->d.kernel == PIPEDP_MCM_TOURNAMENT) {  // the paper's method, diagonal-parallel (mcm_tournament.cu)
+    CK(pipedp_tour::launch(P->n, P->d_dims, cells, split, reinterpret_cast<unsigned*>(P->d_overflow + 2), st));
     P->launches = 1;
     P->last_bits = 64;
     return PIPEDP_OK;
@@ -1531,7 +1531,7 @@ int32_t pipedp_mcm_plan_create(int64_t batch, int64_t n, const int64_t* h_dims, 
   if (e == cudaSuccess) e = cudaMemcpy(P->d_p, p32.data(), sizeof(int32_t) * p32.size(), cudaMemcpyHostToDevice);
   if (e == cudaSuccess) e = cudaMalloc(&P->d_dims, sizeof(int64_t) * p32.size());
   if (e == cudaSuccess) e = cudaMemcpy(P->d_dims, h_dims, sizeof(int64_t) * p32.size(), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess) e = cudaMalloc(&P->d_overflow, sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&P->d_overflow, 4 * sizeof(int));  // + tournament grid barrier
   if (e == cudaSuccess) e = cudaMallocHost(&P->h_overflow, sizeof(int));
   if (e == cudaSuccess && d.kernel == PIPEDP_MCM_TILED) {
     const int64_t T = d.tile, TC = T * T;
@@ -1594,7 +1594,7 @@ int32_t pipedp_mcm_plan_describe(pipedp_mcm_plan_t P, char* name, size_t cap, in
   const bool square = mcm_square_bytes(P->n, (P->last_bits ? P->last_bits : P->d.bits) / 8) <= kSmemBudget &&
                       env_int("PIPEDP_MCM_SQUARE", 1) != 0;
   const char* nm = P->d.kernel == PIPEDP_MCM_SMEM         ? (square ? "mcm_smem_square" : "mcm_smem_cta")
-                   : P->d.kernel == PIPEDP_MCM_TOURNAMENT ? "mcm_tournament"
+                   : P->d.kernel == PIPEDP_MCM_TOURNAMENT ? "mcm_tournament_diag"
                    : (P->d.kernel == PIPEDP_MCM_TILED && P->last_bits != 64)
                        ? (P->d.tile == 32 ? "mcm_tiled_kernel<32>" : "mcm_tiled_kernel<64>")
                                                           : "mcm_wavefront";

@@ -218,60 +218,6 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-// -----------------------------------------------------------------------------
-// The paper's O(n^2 log n) comparison method: cells one
-// at a time in address order; the CTA evaluates the D terms of the cell in
-// parallel and reduces them in a ceil(log2 D)-level tournament with a barrier
-// per level.  Single CTA; the table lives in global memory.
-__global__ void __launch_bounds__(1024, 1)
-    mcm_tournament(int64_t n, const int64_t* __restrict__ g_dims, int64_t* __restrict__ cells,
-                   int64_t* __restrict__ split) {
-  __shared__ int64_t sv[1024];
-  __shared__ int32_t sj[1024];
-  const int tid = threadIdx.x, nt = blockDim.x;
-  const int64_t cc = n * (n + 1) / 2;
-  for (int64_t i = tid; i <= n; i += nt) {
-    cells[i] = 0;
-    split[i] = 0;
-  }
-  __syncthreads();
-  int64_t addr = n + 1;
-  for (int64_t D = 1; D < n; ++D) {
-    int P = 1;
-    while (P < D && P < nt) P <<= 1;
-    for (int64_t r = 1; r + D <= n; ++r, ++addr) {
-      const int64_t c = r + D;
-      McmBest<int64_t> best{INT64_MAX, 0};
-      if (tid < P) {
-        const int64_t prc = g_dims[r - 1] * g_dims[c];
-        for (int64_t j = tid + 1; j <= D; j += P) {
-          const int64_t cost = cells[mcm_dbase(j - 1, n) + r] + cells[mcm_dbase(D - j, n) + r + j] +
-                               prc * g_dims[r + j - 1];
-          mcm_take(best, cost, (int32_t)j);
-        }
-        sv[tid] = best.v;
-        sj[tid] = best.j;
-      }
-      __syncthreads();
-      for (int s = P >> 1; s > 0; s >>= 1) {  // tournament levels
-        if (tid < s) {
-          McmBest<int64_t> a{sv[tid], sj[tid]};
-          mcm_take(a, sv[tid + s], sj[tid + s]);
-          sv[tid] = a.v;
-          sj[tid] = a.j;
-        }
-        __syncthreads();
-      }
-      if (tid == 0) {
-        cells[addr] = sv[0];
-        split[addr] = sj[0];
-      }
-      __syncthreads();
-    }
-  }
-  (void)cc;
-}
-
 }  // namespace pipedp_dev
 
 namespace pipedp_dev {

@@ -106,7 +106,7 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
     out[i] = v;
   }
   if (tid == 0) {
-    *written_count = 0;
+    for (int w = 0; w < 4; ++w) written_count[w] = 0;
     for (int s = 0; s < 2 * kBatchBars + kMidSlots; ++s) mbar_init(&bars[s], 1);
     for (int s = 0; s < kNearSlots; ++s) mbar_init(&near_full[s], (unsigned)(NW > 0 ? NW : 1));
     for (int s = 0; s < kFetchSlots; ++s) mbar_init(&rem_full[s], 1);
@@ -232,7 +232,14 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
         // writer lag <= 48 batches: the ring slots about to be overwritten
         // (R/32 >= 64 batches back) are in HBM, and the writer never trails the
         // 64-entry barrier rings by a full cycle
-        wait_batches(written, b - 32);
+        // per-writer progress counters (writer w owns batches w, w + NWR, ...):
+        // polled here only every 16 batches, so a counter instead of an
+        // mbarrier phase per batch that nobody would wait on
+        const int64_t X = b - 32;
+        for (int w = 0; w < S.writers; ++w) {
+          const int need = X > w ? (int)((X - w + S.writers - 1) / S.writers) : 0;
+          while (ld_acquire_cta(written_count + w) < need) __nanosleep(32);
+        }
       }
       const int64_t c = a1 + 32 * b + lane;
       const uint32_t pos = ((uint32_t)c & (R - 1)) + R;
@@ -414,8 +421,9 @@ __device__ __forceinline__ void sdp_v2_finisher(const SdpV2Shape& S, const int64
       const int64_t c = a1 + 32 * b + lane;
       if (c < n) out[c] = (int64_t)ring[(uint32_t)c & (R - 1)];
       __syncwarp();
-      if (lane == 0) mbar_arrive(&written[b % kBatchBars]);
-      if (REMOTE && (++done % S.pub_every == 0 || b + NWR >= nb)) {
+      ++done;
+      if (lane == 0) st_release_cta(written_count + w, done);  // after the warp barrier: all lanes' stores
+      if (REMOTE && (done % S.pub_every == 0 || b + NWR >= nb)) {
         t0 = PROF_NOW();
         __syncwarp();
         // the warp barrier orders every lane's table stores before lane 0's
