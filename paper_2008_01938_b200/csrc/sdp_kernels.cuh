@@ -730,7 +730,12 @@ __device__ __forceinline__ void sdp_finisher(const SdpShape& S, const int64_t* _
       const int64_t c = a1 + 32 * b + lane;
       if (c < n) out[c] = (int64_t)ring[(uint32_t)c & (R - 1)];
       __syncwarp();
-      if (lane == 0) mbar_arrive(&written[b % kBatchBars]);
+      if (lane == 0) {
+        mbar_arrive(&written[b % kBatchBars]);
+        // the far warps poll only some phases: observe each phase here, so no
+        // phase of the barrier ring is left unobserved (count 1: completes at once)
+        mbar_wait(&written[b % kBatchBars], (unsigned)((b / kBatchBars) & 1));
+      }
       if (REMOTE && ((b + 1) % kPubEvery == 0 || b + 1 == nb)) {
         __threadfence();
         __syncwarp();
@@ -1031,6 +1036,7 @@ __global__ void __launch_bounds__(256, 5)
       xm2 = xm1;
       xm1 = acc;
     }
+    __syncwarp();  // every lane's ring reads of this batch before any lane's writes
     if (c < n) {
       ring[pos - R] = acc;
       ring[pos] = acc;
