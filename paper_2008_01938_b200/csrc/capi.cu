@@ -29,6 +29,7 @@
 #include "sdp_rank.hpp"
 #include "sdp_batch_dom.hpp"
 #include "mcm_tournament.hpp"
+#include "sdp_cluster.hpp"
 
 using namespace pipedp_dev;
 
@@ -65,6 +66,8 @@ struct SdpDispatch {
   int64_t chunk_len;  // chunk length L (a multiple of 32 with few set bits: square-and-multiply)
   int method;   // 0 pipeline, 1 the paper's tournament (prefix), 2 the paper's naive method
   SdpV2Shape s2;
+  bool cluster = false;  // one instance over a thread-block cluster (sdp_cluster.cu)
+  pipedp_cluster::ClusterPlan cplan{};
 };
 
 // value width and associativity from the init values (see common.cuh)
@@ -247,6 +250,7 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
     return fail(PIPEDP_ERR_UNSUPPORTED, "a_1=%lld exceeds the 32-bit byte-offset range of the kernels",
                 (long long)a1);
   d->op = op;
+  d->cluster = false;
   sdp_value_class(op, init, batch * a1, &d->bits, &d->assoc);
   const size_t vb = d->bits / 8;
   SdpShape& s = d->shape;
@@ -319,6 +323,16 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
     return PIPEDP_OK;
   }
   d->v2 = false;
+  if (batch == 1 && d->assoc && d->bits == 32 && op != PIPEDP_OP_SATURATING_ADD &&
+      env_int("PIPEDP_SDP_CLUSTER", 1) != 0) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess &&
+        pipedp_cluster::plan(offsets, (int32_t)k, (int32_t)a1, n, op, dev, &d->cplan)) {
+      d->cluster = true;
+      return PIPEDP_OK;
+    }
+    (void)cudaGetLastError();
+  }
   if (batch == 1 && d->assoc && !(op == PIPEDP_OP_MODULAR_ADD && d->bits == 64) &&
       env_int("PIPEDP_SDP_V2", 1) != 0 && plan_sdp_v2(n, k, a1, offsets, d))
     return PIPEDP_OK;
@@ -459,6 +473,10 @@ int launch_sdp_t(const SdpDispatch& d, int64_t batch, const int64_t* offs, const
     CK(cudaGetLastError());
     return PIPEDP_OK;
   }
+  if (ASSOC && d.cluster) {
+    CK(pipedp_cluster::launch(d.cplan, offs, init, out, st));
+    return PIPEDP_OK;
+  }
   if (ASSOC && d.v2 && !(OP == kModAdd && sizeof(T) == 8)) return launch_v2<OP, T>(d, offs, init, out, rm, st);
   if (d.jump) return launch_jump<OP>(d, offs, init, out, st);
   if (d.serial) {
@@ -497,6 +515,7 @@ int launch_sdp(const SdpDispatch& d, int64_t batch, const int64_t* offs, const i
 const char* sdp_kernel_name(const SdpDispatch& d) {
   if (d.method == 1 && d.assoc) return "sdp_tournament";
   if (d.method == 2 && d.assoc) return "sdp_naive";
+  if (d.cluster) return "sdp_cluster_kernel";
   if (d.jump) return "sdp_jump";
   if (d.serial) return "sdp_serial_thread";
   if (d.v2) return d.remote ? "sdp_v2_multi" : "sdp_v2_cta";

@@ -340,3 +340,27 @@ def test_config2_full_table_digest(gpu):
         d_cells.fill_(-1)
         plan.execute(d_init.data_ptr(), d_cells.data_ptr(), torch.cuda.current_stream().cuda_stream)
         assert f"{gpu.table_digest(d_cells.cpu().numpy()):016x}" == g["digest"]
+
+
+@pytest.mark.parametrize("op,n,k,cap", [("min", 100003, 1024, 4096), ("max", 70001, 700, 12000),
+                                        ("modular-add", 50017, 2000, 8000), ("min", 29103, 7168, 14336)])
+def test_cluster_pipeline(gpu, oracle, op, n, k, cap):
+    """sdp_cluster_kernel: one instance over a 16-CTA cluster, the far offsets
+    folded by producer CTAs from rings fed through DSMEM (st.async with
+    mbarrier transaction bytes).  Forced by disabling the chunked mode."""
+    import os
+    inst = gpu.generate_sdp(n=n, k=k, op=op, seed=n % 97, a1_cap=cap)
+    old = os.environ.get("PIPEDP_SDP_CHUNKED")
+    os.environ["PIPEDP_SDP_CHUNKED"] = "0"
+    try:
+        plan = gpu.SdpPlan(1, n, inst.k, inst.a1, inst.offsets, inst.init, op, device=0)
+        assert plan.describe()[0] == "sdp_cluster_kernel"
+        plan.close()
+        t = gpu.solve_sequential(inst)
+    finally:
+        if old is None:
+            del os.environ["PIPEDP_SDP_CHUNKED"]
+        else:
+            os.environ["PIPEDP_SDP_CHUNKED"] = old
+    want, _ = oracle.sdp_solve(inst.offsets, inst.init, n, op)
+    assert np.array_equal(t.cells, want)
