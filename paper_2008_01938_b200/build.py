@@ -74,7 +74,7 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
     if force or _newer(target, cuda_srcs):
         # one object per top-level translation unit, compiled in parallel, then
         # one shared library (CUDA runtime linked statically)
-        tus = [os.path.join(CSRC, f) for f in ("capi.cu", "engine.cu", "sdp_rank.cu", "sdp_batch_dom.cu", "mcm_tournament.cu", "sdp_cluster.cu")]
+        tus = [os.path.join(CSRC, f) for f in ("capi.cu", "engine.cu", "sdp_rank.cu", "sdp_batch_dom.cu", "mcm_tournament.cu", "sdp_cluster.cu", "mcm_batch.cu")]
         flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr",
                  "-Xptxas", "-v" if verbose else "-O3", "-Xcompiler", "-fPIC,-O3",
                  *(["-DPIPEDP_PROFILE"] if profile else []), "-I", INCLUDE]

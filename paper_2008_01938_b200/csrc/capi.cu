@@ -30,6 +30,7 @@
 #include "sdp_batch_dom.hpp"
 #include "mcm_tournament.hpp"
 #include "sdp_cluster.hpp"
+#include "mcm_batch.hpp"
 
 using namespace pipedp_dev;
 
@@ -764,6 +765,13 @@ size_t mcm_square_bytes(int64_t n, size_t vb) {
 int mcm_smem_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split, cudaStream_t st) {
   const int64_t n = P->n;
   const size_t sq = mcm_square_bytes(n, bits / 8);
+  if (bits == 32 && n <= pipedp_mcmb::kMaxN && P->batch > 1 && env_int("PIPEDP_MCM_BATCH_WARP", 0) != 0) {
+    // one warp per instance, row and column copies (mcm_batch.cu); opt-in:
+    // C5a 3.85 ms against 3.19 for the square-table CTAs (8 warps per SM at
+    // 25 KB of shared memory per instance: latency-bound)
+    CK(pipedp_mcmb::launch((int32_t)n, P->batch, P->d_dims, cells, split, P->d_overflow, st));
+    return PIPEDP_OK;
+  }
   if (sq <= kSmemBudget && env_int("PIPEDP_MCM_SQUARE", 1) != 0) {
     // row-major square table: incremental operand addresses (mcm_smem_square)
     // two warps for n <= 96: the short diagonals keep them busy (C5a: 3.96 ->
@@ -1612,7 +1620,9 @@ int32_t pipedp_mcm_plan_describe(pipedp_mcm_plan_t P, char* name, size_t cap, in
   if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
   const bool square = mcm_square_bytes(P->n, (P->last_bits ? P->last_bits : P->d.bits) / 8) <= kSmemBudget &&
                       env_int("PIPEDP_MCM_SQUARE", 1) != 0;
-  const char* nm = P->d.kernel == PIPEDP_MCM_SMEM         ? (square ? "mcm_smem_square" : "mcm_smem_cta")
+  const int lb = P->last_bits ? P->last_bits : P->d.bits;
+  const bool bwarp = lb == 32 && P->n <= pipedp_mcmb::kMaxN && P->batch > 1 && env_int("PIPEDP_MCM_BATCH_WARP", 0) != 0;
+  const char* nm = P->d.kernel == PIPEDP_MCM_SMEM         ? (bwarp ? "mcm_batch_warp" : square ? "mcm_smem_square" : "mcm_smem_cta")
                    : P->d.kernel == PIPEDP_MCM_TOURNAMENT ? "mcm_tournament_diag"
                    : (P->d.kernel == PIPEDP_MCM_TILED && P->last_bits != 64)
                        ? (P->d.tile == 32 ? "mcm_tiled_kernel<32>" : "mcm_tiled_kernel<64>")

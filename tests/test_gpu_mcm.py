@@ -164,3 +164,13 @@ def test_batch_beyond_shared_memory(gpu, oracle, n, lo, hi):
             wc, _, ws = oracle.mcm_solve(inst.dims)
             assert np.array_equal(c[b * size:(b + 1) * size], wc)
             assert np.array_equal(s[b * size:(b + 1) * size], ws)
+
+
+def test_batch_warp_kernel_opt_in(gpu, oracle, monkeypatch):
+    # mcm_batch_warp (one warp per n <= 64 instance, row + column copies): opt-in
+    monkeypatch.setenv("PIPEDP_MCM_BATCH_WARP", "1")
+    for n in (2, 17, 33, 64):
+        insts = [gpu.McmInstance(oracle.generate_mcm(n, 900 + i, 1, 100)) for i in range(20)]
+        for inst, (t, split) in zip(insts, gpu.solve_mcm_batch(insts)):
+            wc, _, ws = oracle.mcm_solve(inst.dims)
+            assert np.array_equal(t.cells, wc) and np.array_equal(split, ws)
