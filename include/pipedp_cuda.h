@@ -137,6 +137,11 @@ int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t plan, char* name, size_t name
                                  int32_t* value_bits, int32_t* launches);
 /* switch a single-instance plan to the paper's prefix / naive method */
 int32_t pipedp_sdp_plan_set_method(pipedp_sdp_plan_t plan, int32_t method);
+/* chunked mode phase timing (CUDA events on the execute stream): set_timing
+ * resets and enables; phase_ms returns the accumulated milliseconds of
+ * [0] matrix powers, [1] entry-state chain, [2] chunk batch over `runs` executes */
+int32_t pipedp_sdp_plan_set_timing(pipedp_sdp_plan_t plan, int32_t on);
+int32_t pipedp_sdp_plan_phase_ms(pipedp_sdp_plan_t plan, double* out3, int64_t* runs);
 int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t plan);
 
 /* ---- MCM, host buffers ------------------------------------------------------

@@ -55,6 +55,7 @@ EXPORTS = (
     "pipedp_op_latency_ns", "pipedp_mcm_bruteforce", "pipedp_sdp_solve_method",
     "pipedp_sdp_plan_set_method", "pipedp_mcm_engine", "pipedp_sdp_engine", "pipedp_engine_records",
     "pipedp_engine_hazards", "pipedp_engine_conflicts", "pipedp_engine_stall_heads", "pipedp_engine_free",
+    "pipedp_sdp_plan_set_timing", "pipedp_sdp_plan_phase_ms",
 )
 ENGINE_TRACE, ENGINE_ANALYSIS = 1, 2
 TRACE_LIMIT = 1 << 28  # engine.cu kMaxRecords
@@ -141,6 +142,8 @@ def lib():
     L.pipedp_sdp_solve_method.argtypes = [_i64p, C.c_int64, _i64p, C.c_int64, C.c_int64, C.c_int32,
                                           C.c_int32, _i64p, _u8p]
     L.pipedp_sdp_plan_set_method.argtypes = [C.c_void_p, C.c_int32]
+    L.pipedp_sdp_plan_set_timing.argtypes = [C.c_void_p, C.c_int32]
+    L.pipedp_sdp_plan_phase_ms.argtypes = [C.c_void_p, C.POINTER(C.c_double), C.POINTER(C.c_int64)]
     _i32p = C.POINTER(C.c_int32)
     L.pipedp_mcm_engine.argtypes = [_i64p, C.c_int64, C.c_int32, C.c_int32, _i64p, C.POINTER(EngineSummary),
                                     C.POINTER(C.c_void_p)]
@@ -609,6 +612,17 @@ class SdpPlan:
     def set_method(self, method: int) -> None:
         """SDP_PIPELINE (default), SDP_PREFIX or SDP_NAIVE (the paper's methods)."""
         _check(lib().pipedp_sdp_plan_set_method(self.handle, method))
+
+    def set_timing(self, on: bool = True) -> None:
+        """chunked mode: record per-phase CUDA events on the execute stream"""
+        _check(lib().pipedp_sdp_plan_set_timing(self.handle, int(on)))
+
+    def phase_ms(self):
+        """accumulated (powers, chain, chunk batch) ms and the number of executes"""
+        out = (C.c_double * 3)()
+        runs = C.c_int64()
+        _check(lib().pipedp_sdp_plan_phase_ms(self.handle, out, C.byref(runs)))
+        return tuple(out), runs.value
 
     def describe(self):
         buf = C.create_string_buffer(64)

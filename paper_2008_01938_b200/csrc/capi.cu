@@ -591,6 +591,14 @@ struct pipedp_sdp_plan {
   // the fallback instances run beside the dominance kernel (fork / join)
   cudaStream_t side = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // phase timing of the chunked mode (pipedp_sdp_plan_set_timing): events at
+  // the start, after the matrix powers, after the entry-state chain, after
+  // the chunk batch; accumulated per phase until read
+  bool timing = false;
+  cudaEvent_t ev_phase[4] = {nullptr, nullptr, nullptr, nullptr};
+  double phase_ms[3] = {0, 0, 0};
+  int64_t phase_runs = 0;
+  bool phase_pending = false;
 };
 
 // ================================================================== MCM ===
@@ -1099,6 +1107,20 @@ int32_t pipedp_sdp_plan_create(int64_t batch, int64_t n, int64_t k, int64_t a1,
   return PIPEDP_OK;
 }
 
+// fold the last recorded run's phase durations into the accumulators
+static int phase_collect(pipedp_sdp_plan_t P) {
+  if (!P->phase_pending) return PIPEDP_OK;
+  CK(cudaEventSynchronize(P->ev_phase[3]));
+  for (int i = 0; i < 3; ++i) {
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, P->ev_phase[i], P->ev_phase[i + 1]));
+    P->phase_ms[i] += ms;
+  }
+  ++P->phase_runs;
+  P->phase_pending = false;
+  return PIPEDP_OK;
+}
+
 // Chunked mode (sdp_chunked.cuh): Q = M^Lc by boolean squarings, the chunk
 // entry states by Q (.) state, then all chunks as one batch.
 extern "C++" {
@@ -1107,6 +1129,12 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
                                int64_t split_at = 0, cudaEvent_t split_event = nullptr) {
   const int32_t W = P->W, a1 = (int32_t)P->a1;
   const size_t mat = (size_t)64 * W * W;
+  if (P->timing) {
+    TRY(phase_collect(P));  // the previous run's phases
+    for (auto& e : P->ev_phase)
+      if (!e) CK(cudaEventCreate(&e));
+    CK(cudaEventRecord(P->ev_phase[0], st));
+  }
   unsigned long long *X = P->d_bm, *XT = X + mat, *Z = XT + mat, *ZT = Z + mat;
   CK(cudaMemsetAsync(X, 0, sizeof(unsigned long long) * 2 * mat, st));
   bm_build<<<1, 1024, 0, st>>>(P->d_offsets, (int32_t)P->k, a1, W, X, XT);
@@ -1165,6 +1193,7 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
   int64_t* E[2] = {P->d_E, P->d_E + 64 * W};
   CK(cudaFuncSetAttribute(bm_matvec<OP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)(sizeof(int64_t) * 64 * W)));
+  if (P->timing) CK(cudaEventRecord(P->ev_phase[1], st));
   bm_state0<<<(a1 + 255) / 256, 256, 0, st>>>(d_init, a1, E[0], P->d_cinit);
   const int B = P->G >= 64 ? 16 : 1;  // two-level chain block
   if (env_int("PIPEDP_SDP_CHAIN_PERSISTENT", 1) != 0) {
@@ -1204,6 +1233,7 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
     CK(cudaGetLastError());
   }
   CK(cudaMemcpyAsync(d_cells, d_init, sizeof(int64_t) * a1, cudaMemcpyDeviceToDevice, st));
+  if (P->timing) CK(cudaEventRecord(P->ev_phase[2], st));
   // chunks [0, gs) then [gs, G), each gathered into the instance's table; an
   // event after the first range lets the host copy it out while the second runs
   const int64_t gs = split_at > 0 && split_at < P->G ? split_at : P->G;
@@ -1235,6 +1265,10 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
                          sizeof(int64_t) * last, cudaMemcpyDeviceToDevice, st));
     }
     if (g0 == 0 && split_event) CK(cudaEventRecord(split_event, st));
+  }
+  if (P->timing) {
+    CK(cudaEventRecord(P->ev_phase[3], st));
+    P->phase_pending = true;
   }
   return PIPEDP_OK;
 }
@@ -1401,6 +1435,23 @@ int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, in
   return PIPEDP_OK;
 }
 
+int32_t pipedp_sdp_plan_set_timing(pipedp_sdp_plan_t P, int32_t on) {
+  if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
+  P->timing = on != 0;
+  P->phase_ms[0] = P->phase_ms[1] = P->phase_ms[2] = 0;
+  P->phase_runs = 0;
+  P->phase_pending = false;
+  return PIPEDP_OK;
+}
+
+int32_t pipedp_sdp_plan_phase_ms(pipedp_sdp_plan_t P, double* out3, int64_t* runs) {
+  if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
+  TRY(phase_collect(P));
+  for (int i = 0; i < 3; ++i) out3[i] = P->phase_ms[i];
+  if (runs) *runs = P->phase_runs;
+  return PIPEDP_OK;
+}
+
 int32_t pipedp_sdp_plan_set_method(pipedp_sdp_plan_t P, int32_t method) {
   if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
   if (method < PIPEDP_SDP_PIPELINE || method > PIPEDP_SDP_NAIVE)
@@ -1433,6 +1484,8 @@ int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t P) {
   cudaFree(P->d_sorted);
   cudaFree(P->d_dinfo);
   if (P->side) cudaStreamDestroy(P->side);
+  for (auto e : P->ev_phase)
+    if (e) cudaEventDestroy(e);
   if (P->ev_fork) cudaEventDestroy(P->ev_fork);
   if (P->ev_join) cudaEventDestroy(P->ev_join);
   delete P->rank;
