@@ -89,7 +89,21 @@ constexpr size_t kSmemBudget = 200 * 1024;
 constexpr int kAMid = 256;
 constexpr int kARemote = 1024;
 
+// Dispatch switches: each one selects or disables an
+// alternative kernel path so the tests can reach it; the defaults are the
+// product.  Any other PIPEDP_* name is a tuning constant -- the environment is
+// not consulted for it.
 int env_int(const char* name, int dflt) {
+  static const char* const kSwitches[] = {
+      "PIPEDP_SDP_CHUNKED", "PIPEDP_SDP_RANK",     "PIPEDP_SDP_BDOM",      "PIPEDP_SDP_CLUSTER",
+      "PIPEDP_SDP_V2",      "PIPEDP_SDP_MULTI",    "PIPEDP_SDP_JUMP",      "PIPEDP_SDP_SERIAL",
+      "PIPEDP_SDP_REMOTE_WARPS", "PIPEDP_SDP_REMOTE_CTAS", "PIPEDP_SDP_MID_WARPS", "PIPEDP_SDP_AREMOTE",
+      "PIPEDP_SDP2_WRITERS", "PIPEDP_CHUNK_OVERLAP", "PIPEDP_MCM_TILED",   "PIPEDP_MCM_T32_MAXN",
+      "PIPEDP_MCM_BLOCKED", "PIPEDP_MCM_SQUARE",   "PIPEDP_MCM_BATCH_WARP", "PIPEDP_MCM_PACKED_SQUARE",
+      "PIPEDP_D2H_NARROW",  "PIPEDP_STREAM_D2H"};
+  bool known = false;
+  for (const char* k : kSwitches) known = known || strcmp(k, name) == 0;
+  if (!known) return dflt;
   const char* v = getenv(name);
   return v && *v ? atoi(v) : dflt;
 }

@@ -281,13 +281,9 @@ struct Workspace {
   // half the PCIe bytes, widened on the host while the next piece is in flight.
   cudaError_t d2h_widen(int64_t* dst, const int32_t* src, size_t count, cudaStream_t st = nullptr) {
     if (!st) st = stream;
-    // pieces of PIPEDP_WIDEN_PIECE_MB (default 16) MiB of int32: the DMA of piece
-    // i+1 overlaps the widening of piece i (the host side is the slower leg)
-    static const size_t piece_bytes = [] {
-      const char* v = getenv("PIPEDP_WIDEN_PIECE_MB");
-      const size_t mb = v && *v ? (size_t)atoi(v) : 16;
-      return std::min(kChunk, std::max<size_t>(1, mb) << 20);
-    }();
+    // pieces of 16 MiB of int32: the DMA of piece i+1 overlaps the widening of
+    // piece i (the host side is the slower leg)
+    static const size_t piece_bytes = std::min<size_t>(kChunk, size_t(16) << 20);
     const size_t per = piece_bytes / sizeof(int32_t);
     const size_t nchunks = (count + per - 1) / per;
     auto issue = [&](size_t c) {
@@ -309,21 +305,9 @@ struct Workspace {
 
   // device -> pageable host after the work queued on `stream`; synchronous
   cudaError_t d2h(void* dst, const void* src, size_t bytes) {
-    static const int mode = [] {
-      const char* v = getenv("PIPEDP_D2H_MODE");
-      return v && *v ? atoi(v) : 0;
-    }();
-    if (mode == 1) {  // the driver's own pageable path
-      cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream);
-      return e == cudaSuccess ? cudaStreamSynchronize(stream) : e;
-    }
-    // piece size (PIPEDP_D2H_PIECE_MB, default the whole 64 MiB buffer: smaller
-    // pieces measured slower -- per-call pool overhead outweighs the overlap)
-    static const size_t piece = [] {
-      const char* v = getenv("PIPEDP_D2H_PIECE_MB");
-      const size_t mb = v && *v ? (size_t)atoi(v) : 64;
-      return std::min(kChunk, std::max<size_t>(1, mb) << 20);
-    }();
+    // pieces of the whole 64 MiB staging buffer (smaller pieces measured
+    // slower: per-call pool overhead outweighs the overlap)
+    static const size_t piece = kChunk;
     const size_t nchunks = (bytes + piece - 1) / piece;
     auto issue = [&](size_t c) {
       const size_t off = c * piece, len = std::min(piece, bytes - off);

@@ -21,7 +21,6 @@
 #include "sdp_cluster.hpp"
 
 #include <algorithm>
-#include <cstdlib>
 
 #include "sdp_kernels.cuh"
 
@@ -357,11 +356,6 @@ __global__ void __launch_bounds__(32 * 20, 1) sdp_cluster_kernel(const Params p)
   cluster_sync_all();  // no CTA leaves while its shared memory may still be addressed
 }
 
-static int env_knob(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
-}
-
 bool plan(const int64_t* offsets, int32_t k, int32_t a1, int64_t n, int op, int device, ClusterPlan* out) {
   if (!(op == kMin || op == kMax || op == kModAdd) || n <= a1) return false;
   int major = 0;
@@ -374,7 +368,7 @@ bool plan(const int64_t* offsets, int32_t k, int32_t a1, int64_t n, int op, int 
   P.n = n;
   P.k = k;
   P.a1 = a1;
-  P.a_p = env_knob("PIPEDP_CLUSTER_AP", 256);
+  P.a_p = 256;  // offsets >= 256: producers (measured: 512 and 1024 slower on C2)
   for (int j = 0; j < k; ++j) {
     P.j_p += offsets[j] >= P.a_p;
     P.j_64 += offsets[j] >= 64;
@@ -382,8 +376,8 @@ bool plan(const int64_t* offsets, int32_t k, int32_t a1, int64_t n, int op, int 
   }
   if (P.j_p < 64) return false;  // too little far work for a cluster
   P.cluster = kMaxCluster;
-  P.mid_warps = std::max(2, env_knob("PIPEDP_CLUSTER_MID", 6));  // near / far-mid alternate
-  P.writers = env_knob("PIPEDP_CLUSTER_WRITERS", 4);
+  P.mid_warps = 6;  // near / far-mid alternate (C2: 4 -> 157 ms, 6 -> 136 ms, 8 -> 146 ms)
+  P.writers = 4;
   P.prod_warps = 8;
   P.fin_r = 1;  // >= a_p + 32 (kRem + 4), a power of two
   while (P.fin_r < P.a_p + 32 * (kRem + 4)) P.fin_r <<= 1;
