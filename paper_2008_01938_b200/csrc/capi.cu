@@ -1347,8 +1347,30 @@ int32_t pipedp_sdp_plan_execute(pipedp_sdp_plan_t P, const int64_t* d_init, int6
 // prefix in `published` (batches of 32 cells past a1): copy the table out
 // while the kernel is still producing its tail.
 static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* W,
-                                   const int64_t* d_init, int64_t* d_cells, int64_t* cells_out) {
+                                   const int64_t* d_init, int64_t* d_cells, int64_t* cells_out,
+                                   const int64_t* h_init) {
   const size_t bytes = sizeof(int64_t) * P->batch * P->n;
+  if (P->rank && P->d.method == PIPEDP_SDP_PIPELINE && bytes >= kHostCopyBig && h_init &&
+      env_int("PIPEDP_D2H_NARROW", 1) != 0) {
+    // chunked min / max on ranks: the cells leave the device as 16-bit ranks
+    // (2 B per cell) and become values on the host by a lookup into the
+    // sorted init values -- the same multiset the device sorted, so the same
+    // rank -> value map; the preset prefix is the caller's init
+    void* d_rank = nullptr;
+    CK(W->buffer(4, sizeof(uint16_t) * (size_t)P->n + 16, &d_rank));
+    P->rank->out_rank = static_cast<uint16_t*>(d_rank);
+    const int32_t rc = P->d.op == PIPEDP_OP_MAX ? sdp_chunked_run<kMax>(P, d_init, d_cells, W->stream)
+                                                : sdp_chunked_run<kMin>(P, d_init, d_cells, W->stream);
+    P->rank->out_rank = nullptr;
+    TRY(rc);
+    std::vector<int64_t> sorted(h_init, h_init + P->a1);
+    std::sort(sorted.begin(), sorted.end());
+    pipedp_host::parallel_prefault(cells_out, bytes);  // overlaps the kernels
+    memcpy(cells_out, h_init, sizeof(int64_t) * P->a1);
+    CK(W->d2h_lookup16(cells_out + P->a1, static_cast<const uint16_t*>(d_rank) + P->a1,
+                       (size_t)(P->n - P->a1), sorted.data()));
+    return PIPEDP_OK;
+  }
   // (chunked plans never run the remote pipeline: no progress counters)
   if (!(P->d.remote && !P->d.chunked && P->batch == 1 && P->d.method == PIPEDP_SDP_PIPELINE) ||
       bytes < (64u << 20) ||
@@ -1552,7 +1574,7 @@ static int32_t sdp_solve_host(int64_t batch, int64_t n, int64_t k, int64_t a1,
   CK(W->buffer(0, sizeof(int64_t) * batch * a1, &d_init));
   CK(W->buffer(1, sizeof(int64_t) * batch * n, &d_cells));
   CK(W->h2d(d_init, init, sizeof(int64_t) * batch * a1));
-  return sdp_execute_to_host(P, W, (const int64_t*)d_init, (int64_t*)d_cells, cells_out);
+  return sdp_execute_to_host(P, W, (const int64_t*)d_init, (int64_t*)d_cells, cells_out, init);
 }
 
 int32_t pipedp_sdp_solve(const int64_t* offsets, int64_t k, const int64_t* init,

@@ -180,7 +180,10 @@ __global__ void __launch_bounds__(32 * 16) chunk_rank_kernel(const __grid_consta
       h16[2 * (w2 + R2) + 1] = (uint16_t)acc;
       __syncwarp();
       if (lane == 0) mbar_arrive(&batch_done[b % kBars]);
-      if (c < e) p.out[c] = __ldg(p.sorted + acc);
+      if (c < e) {
+        if (p.out_rank) p.out_rank[c] = (uint16_t)acc;  // 2 B per cell for the trip to the host
+        else p.out[c] = __ldg(p.sorted + acc);
+      }
       w += 32;
       if (w >= R2) w -= R2;
       w2 += 32;

@@ -29,6 +29,7 @@ struct ChunkRankParams {
   const int64_t* cinit;   // [G][a1] chunk entry states (values)
   const int64_t* sorted;  // [a1] init values ascending: rank -> value
   int64_t* out;           // the table
+  uint16_t* out_rank;     // nullable: write each cell's rank here instead (host-bound solves)
   const int64_t* offsets; // [k] the offsets (device), for the chain's masks
   int32_t nob[kMaxK];     // -4 a_j: byte offset of offset a_j in a ring of 32-bit words
 };
