@@ -21,8 +21,29 @@ while time.time() - t0 < budget:
     it += 1
     seed = int(rng.integers(1 << 31))
     r = np.random.default_rng(seed)
-    kind = r.choice(["sdp_small", "sdp_mid", "sdp_big", "mcm", "sdp_batch"], p=[0.25, 0.3, 0.15, 0.15, 0.15])
-    if kind == "sdp_batch":
+    kind = r.choice(["sdp_small", "sdp_mid", "sdp_big", "mcm", "sdp_batch", "sdp_cluster"],
+                    p=[0.2, 0.25, 0.1, 0.15, 0.15, 0.15])
+    if kind == "sdp_cluster":
+        # one instance over the thread-block cluster (chunked mode off for min/max)
+        import os
+        op = ["min", "max", "modular-add"][int(r.integers(3))]
+        a1 = int(r.integers(300, 20000))
+        k = int(r.integers(70, min(a1 - 1, 3000)))
+        n = int(r.integers(a1 + 1, 400000))
+        rest = r.choice(np.arange(1, a1), k - 1, replace=False)
+        offs = np.concatenate([[a1], np.sort(rest)[::-1]]).astype(np.int64)
+        init = r.integers(-(1 << 30), 1 << 30, a1) if op != "modular-add" else r.integers(0, 2**31 - 1, a1)
+        os.environ["PIPEDP_SDP_CHUNKED"] = "0"
+        try:
+            t = pd.solve_sequential(pd.SdpInstance(n, offs, init, op))
+            plan = pd.SdpPlan(1, n, k, a1, offs, init, op)
+            name = plan.describe()[0].split("[")[0]
+            plan.close()
+        finally:
+            del os.environ["PIPEDP_SDP_CHUNKED"]
+        want, _ = orc.sdp_solve(offs, init, n, op)
+        ok = np.array_equal(t.cells, want)
+    elif kind == "sdp_batch":
         # warp-per-instance batches (a_1 <= 128): the three sdp_batch_warp paths
         op = ["min", "max", "saturating-add", "modular-add"][int(r.integers(4))]
         a1 = int(r.integers(2, 129))
@@ -43,7 +64,10 @@ while time.time() - t0 < budget:
         for inst, t in zip(insts, pd.solve_sequential_batch(insts)):
             want, _ = orc.sdp_solve(inst.offsets, inst.init, inst.n, op)
             ok = ok and np.array_equal(t.cells, want)
-        name = "sdp_batch"
+        plan = pd.SdpPlan(count, n, k, a1, np.concatenate([i.offsets for i in insts]),
+                          np.concatenate([i.init for i in insts]), op)
+        name = plan.describe()[0].split("[")[0]
+        plan.close()
     elif kind == "mcm":
         n = int(r.integers(2, 700))
         dims = orc.generate_mcm(n, seed % 1000, 1, int(r.choice([100, 322, 1290])))
