@@ -412,20 +412,24 @@ __device__ __forceinline__ IdemMasks idem_masks(const int32_t* offs, int k, int 
 }
 
 // General form: broadcast b_t, t = 0..31 (independent shuffles), fold into x
-// when t in T_l and into the next-batch accumulator when t in V_l.
+// when t in T_l and into the next-batch accumulator when t in V_l.  Four
+// accumulators per side (t mod 4), combined at the end: the 32 folds form four
+// independent chains of 8 instead of one chain of 32 (the batch's critical
+// path is the chain warp's closure latency); regrouping an idempotent,
+// commutative (x) changes nothing.
 template <int OP, typename T, int TT>
 struct IdemBcast {
-  __device__ __forceinline__ static void run(const T& b, T& x, T& nx, uint32_t mt, uint32_t mv) {
+  __device__ __forceinline__ static void run(const T& b, T* x, T* nx, uint32_t mt, uint32_t mv) {
     using O = SemiOp<OP, T>;
     const T v = shfl_idx(b, TT);
-    if (bit_at<32 - TT>(mt)) x = O::apply(x, v);  // bit TT
-    if (bit_at<32 - TT>(mv)) nx = O::apply(nx, v);
+    if (bit_at<32 - TT>(mt)) x[TT & 3] = O::apply(x[TT & 3], v);  // bit TT
+    if (bit_at<32 - TT>(mv)) nx[TT & 3] = O::apply(nx[TT & 3], v);
     IdemBcast<OP, T, TT + 1>::run(b, x, nx, mt, mv);
   }
 };
 template <int OP, typename T>
 struct IdemBcast<OP, T, 32> {
-  __device__ __forceinline__ static void run(const T&, T&, T&, uint32_t, uint32_t) {}
+  __device__ __forceinline__ static void run(const T&, T*, T*, uint32_t, uint32_t) {}
 };
 
 // acc: in b, out x.  nxt: out, the next batch's fold of this batch's cells.
@@ -442,10 +446,10 @@ __device__ __forceinline__ void idem_closure(T& acc, T& nxt, const IdemMasks& m)
     const T v = shfl_idx(acc, m.src < 0 ? 0 : m.src);
     nxt = m.src < 0 ? id : v;
   } else {
-    T x = id, nx = id;
+    T x[4] = {id, id, id, id}, nx[4] = {id, id, id, id};
     IdemBcast<OP, T, 0>::run(acc, x, nx, m.T, m.V);
-    acc = x;
-    nxt = nx;
+    acc = O::apply(O::apply(x[0], x[1]), O::apply(x[2], x[3]));
+    nxt = O::apply(O::apply(nx[0], nx[1]), O::apply(nx[2], nx[3]));
   }
 }
 
