@@ -315,7 +315,12 @@ int plan_sdp(int64_t batch, int64_t n, int64_t k, int64_t a1, const int64_t* off
     d->chunked = false;
     if (batch == 1 && (op == PIPEDP_OP_MIN || op == PIPEDP_OP_MAX) && a1 >= 64 && a1 <= 8192 &&
         env_int("PIPEDP_SDP_CHUNKED", 1) != 0) {
-      const int64_t slots = std::max(1, env_int("PIPEDP_SDP_CHUNKS", 2 * sm_count()));
+      // chunk CTAs per SM: two for the generic chunk pipeline; the rank
+      // kernel (k <= 4096) fits three when its pair ring is small enough
+      // (C2: 293 -> 443 chunks, 3.04 -> 2.96 ms measured)
+      const int64_t rank_smem = 8 * (a1 + 160) + 20 * 1024;
+      const int per_sm = k <= 4096 && 3 * rank_smem <= 220 * 1024 ? 3 : 2;
+      const int64_t slots = (int64_t)per_sm * sm_count();
       const int64_t lmin = std::max<int64_t>(4096, 8 * a1);
       int64_t target = std::max<int64_t>(lmin, (n - a1 + slots - 1) / slots);
       int64_t L = (target + 31) / 32;  // in units of 32 cells

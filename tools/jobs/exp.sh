@@ -1,5 +1,4 @@
-cp paper_2008_01938_b200/_lib/libpipedp_cuda.so /tmp/orig.so
-for v in orig ap128 ap192; do
+for v in orig s3 s4; do
   if [ $v != orig ]; then cp tools/libexp_$v.so paper_2008_01938_b200/_lib/libpipedp_cuda.so; fi
-  echo $v; PIPEDP_SDP_CHUNKED=0 python tools/cluster_probe.py 20 | tail -1
+  timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$v', round(d['ms_per_step'],3), d['parity']['match'], d['roofline']['kernel'], {k: round(v,3) for k,v in d.get('phases',{}).items() if k.endswith('ms')})"
 done
