@@ -216,7 +216,10 @@ constexpr int kWarps = 8;
 constexpr int kRing = 256;  // exact-phase ring per warp: a_1 presets + a_1 computed cells
 
 template <int OP>
-__global__ void __launch_bounds__(32 * kWarps, 4) sdp_batch_dom(int64_t count, const int32_t* __restrict__ perm,
+// 64 warps per SM (32 registers; the few spills are in the per-instance setup):
+// the steps are shuffle-latency chains, so occupancy is what hides them
+// (C5b: 4 blocks per SM 17.6 ms, 6 15.0, 8 13.9 measured)
+__global__ void __launch_bounds__(32 * kWarps, 8) sdp_batch_dom(int64_t count, const int32_t* __restrict__ perm,
                                                              int64_t n, int32_t k, int32_t a1,
                                                              const int64_t* __restrict__ offsets,
                                                              const int64_t* __restrict__ init,
