@@ -209,27 +209,48 @@ __device__ __forceinline__ void bm_grid_sync(unsigned* bar) {
 // contributes wmin[w] (one operation for 64 columns -- dense powers are the
 // common case), a partial word its set bits one by one.
 template <int OP>
-__device__ __forceinline__ void bm_row(const unsigned long long* __restrict__ P, int32_t W, int32_t a1, int64_t r,
-                                       const int64_t* es, const int64_t* wmin, int64_t* dst_init) {
+__device__ __forceinline__ int64_t bm_word(unsigned long long bits, int w, const int64_t* es, const int64_t* wmin,
+                                           int64_t acc) {
+  using O = SemiOp<OP, int64_t>;
+  if (bits == ~0ull) return O::apply(acc, wmin[w]);
+  while (bits) {
+    const int b = __ffsll((long long)bits) - 1;
+    bits &= bits - 1;
+    acc = O::apply(acc, es[64 * w + b]);
+  }
+  return acc;
+}
+
+// Rows r0 and r1 (r1 < 0: none) of P (.) E, their words loaded together so
+// the L2 latency of one row hides behind the other's.
+template <int OP>
+__device__ __forceinline__ void bm_row2(const unsigned long long* __restrict__ P, int32_t W, int32_t a1, int64_t r0,
+                                        int64_t r1, const int64_t* es, const int64_t* wmin, int64_t* dst_init) {
   using O = SemiOp<OP, int64_t>;
   const int lane = threadIdx.x & 31;
-  int64_t acc = SemiId<OP, int64_t>::value();
-  const unsigned long long* qr = P + r * W;
-  for (int w = lane; w < W; w += 32) {
-    unsigned long long bits = __ldg(qr + w);
-    if (bits == ~0ull) {
-      acc = O::apply(acc, wmin[w]);
-    } else {
-      while (bits) {
-        const int b = __ffsll((long long)bits) - 1;
-        bits &= bits - 1;
-        acc = O::apply(acc, es[64 * w + b]);
-      }
+  int64_t a0 = SemiId<OP, int64_t>::value(), a1v = a0;
+  const unsigned long long* q0 = P + r0 * W;
+  const unsigned long long* q1 = P + (r1 >= 0 ? r1 : r0) * W;
+  for (int w = lane; w < W; w += 64) {  // two words of each row in flight per lane
+    const bool two = w + 32 < W;
+    const unsigned long long b00 = __ldg(q0 + w), b10 = __ldg(q1 + w);
+    const unsigned long long b01 = two ? __ldg(q0 + w + 32) : 0ull, b11 = two ? __ldg(q1 + w + 32) : 0ull;
+    a0 = bm_word<OP>(b00, w, es, wmin, a0);
+    a1v = bm_word<OP>(b10, w, es, wmin, a1v);
+    if (two) {
+      a0 = bm_word<OP>(b01, w + 32, es, wmin, a0);
+      a1v = bm_word<OP>(b11, w + 32, es, wmin, a1v);
     }
   }
 #pragma unroll
-  for (int s = 16; s >= 1; s >>= 1) acc = O::apply(acc, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)acc, s));
-  if (lane == 0) dst_init[a1 - 1 - r] = acc;
+  for (int s = 16; s >= 1; s >>= 1) {
+    a0 = O::apply(a0, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)a0, s));
+    a1v = O::apply(a1v, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)a1v, s));
+  }
+  if (lane == 0) {
+    dst_init[a1 - 1 - r0] = a0;
+    if (r1 >= 0) dst_init[a1 - 1 - r1] = a1v;
+  }
 }
 
 // The entry-state chain in one persistent launch (all CTAs co-resident).
@@ -263,8 +284,8 @@ __global__ void __launch_bounds__(1024, 1) bm_chain(const unsigned long long* __
   // A: the group heads, every CTA on one matrix-vector product per step
   for (int64_t m = 1; m < groups; ++m) {
     load(B * (m - 1));
-    for (int64_t r = (int64_t)blockIdx.x * nw + warp; r < a1; r += (int64_t)gridDim.x * nw)
-      bm_row<OP>(QB, W, a1, r, es, wmin, cinit + B * m * a1);
+    for (int64_t r = (int64_t)blockIdx.x * nw + warp, st = (int64_t)gridDim.x * nw; r < a1; r += 2 * st)
+      bm_row2<OP>(QB, W, a1, r, r + st < a1 ? r + st : -1, es, wmin, cinit + B * m * a1);
     bm_grid_sync(bar);
   }
   // B: inside every group at once; CTA b serves group b % groups
@@ -275,7 +296,8 @@ __global__ void __launch_bounds__(1024, 1) bm_chain(const unsigned long long* __
     const int64_t g = B * m + j;
     if (g < G && per > 0) {
       load(g - 1);
-      for (int64_t r = slot * nw + warp; r < a1; r += per * nw) bm_row<OP>(Q, W, a1, r, es, wmin, cinit + g * a1);
+      for (int64_t r = slot * nw + warp, st = per * nw; r < a1; r += 2 * st)
+        bm_row2<OP>(Q, W, a1, r, r + st < a1 ? r + st : -1, es, wmin, cinit + g * a1);
     }
     bm_grid_sync(bar);
   }

@@ -1,4 +1,5 @@
-for v in lb7 lb8; do
-  if [ $v != orig ]; then cp tools/libexp_$v.so paper_2008_01938_b200/_lib/libpipedp_cuda.so; fi
-  timeout 600 python bench.py --workload c5b --steps 5 --warmup 3 --no-cpu-baseline --e2e-steps 0 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$v', round(d['ms_per_step'],3), d['parity']['match'])"
-done
+O=gpurun_out/exp; mkdir -p $O
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:bm_chain -c 1 -f -o /tmp/ncu_ch python bench.py --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
+ncu -i /tmp/ncu_ch.ncu-rep --page source --csv --print-source=sass > /tmp/src_ch.csv 2>/dev/null
+python tools/ncu_hot.py /tmp/src_ch.csv 25 > $O/ncu_hot_chain.txt 2>&1; head -30 $O/ncu_hot_chain.txt
+ncu -i /tmp/ncu_ch.ncu-rep --page details --csv 2>/dev/null | grep -E '"Duration"|"Executed Instructions"|"Issue Slots Busy"' 
