@@ -1351,9 +1351,25 @@ int32_t pipedp_sdp_plan_execute(pipedp_sdp_plan_t P, const int64_t* d_init, int6
 // Remote-mode (multi-CTA) single-instance solves publish their finished
 // prefix in `published` (batches of 32 cells past a1): copy the table out
 // while the kernel is still producing its tail.
+// The caller's `filled` flags (all ones on success, sdp.cpp:62-64): written by
+// the copy pool while the kernels run, together with the output's prefault;
+// whatever is left (paths without an overlap window) the caller writes after.
+struct HostFill {
+  uint8_t* p = nullptr;
+  size_t n = 0;
+};
+
+static void host_prep(int64_t* cells_out, size_t bytes, HostFill* fill) {
+  pipedp_host::parallel_prefault(cells_out, bytes);
+  if (fill && fill->p) {
+    pipedp_host::parallel_fill(fill->p, 1, fill->n);
+    fill->p = nullptr;
+  }
+}
+
 static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* W,
                                    const int64_t* d_init, int64_t* d_cells, int64_t* cells_out,
-                                   const int64_t* h_init) {
+                                   const int64_t* h_init, HostFill* fill = nullptr) {
   const size_t bytes = sizeof(int64_t) * P->batch * P->n;
   if (P->rank && P->d.method == PIPEDP_SDP_PIPELINE && bytes >= kHostCopyBig && h_init &&
       env_int("PIPEDP_D2H_NARROW", 1) != 0) {
@@ -1370,7 +1386,7 @@ static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* 
     TRY(rc);
     std::vector<int64_t> sorted(h_init, h_init + P->a1);
     std::sort(sorted.begin(), sorted.end());
-    pipedp_host::parallel_prefault(cells_out, bytes);  // overlaps the kernels
+    host_prep(cells_out, bytes, fill);  // overlaps the kernels
     memcpy(cells_out, h_init, sizeof(int64_t) * P->a1);
     CK(W->d2h_lookup16(cells_out + P->a1, static_cast<const uint16_t*>(d_rank) + P->a1,
                        (size_t)(P->n - P->a1), sorted.data()));
@@ -1393,7 +1409,7 @@ static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* 
       const int64_t gs = sm_count();
       TRY(P->d.op == PIPEDP_OP_MAX ? sdp_chunked_run<kMax>(P, d_init, d_cells, W->stream, gs, W->armed)
                                    : sdp_chunked_run<kMin>(P, d_init, d_cells, W->stream, gs, W->armed));
-      pipedp_host::parallel_prefault(cells_out, bytes);  // overlaps the kernels
+      host_prep(cells_out, bytes, fill);  // overlaps the kernels
       // cells [0, cut) are final at `armed`; cut is even so both halves stay
       // 16-byte aligned for narrow_i64_i32's int4 loads
       const int64_t cut = (P->a1 + gs * P->Lc) & ~(int64_t)1;
@@ -1403,7 +1419,7 @@ static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* 
       return PIPEDP_OK;
     }
     TRY(sdp_execute(P, d_init, d_cells, W->stream, nullptr));
-    if (bytes >= kHostCopyBig) pipedp_host::parallel_prefault(cells_out, bytes);  // overlaps the kernel
+    if (bytes >= kHostCopyBig) host_prep(cells_out, bytes, fill);  // overlaps the kernel
     // 32-bit value class (min/max of int32 presets, normalised mod-add): every
     // table value fits int32 -- copy out half the bytes
     if (narrow) return d2h_narrowed(W, 4, cells_out, d_cells, P->batch * P->n);
@@ -1538,7 +1554,7 @@ int32_t pipedp_sdp_plan_destroy(pipedp_sdp_plan_t P) {
 // (host_io.hpp); the tables themselves come only from the kernels.
 static int32_t sdp_solve_host(int64_t batch, int64_t n, int64_t k, int64_t a1,
                               const int64_t* offsets, const int64_t* init, int32_t op,
-                              int64_t* cells_out, int32_t device) {
+                              int64_t* cells_out, int32_t device, HostFill* fill = nullptr) {
   // The last plan of this thread is kept (as for MCM): a caller re-solving an
   // instance with the same offsets (the reference's bench loops) skips the
   // planning uploads and allocations.  The dispatch is re-planned every call
@@ -1579,15 +1595,16 @@ static int32_t sdp_solve_host(int64_t batch, int64_t n, int64_t k, int64_t a1,
   CK(W->buffer(0, sizeof(int64_t) * batch * a1, &d_init));
   CK(W->buffer(1, sizeof(int64_t) * batch * n, &d_cells));
   CK(W->h2d(d_init, init, sizeof(int64_t) * batch * a1));
-  return sdp_execute_to_host(P, W, (const int64_t*)d_init, (int64_t*)d_cells, cells_out, init);
+  return sdp_execute_to_host(P, W, (const int64_t*)d_init, (int64_t*)d_cells, cells_out, init, fill);
 }
 
 int32_t pipedp_sdp_solve(const int64_t* offsets, int64_t k, const int64_t* init,
                          int64_t init_len, int64_t n, int32_t op, int64_t* cells_out,
                          uint8_t* filled_out) {
   TRY(validate_sdp(offsets, k, init_len, n));
-  TRY(sdp_solve_host(1, n, k, init_len, offsets, init, op, cells_out, -1));
-  if (filled_out) memset(filled_out, 1, (size_t)n);
+  HostFill fill{filled_out, (size_t)n};
+  TRY(sdp_solve_host(1, n, k, init_len, offsets, init, op, cells_out, -1, &fill));
+  if (fill.p) memset(fill.p, 1, fill.n);
   return PIPEDP_OK;
 }
 
@@ -1771,7 +1788,7 @@ static int mcm_plan_reload(pipedp_mcm_plan_t P, const int64_t* h_dims, const Mcm
 }
 
 static int32_t mcm_solve_host(int64_t batch, int64_t n, const int64_t* dims, int32_t kernel,
-                              int64_t* cells_out, int64_t* split_out, int32_t device) {
+                              int64_t* cells_out, int64_t* split_out, int32_t device, HostFill* fill = nullptr) {
   // The last plan of this thread is kept: a caller solving instance after
   // instance of one shape (the reference's bench/verify loops) reuses its
   // device tables instead of reallocating hundreds of MiB per call.
@@ -1816,6 +1833,10 @@ static int32_t mcm_solve_host(int64_t batch, int64_t n, const int64_t* dims, int
     touch = std::thread([&] {
       pipedp_host::parallel_prefault(cells_out, sizeof(int64_t) * size);
       if (split_out) pipedp_host::parallel_prefault(split_out, sizeof(int64_t) * size);
+      if (fill && fill->p) {
+        pipedp_host::parallel_fill(fill->p, 1, fill->n);
+        fill->p = nullptr;
+      }
     });
   const int32_t rc = pipedp_mcm_plan_execute(P, (int64_t*)d_cells, (int64_t*)d_split, W->stream);
   if (touch.joinable()) touch.join();
@@ -1837,8 +1858,9 @@ int32_t pipedp_mcm_solve(const int64_t* dims, int64_t dims_len, int32_t kernel,
                          int64_t* cells_out, uint8_t* filled_out, int64_t* split_out) {
   TRY(validate_mcm(dims, dims_len));
   const int64_t n = dims_len - 1;
-  TRY(mcm_solve_host(1, n, dims, kernel, cells_out, split_out, -1));
-  if (filled_out) memset(filled_out, 1, (size_t)(n * (n + 1) / 2 + 1));
+  HostFill fill{filled_out, (size_t)(n * (n + 1) / 2 + 1)};
+  TRY(mcm_solve_host(1, n, dims, kernel, cells_out, split_out, -1, &fill));
+  if (fill.p) memset(fill.p, 1, fill.n);
   return PIPEDP_OK;
 }
 

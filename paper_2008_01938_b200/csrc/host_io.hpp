@@ -126,6 +126,21 @@ inline void parallel_prefault(void* dst, size_t bytes) {
   });
 }
 
+// memset split over the pool (a large host flag array written while the
+// kernels run)
+inline void parallel_fill(void* dst, int value, size_t bytes) {
+  constexpr size_t kPiece = 4u << 20;
+  const int pieces = (int)((bytes + kPiece - 1) / kPiece);
+  if (pieces <= 1) {
+    std::memset(dst, value, bytes);
+    return;
+  }
+  CopyPool::get().parallel_for(pieces, [&](int i) {
+    const size_t lo = (size_t)i * kPiece;
+    std::memset(static_cast<char*>(dst) + lo, value, std::min(kPiece, bytes - lo));
+  });
+}
+
 // dst[i] = src[i] widened, split over the pool (the host half of a narrowed
 // device -> host copy).
 inline void parallel_widen(int64_t* dst, const int32_t* src, size_t count) {
