@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cstdarg>
 #include <cstdio>
@@ -100,7 +101,7 @@ int env_int(const char* name, int dflt) {
       "PIPEDP_SDP_REMOTE_WARPS", "PIPEDP_SDP_REMOTE_CTAS", "PIPEDP_SDP_MID_WARPS", "PIPEDP_SDP_AREMOTE",
       "PIPEDP_SDP2_WRITERS", "PIPEDP_CHUNK_OVERLAP", "PIPEDP_MCM_TILED",   "PIPEDP_MCM_T32_MAXN",
       "PIPEDP_MCM_BLOCKED", "PIPEDP_MCM_SQUARE",   "PIPEDP_MCM_BATCH_WARP", "PIPEDP_MCM_PACKED_SQUARE",
-      "PIPEDP_D2H_NARROW",  "PIPEDP_STREAM_D2H"};
+      "PIPEDP_D2H_NARROW",  "PIPEDP_STREAM_D2H",   "PIPEDP_D2H_PROGRESSIVE"};
   bool known = false;
   for (const char* k : kSwitches) known = known || strcmp(k, name) == 0;
   if (!known) return dflt;
@@ -1378,18 +1379,37 @@ static int32_t sdp_execute_to_host(pipedp_sdp_plan_t P, pipedp_host::Workspace* 
     // sorted init values -- the same multiset the device sorted, so the same
     // rank -> value map; the preset prefix is the caller's init
     void* d_rank = nullptr;
-    CK(W->buffer(4, sizeof(uint16_t) * (size_t)P->n + 16, &d_rank));
+    CK(W->buffer(4, sizeof(uint16_t) * (size_t)(P->a1 + P->G * P->Lc) + 16, &d_rank));
+    // progressive: every chunk publishes how far it is, and the finished
+    // column band of all chunks leaves the device while they run
+    const bool progressive = env_int("PIPEDP_D2H_PROGRESSIVE", 1) != 0;
+    uint32_t epoch = 0;
+    if (progressive) {
+      CK(W->streaming_init());
+      CK(W->progress_words((size_t)P->G));
+      epoch = ++W->prog_epoch;
+      P->rank->progress = W->prog_d;
+      P->rank->epoch = epoch;
+    }
     P->rank->out_rank = static_cast<uint16_t*>(d_rank);
     const int32_t rc = P->d.op == PIPEDP_OP_MAX ? sdp_chunked_run<kMax>(P, d_init, d_cells, W->stream)
                                                 : sdp_chunked_run<kMin>(P, d_init, d_cells, W->stream);
     P->rank->out_rank = nullptr;
+    P->rank->progress = nullptr;
     TRY(rc);
+    if (progressive) CK(cudaEventRecord(W->done, W->stream));
     std::vector<int64_t> sorted(h_init, h_init + P->a1);
     std::sort(sorted.begin(), sorted.end());
-    host_prep(cells_out, bytes, fill);  // overlaps the kernels
+    // first-touch the output while the kernels run (measured: faulting it in
+    // from the conversion instead is 0.6 ms slower on C2)
+    host_prep(cells_out, bytes, fill);
     memcpy(cells_out, h_init, sizeof(int64_t) * P->a1);
-    CK(W->d2h_lookup16(cells_out + P->a1, static_cast<const uint16_t*>(d_rank) + P->a1,
-                       (size_t)(P->n - P->a1), sorted.data()));
+    if (progressive)
+      CK(W->d2h_lookup16_chunks(cells_out, static_cast<const uint16_t*>(d_rank), P->a1, P->n, P->G, P->Lc,
+                                sorted.data(), epoch, W->done));
+    else
+      CK(W->d2h_lookup16(cells_out + P->a1, static_cast<const uint16_t*>(d_rank) + P->a1,
+                         (size_t)(P->n - P->a1), sorted.data()));
     return PIPEDP_OK;
   }
   // (chunked plans never run the remote pipeline: no progress counters)

@@ -358,6 +358,103 @@ struct Workspace {
     return e;
   }
 
+  // Mapped pinned words the device publishes progress into (grow-only).
+  unsigned long long* prog_h = nullptr;
+  unsigned long long* prog_d = nullptr;
+  size_t prog_cap = 0;
+  uint32_t prog_epoch = 0;
+  cudaError_t progress_words(size_t count) {
+    if (prog_cap >= count) return cudaSuccess;
+    if (prog_h) cudaFreeHost(prog_h);
+    prog_h = prog_d = nullptr;
+    prog_cap = 0;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&prog_h), sizeof(unsigned long long) * count,
+                                  cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&prog_d), prog_h, 0);
+    if (e != cudaSuccess) return e;
+    memset(prog_h, 0, sizeof(unsigned long long) * count);
+    prog_cap = count;
+    return cudaSuccess;
+  }
+
+  // Chunked min / max solve, ranks leaving the device while the chunks still
+  // run.  Chunk g owns cells [a1 + g L, a1 + (g+1) L) of d_rank (the last one
+  // ragged at n) and publishes (epoch << 32 | cells final) in prog_h[g]; the
+  // cells every chunk has finished form a column band [lo, hi) of the G x L
+  // view, copied by one strided DMA on `side` and turned into int64 values by
+  // the pool (dst[c] = table[rank]) while the next band is in flight.  After
+  // `done` (the launch's completion) the rest goes the same way.
+  cudaError_t d2h_lookup16_chunks(int64_t* dst, const uint16_t* d_rank, int64_t a1, int64_t n, int64_t G, int64_t L,
+                                  const int64_t* table, uint32_t epoch, cudaEvent_t done) {
+    constexpr int64_t kMinBand = 4096;  // one publication step
+    const int64_t max_band = std::max<int64_t>(1, (int64_t)(kChunk / (sizeof(uint16_t) * G)));
+    const volatile unsigned long long* prog = prog_h;
+    auto ready = [&]() -> int64_t {
+      int64_t m = L;
+      for (int64_t g = 0; g < G && m > 0; ++g) {
+        const unsigned long long v = prog[g];
+        const int64_t len = std::min(L, n - a1 - g * L);
+        int64_t d = (uint32_t)(v >> 32) == epoch ? (int64_t)(v & 0xffffffffu) : 0;
+        if (d >= len) d = L;
+        m = std::min(m, d);
+      }
+      return m;
+    };
+    static const bool trace = getenv("PIPEDP_TRACE_D2H") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+    int64_t band[2][2] = {{0, 0}, {0, 0}};
+    int64_t lo = 0;
+    size_t issued = 0, drained = 0;
+    bool fin = false;
+    for (;;) {
+      if (!fin) {
+        const cudaError_t q = cudaEventQuery(done);
+        if (q == cudaSuccess) fin = true;
+        else if (q != cudaErrorNotReady) return q;
+      }
+      if (issued - drained < 2 && lo < L) {
+        const int64_t hi = std::min(fin ? L : ready(), lo + max_band);
+        if (hi > lo && (fin || hi == L || hi - lo >= kMinBand)) {
+          const int sl = (int)(issued & 1);
+          const size_t w = sizeof(uint16_t) * (size_t)(hi - lo);
+          cudaError_t e = cudaMemcpy2DAsync(pinned[sl], w, d_rank + a1 + lo, sizeof(uint16_t) * (size_t)L, w,
+                                            (size_t)G, cudaMemcpyDeviceToHost, side);
+          if (e == cudaSuccess) e = cudaEventRecord(ev[sl], side);
+          if (e != cudaSuccess) return e;
+          if (trace) fprintf(stderr, "band [%lld, %lld) issued at %.3f ms (fin %d)\n", (long long)lo, (long long)hi, ms(), (int)fin);
+          band[sl][0] = lo;
+          band[sl][1] = hi;
+          lo = hi;
+          ++issued;
+          continue;
+        }
+      }
+      if (drained < issued) {
+        const int sl = (int)(drained & 1);
+        cudaError_t e = cudaEventSynchronize(ev[sl]);
+        if (e != cudaSuccess) return e;
+        const int64_t b0 = band[sl][0], w = band[sl][1] - b0;
+        const uint16_t* src = static_cast<const uint16_t*>(pinned[sl]);
+        const int pieces = (int)std::min<int64_t>(G, CopyPool::get().size());
+        const int64_t per = (G + pieces - 1) / pieces;
+        CopyPool::get().parallel_for(pieces, [&](int i) {
+          for (int64_t g = i * per; g < std::min(G, (i + 1) * per); ++g) {
+            const int64_t c0 = a1 + g * L + b0, cnt = std::min(w, n - c0);
+            const uint16_t* r = src + g * w;
+            int64_t* o = dst + c0;
+            for (int64_t j = 0; j < cnt; ++j) o[j] = table[r[j]];
+          }
+        });
+        if (trace) fprintf(stderr, "band [%lld, %lld) converted at %.3f ms\n", (long long)b0, (long long)(b0 + w), ms());
+        ++drained;
+        continue;
+      }
+      if (fin && lo >= L) return cudaSuccess;
+      std::this_thread::yield();
+    }
+  }
+
   // device -> pageable host after the work queued on `stream`; synchronous
   cudaError_t d2h(void* dst, const void* src, size_t bytes) {
     // pieces of the whole 64 MiB staging buffer (smaller pieces measured

@@ -184,6 +184,16 @@ __global__ void __launch_bounds__(32 * 16) chunk_rank_kernel(const __grid_consta
         if (p.out_rank) p.out_rank[c] = (uint16_t)acc;  // 2 B per cell for the trip to the host
         else p.out[c] = __ldg(p.sorted + acc);
       }
+      if (p.progress && ((b + 1) % kPublishBatches == 0 || b + 1 == nb)) {
+        // this warp's ranks up to batch b are written: order them (system
+        // scope -- the reader is the host, then a copy engine) before the count
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence_system();
+          const unsigned long long done = (unsigned long long)min(32 * (b + 1), e - s);
+          *reinterpret_cast<volatile unsigned long long*>(p.progress + g) = ((unsigned long long)p.epoch << 32) | done;
+        }
+      }
       w += 32;
       if (w >= R2) w -= R2;
       w2 += 32;

@@ -9,6 +9,7 @@
 namespace pipedp_rank {
 
 constexpr int kMaxK = 4096;  // offsets carried in the kernel parameter block
+constexpr int kPublishBatches = 128;  // progress granularity: 4096 cells
 
 // Kernel parameters (a __grid_constant__ block: the offsets are read through
 // the uniform datapath, LDCU, and fold into the LDS address as [R + UR]).
@@ -30,6 +31,12 @@ struct ChunkRankParams {
   const int64_t* sorted;  // [a1] init values ascending: rank -> value
   int64_t* out;           // the table
   uint16_t* out_rank;     // nullable: write each cell's rank here instead (host-bound solves)
+  // nullable (out_rank only): per chunk, (epoch << 32) | cells of the chunk
+  // final in out_rank, published every kPublish cells into mapped host memory
+  // so the host copies and converts the finished part of every chunk while
+  // the chunks still run
+  unsigned long long* progress;
+  uint32_t epoch;
   const int64_t* offsets; // [k] the offsets (device), for the chain's masks
   int32_t nob[kMaxK];     // -4 a_j: byte offset of offset a_j in a ring of 32-bit words
 };

@@ -309,6 +309,24 @@ def test_chunked_overlapped_copy_out(gpu, oracle, op, monkeypatch):
 
 
 @pytest.mark.parametrize("op", ["min", "max"])
+@pytest.mark.parametrize("progressive", ["1", "0"])
+def test_rank_progressive_copy_out(gpu, oracle, op, progressive, monkeypatch):
+    # rank-compressed chunks through the host-buffer call: with progressive
+    # copy-out the chunks publish their progress into mapped host memory and
+    # the finished column band of all chunks is copied and converted while they
+    # run (ragged last chunk); without it, one copy after the launch
+    monkeypatch.setenv("PIPEDP_D2H_PROGRESSIVE", progressive)
+    n = 3_000_000 + 12_345
+    offs, init = oracle.generate_sdp(n, 300, 21, False, 2048)
+    plan = gpu.SdpPlan(1, n, len(offs), len(init), offs, init, op)
+    name = plan.describe()[0]
+    plan.close()
+    assert "chunk_rank_kernel" in name
+    for _ in range(2):  # a second call: the progress words carry the previous epoch
+        _check(gpu, oracle, offs, init, n, op)
+
+
+@pytest.mark.parametrize("op", ["min", "max"])
 def test_chunked_int64_values(gpu, oracle, op):
     # presets beyond int32: 64-bit chunk kernels, entry states and a full-width copy-out
     rng = np.random.default_rng(77)
