@@ -793,10 +793,8 @@ size_t mcm_square_bytes(int64_t n, size_t vb) {
 int mcm_smem_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split, cudaStream_t st) {
   const int64_t n = P->n;
   const size_t sq = mcm_square_bytes(n, bits / 8);
-  if (bits == 32 && n <= pipedp_mcmb::kMaxN && P->batch > 1 && env_int("PIPEDP_MCM_BATCH_WARP", 0) != 0) {
-    // one warp per instance, row and column copies (mcm_batch.cu); opt-in:
-    // C5a 3.85 ms against 3.19 for the square-table CTAs (8 warps per SM at
-    // 25 KB of shared memory per instance: latency-bound)
+  if (bits == 32 && P->packed_now && n <= pipedp_mcmb::kMaxN && env_int("PIPEDP_MCM_BATCH_WARP", 1) != 0) {
+    // one warp per instance, packed keys (mcm_batch.cu)
     CK(pipedp_mcmb::launch((int32_t)n, P->batch, P->d_dims, cells, split, P->d_overflow, st));
     return PIPEDP_OK;
   }
@@ -848,10 +846,10 @@ int mcm_execute(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t
   // packed keys: the 64-wide tiles' far tasks (ALU-bound; the 32-wide ones are
   // latency-bound and keep the plain fold) and the n <= 64 square-table batches
   const bool tiled_pk = P->d.kernel == PIPEDP_MCM_TILED && P->d.tile == 64 && P->maxd3 < (int64_t)kMcmPackedLimit;
-  // (square batches: measured no faster -- lane occupancy, not the fold, bounds
-  // them -- so opt-in with PIPEDP_MCM_PACKED_SQUARE=1)
+  // (n <= 64: the warp-per-instance kernel mcm_batch_warp, or with
+  // PIPEDP_MCM_BATCH_WARP=0 the square-table CTAs' packed fold)
   const bool square_pk = P->d.kernel == PIPEDP_MCM_SMEM && P->d.bits == 32 && P->n <= 64 &&
-                         P->maxd3 < (1ll << 24) && env_int("PIPEDP_MCM_PACKED_SQUARE", 0) != 0;
+                         P->maxd3 < (1ll << 24) && env_int("PIPEDP_MCM_PACKED_SQUARE", 1) != 0;
   P->packed_now = (tiled_pk || square_pk) && env_int("PIPEDP_MCM_PACKED", 1) != 0;
   int kernel = P->d.kernel;  // this execute's kernel (the plan itself is never changed)
   for (;;) {

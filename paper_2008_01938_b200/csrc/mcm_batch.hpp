@@ -1,4 +1,5 @@
-// mcm_batch.hpp -- batched small-n MCM, one warp per instance (mcm_batch.cu).
+// mcm_batch.hpp -- batched small-n MCM, one warp per instance, packed keys
+// (mcm_batch.cu).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -9,7 +10,8 @@ namespace pipedp_mcmb {
 
 constexpr int kMaxN = 64;
 
-// n <= kMaxN, 32-bit values (overflow bit 1 set when a cell reaches 2^30)
+// n <= kMaxN, every weight p[i] p[k] p[j] < 2^24 (host-checked); overflow bit 2
+// set when a cell reaches 2^24 (the host then reruns unpacked)
 cudaError_t launch(int32_t n, int64_t batch, const int64_t* d_dims, int64_t* d_cells, int64_t* d_split,
                    int* d_overflow, cudaStream_t st);
 

@@ -166,11 +166,22 @@ def test_batch_beyond_shared_memory(gpu, oracle, n, lo, hi):
             assert np.array_equal(s[b * size:(b + 1) * size], ws)
 
 
-def test_batch_warp_kernel_opt_in(gpu, oracle, monkeypatch):
-    # mcm_batch_warp (one warp per n <= 64 instance, row + column copies): opt-in
-    monkeypatch.setenv("PIPEDP_MCM_BATCH_WARP", "1")
-    for n in (2, 17, 33, 64):
+@pytest.mark.parametrize("warp", ["1", "0"])
+def test_batch_warp_kernel_and_square(gpu, oracle, monkeypatch, warp):
+    # n <= 64 batches: mcm_batch_warp (one warp per instance, packed keys with
+    # the split column in the low field; the default) and, with
+    # PIPEDP_MCM_BATCH_WARP=0, the square-table CTAs' packed fold
+    monkeypatch.setenv("PIPEDP_MCM_BATCH_WARP", warp)
+    for n in (1, 2, 17, 31, 32, 33, 63, 64):
         insts = [gpu.McmInstance(oracle.generate_mcm(n, 900 + i, 1, 100)) for i in range(20)]
+        for inst, (t, split) in zip(insts, gpu.solve_mcm_batch(insts)):
+            wc, _, ws = oracle.mcm_solve(inst.dims)
+            assert np.array_equal(t.cells, wc) and np.array_equal(split, ws)
+    # all-equal dimensions (every cell a tie: the first split must win), and
+    # weights just under 2^24 whose cells pass 2^24 (overflow bit 2: the
+    # launch reruns unpacked)
+    for dims in ([7] * 65, [3] * 40, oracle.generate_mcm(64, 5, 200, 255), oracle.generate_mcm(50, 6, 240, 255)):
+        insts = [gpu.McmInstance(dims)] * 3
         for inst, (t, split) in zip(insts, gpu.solve_mcm_batch(insts)):
             wc, _, ws = oracle.mcm_solve(inst.dims)
             assert np.array_equal(t.cells, wc) and np.array_equal(split, ws)

@@ -17,5 +17,3 @@ for i in range(8):
     t0 = time.perf_counter(); pd.lib().pipedp_sdp_solve(p(offs), len(offs), p(init), len(init), inst.n, 0, p(out), fl.ctypes.data_as(C.POINTER(C.c_uint8))); ts.append(1e3 * (time.perf_counter() - t0))
 print("reused min %.3f med %.3f" % (min(ts), sorted(ts)[4]))
 PY
-for pf in 0 1 0 1; do for pr in 1 0; do echo "prefault=$pf progressive=$pr"; PIPEDP_PREFAULT=$pf PIPEDP_D2H_PROGRESSIVE=$pr python /tmp/t.py; done; done
-PIPEDP_TRACE_D2H=1 python /tmp/t.py 2>&1 | tail -12
