@@ -24,13 +24,25 @@
 // over the diagonals every candidate of an unflagged run is < 3 * 2^24 < 2^26,
 // so no key wrapped.
 //
-// Layout: the (n+1) x P square, P even: the row walk M'[r][r+q+Gt] and the
-// column walk M'[r+1+q+Gt][c] of the 32 cells of a pass (G = 1) land on 32
-// distinct banks (bank = r (P+1) + const, P+1 odd).  A diagonal of ncell cells
-// runs as passes of 32 cells (one lane each) and a remainder pass in which the
-// last ncell mod 32 cells get G lanes each (G the largest power of two that
-// fits), the G partial keys min-reduced by shuffles.  The warp synchronises
-// per diagonal with __syncwarp only.
+// Layout: one (n+2) x P square, P even, holds TWO instances, one per warp of
+// the CTA, at addr(r, c) = sg (P r + c) + gm:
+//   instance A (sg = +1, gm = 0):  A(r, c) at [r][c]          (upper triangle)
+//   instance B (sg = -1, gm = P(n+2) + n+1): B(r, c) at [n+2-r][n+1-c]
+//                                  (point-reflected: strict lower triangle)
+// A walks its terms k ascending from r, B descending from c-1; with the
+// reflection both walks then move by +1 (left operand (r, k)) and +P (right
+// operand (k+1, c)) per term, and B's weights are stored reversed, so ONE code
+// path (same immediates) serves both warps -- two specialised copies thrash
+// the instruction cache (measured: 12.8 no-instruction stalls per issue).
+// The 32 cells of a pass (G = 1) land on 32 distinct banks in both layouts
+// (bank = +-(P+1) r + const, P+1 odd).  Sharing the square halves the shared
+// memory per instance: 22 instances (warps) per SM instead of 12 -- the
+// kernel is latency-bound, so resident warps are what it runs on.  A diagonal
+// of ncell cells runs as passes of 32 cells (one lane each) and a remainder
+// pass in which the last ncell mod 32 cells get G lanes each (G the largest
+// power of two that fits), the G partial keys min-reduced by shuffles.  Each
+// warp synchronises per diagonal with __syncwarp only; the two warps never
+// touch each other's cells.
 #include "mcm_batch.hpp"
 
 #include <cstdint>
@@ -39,76 +51,108 @@
 
 namespace pipedp_mcmb {
 
-constexpr int kPitch = 66;                       // even, >= kMaxN + 1
-constexpr int kSquare = (kMaxN + 1) * kPitch;    // words
-constexpr uint32_t kCellLimit = 1u << 24;        // packed-key validity (see above)
+constexpr int kPitch = 66;                          // even, >= kMaxN + 1
+constexpr int kSquare = (kMaxN + 2) * kPitch;       // words (rows 0..n+1)
+constexpr uint32_t kCellLimit = 1u << 24;           // packed-key validity (see above)
+constexpr int kCtasPerSm = 11;                      // 11 x (19 + 1) KB of the 228 KB
 
 struct Smem {
   uint32_t M[kSquare];
-  uint32_t p[kMaxN + 2];    // raw dimensions
-  uint32_t pk[kMaxN + 2];   // dimensions << 6
+  uint32_t p[2][kMaxN + 2];    // raw dimensions, per instance
+  uint32_t pk[2][kMaxN + 2];   // dimensions << 6 (instance B: reversed, [n+1-k])
+};
+
+// One warp's instance in the shared square (see the layout note).
+struct Geo {
+  int sg;              // +1 (A) or -1 (B)
+  int gm;              // address offset
+  int om;              // weight index offset: weight of k at pk[sg k + om]
+  uint32_t* M;
+  const uint32_t* p;   // raw dimensions (natural order)
+  const uint32_t* pk;  // weights << 6, walked +1 per term
+  __device__ __forceinline__ int at(int r, int c) const { return sg * (kPitch * r + c) + gm; }
 };
 
 // Cells [base, base + 32 / G) of diagonal D (cells numbered from 0: r = 1 + i),
-// G lanes per cell.  G is a compile-time stride so the unrolled term loop
-// addresses its operands with immediate offsets.
+// G lanes per cell.  G is a compile-time stride: the term loop walks three
+// pointers with immediate offsets, four terms per trip into two accumulators.
+// The per-cell constant c & 63 (the right operand's low field) is taken off
+// once after the fold: every sum is < 2^32 before it, so the min commutes.
 template <int G>
-__device__ __forceinline__ bool diag_pass(int n, int D, int base, int ncell, int lane, Smem& s, int64_t* oc,
+__device__ __forceinline__ bool diag_pass(int D, int base, int ncell, int lane, const Geo& g, int64_t* oc,
                                           int64_t* os) {
-  constexpr int kCells = 32 / G;
-  (void)kCells;
+  constexpr int SL = G, SR = G * kPitch;
   const int q = lane & (G - 1);
-  const int r = 1 + base + lane / G, c = r + D;
-  const bool live = base + lane / G < ncell;
+  const int i = base + lane / G;
+  const int r = 1 + i, c = r + D;
+  const bool live = i < ncell;
   uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu;
   if (live) {
-    const uint32_t prc = s.p[r - 1] * s.p[c];
-    const uint32_t negc = 0u - (uint32_t)(c & 63);  // the right operand's low field
-    const uint32_t* L = s.M + r * kPitch + r + q;            // M'[r][k],   k = r + q + G t
-    const uint32_t* R = s.M + (r + 1 + q) * kPitch + c;      // M'[k+1][c]
-    const uint32_t* W = s.pk + r + q;                        // p''[k]
-    const int cnt = (D - q + G - 1) / G;                     // this lane's terms
-    int t = 0;
-#pragma unroll 2
-    for (; t + 2 <= cnt; t += 2) {
-      const uint32_t a = prc * W[G * t] + L[G * t] + R[G * t * kPitch] + negc;
-      const uint32_t b = prc * W[G * (t + 1)] + L[G * (t + 1)] + R[G * (t + 1) * kPitch] + negc;
-      k0 = min(k0, a);
-      k1 = min(k1, b);
+    const uint32_t prc = g.p[r - 1] * g.p[c];
+    const int kq = g.sg > 0 ? r + q : c - 1 - q;     // this lane's first split column
+    const uint32_t* L = g.M + g.at(r, kq);            // M'(r, k)
+    const uint32_t* R = g.M + g.at(kq + 1, c);        // M'(k+1, c)
+    const uint32_t* W = g.pk + g.sg * kq + g.om;      // p''[k]
+    int cnt = (D - q + G - 1) / G;                    // this lane's terms
+    for (; cnt >= 4; cnt -= 4) {
+      k0 = min(k0, prc * W[0] + L[0] + R[0]);
+      k1 = min(k1, prc * W[G] + L[SL] + R[SR]);
+      k0 = min(k0, prc * W[2 * G] + L[2 * SL] + R[2 * SR]);
+      k1 = min(k1, prc * W[3 * G] + L[3 * SL] + R[3 * SR]);
+      L += 4 * SL;
+      R += 4 * SR;
+      W += 4 * G;
     }
-    if (t < cnt) k0 = min(k0, prc * W[G * t] + L[G * t] + R[G * t * kPitch] + negc);
+    if (cnt >= 2) {
+      k0 = min(k0, prc * W[0] + L[0] + R[0]);
+      k1 = min(k1, prc * W[G] + L[SL] + R[SR]);
+      L += 2 * SL;
+      R += 2 * SR;
+      W += 2 * G;
+    }
+    if (cnt & 1) k0 = min(k0, prc * W[0] + L[0] + R[0]);
   }
   uint32_t key = min(k0, k1);
 #pragma unroll
   for (int sh = G >> 1; sh > 0; sh >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, sh));
   bool ovf = false;
   if (live && q == 0) {
+    key -= (uint32_t)(c & 63);
     const uint32_t v = key >> 6;
-    const int k = (int)(key & 63u);
-    s.M[r * kPitch + c] = (key & ~63u) | (uint32_t)(c & 63);
+    g.M[g.at(r, c)] = (key & ~63u) | (uint32_t)(c & 63);
     oc[r] = (int64_t)v;
-    os[r] = k - r + 1;
+    os[r] = (int64_t)(key & 63u) - r + 1;
     ovf = v >= kCellLimit;
   }
   return ovf;
 }
 
-__global__ void __launch_bounds__(32) mcm_batch_warp(int32_t n, int64_t batch, const int64_t* __restrict__ g_dims,
-                                                    int64_t* __restrict__ out_cells, int64_t* __restrict__ out_split,
-                                                    int* __restrict__ overflow) {
+__global__ void __launch_bounds__(64, kCtasPerSm) mcm_batch_warp(int32_t n, int64_t batch,
+                                                                 const int64_t* __restrict__ g_dims,
+                                                                 int64_t* __restrict__ out_cells,
+                                                                 int64_t* __restrict__ out_split,
+                                                                 int* __restrict__ overflow) {
   __shared__ Smem s;
-  const int lane = threadIdx.x;
-  const int64_t inst = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);  // warp-uniform
+  const int64_t inst = 2 * (int64_t)blockIdx.x + warp;
   if (inst >= batch) return;
   const int64_t cc = (int64_t)n * (n + 1) / 2;
   const int64_t* gd = g_dims + inst * (n + 1);
   int64_t* oc = out_cells + inst * (cc + 1);
   int64_t* os = out_split + inst * (cc + 1);
+  Geo g;
+  g.sg = warp == 0 ? 1 : -1;
+  g.gm = warp == 0 ? 0 : kPitch * (n + 2) + n + 1;
+  g.om = warp == 0 ? 0 : n + 1;
+  g.M = s.M;
+  g.p = s.p[warp];
+  g.pk = s.pk[warp];
   for (int i = lane; i <= n; i += 32) {
     const uint32_t d = (uint32_t)gd[i];
-    s.p[i] = d;
-    s.pk[i] = d << 6;
-    s.M[i * kPitch + i] = (uint32_t)(i & 63);  // base cells m[i][i] = 0 (row 0 unused)
+    s.p[warp][i] = d;
+    s.pk[warp][g.sg * i + g.om] = d << 6;
+    if (i >= 1) s.M[g.at(i, i)] = (uint32_t)(i & 63);  // base cells m[i][i] = 0
     oc[i] = 0;  // slot 0 and the base cells (mcm.cpp:77-83)
     os[i] = 0;
   }
@@ -119,18 +163,18 @@ __global__ void __launch_bounds__(32) mcm_batch_warp(int32_t n, int64_t batch, c
     db += n - (D - 1);
     const int ncell = n - D;
     int base = 0;
-    for (; base + 32 <= ncell; base += 32) ovf |= diag_pass<1>(n, D, base, ncell, lane, s, oc + db, os + db);
+    for (; base + 32 <= ncell; base += 32) ovf |= diag_pass<1>(D, base, ncell, lane, g, oc + db, os + db);
     const int rem = ncell - base;
     if (rem > 0) {
-      int lg = 0;  // G = 2^lg lanes per remaining cell
-      while (lg < 5 && (rem << (lg + 1)) <= 32 && (1 << lg) < D) ++lg;
+      // G = 2^lg lanes per remaining cell: rem G <= 32, and G / 2 < D
+      const int lg = min(5 - (rem > 1 ? 32 - __clz(rem - 1) : 0), D > 1 ? 32 - __clz(D - 1) : 0);
       switch (lg) {
-        case 0: ovf |= diag_pass<1>(n, D, base, ncell, lane, s, oc + db, os + db); break;
-        case 1: ovf |= diag_pass<2>(n, D, base, ncell, lane, s, oc + db, os + db); break;
-        case 2: ovf |= diag_pass<4>(n, D, base, ncell, lane, s, oc + db, os + db); break;
-        case 3: ovf |= diag_pass<8>(n, D, base, ncell, lane, s, oc + db, os + db); break;
-        case 4: ovf |= diag_pass<16>(n, D, base, ncell, lane, s, oc + db, os + db); break;
-        default: ovf |= diag_pass<32>(n, D, base, ncell, lane, s, oc + db, os + db); break;
+        case 0: ovf |= diag_pass<1>(D, base, ncell, lane, g, oc + db, os + db); break;
+        case 1: ovf |= diag_pass<2>(D, base, ncell, lane, g, oc + db, os + db); break;
+        case 2: ovf |= diag_pass<4>(D, base, ncell, lane, g, oc + db, os + db); break;
+        case 3: ovf |= diag_pass<8>(D, base, ncell, lane, g, oc + db, os + db); break;
+        case 4: ovf |= diag_pass<16>(D, base, ncell, lane, g, oc + db, os + db); break;
+        default: ovf |= diag_pass<32>(D, base, ncell, lane, g, oc + db, os + db); break;
       }
     }
     __syncwarp();
@@ -140,10 +184,10 @@ __global__ void __launch_bounds__(32) mcm_batch_warp(int32_t n, int64_t batch, c
 
 cudaError_t launch(int32_t n, int64_t batch, const int64_t* d_dims, int64_t* d_cells, int64_t* d_split,
                    int* d_overflow, cudaStream_t st) {
-  // all of the SM's 228 KB as shared memory: twelve instances per SM
+  // all of the SM's 228 KB as shared memory: eleven CTAs (22 instances) per SM
   cudaError_t e = cudaFuncSetAttribute(mcm_batch_warp, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   if (e != cudaSuccess) return e;
-  mcm_batch_warp<<<(unsigned)batch, 32, 0, st>>>(n, batch, d_dims, d_cells, d_split, d_overflow);
+  mcm_batch_warp<<<(unsigned)((batch + 1) / 2), 64, 0, st>>>(n, batch, d_dims, d_cells, d_split, d_overflow);
   return cudaGetLastError();
 }
 
