@@ -67,62 +67,98 @@ struct Geo {
   int sg;              // +1 (A) or -1 (B)
   int gm;              // address offset
   int om;              // weight index offset: weight of k at pk[sg k + om]
+  int spare;           // a column no cell of this instance uses (B's partial keys)
   uint32_t* M;
   const uint32_t* p;   // raw dimensions (natural order)
   const uint32_t* pk;  // weights << 6, walked +1 per term
   __device__ __forceinline__ int at(int r, int c) const { return sg * (kPitch * r + c) + gm; }
 };
 
-// Cells [base, base + 32 / G) of diagonal D (cells numbered from 0: r = 1 + i),
-// G lanes per cell.  G is a compile-time stride: the term loop walks three
-// pointers with immediate offsets, four terms per trip into two accumulators.
-// The per-cell constant c & 63 (the right operand's low field) is taken off
-// once after the fold: every sum is < 2^32 before it, so the min commutes.
+// Diagonals are taken in PAIRS (D, D+1): cell A = (r, r+D) and cell B =
+// (r, r+D+1) of the same row share the left operand M'(r, k) and the weight
+// p''[k] of every split column k in [r+1, r+D-1] -- all of those terms only
+// read diagonals < D -- so one lane folds both cells' terms over that range
+// with four loads per two terms (8 B per term instead of 12).  A's remaining
+// term (k = r) is folded too; B's two remaining terms (k = r and k = r+D, whose
+// operands lie on diagonal D) follow after the warp has finished diagonal D,
+// from B's partial key parked in the square's spare column (col 0 for the
+// upper-triangle instance, col P-1 for the reflected one: neither is a cell).
+//
+// Phase 1: cells [base, base + 32 / G) of diagonal D (r = 1 + i), G lanes
+// per cell, G a compile-time stride (the term loop walks four pointers with
+// immediate offsets).  The per-cell constant c & 63 (the right operand's low
+// field) is taken off once after the fold: every sum is < 2^32 before it, so
+// the min commutes.
 template <int G>
-__device__ __forceinline__ bool diag_pass(int D, int base, int ncell, int lane, const Geo& g, int64_t* oc,
+__device__ __forceinline__ bool pair_pass(int D, int base, int nA, int lane, const Geo& g, int64_t* oc,
                                           int64_t* os) {
   constexpr int SL = G, SR = G * kPitch;
   const int q = lane & (G - 1);
   const int i = base + lane / G;
-  const int r = 1 + i, c = r + D;
-  const bool live = i < ncell;
-  uint32_t k0 = 0xFFFFFFFFu, k1 = 0xFFFFFFFFu;
-  if (live) {
-    const uint32_t prc = g.p[r - 1] * g.p[c];
-    const int kq = g.sg > 0 ? r + q : c - 1 - q;     // this lane's first split column
-    const uint32_t* L = g.M + g.at(r, kq);            // M'(r, k)
-    const uint32_t* R = g.M + g.at(kq + 1, c);        // M'(k+1, c)
-    const uint32_t* W = g.pk + g.sg * kq + g.om;      // p''[k]
-    int cnt = (D - q + G - 1) / G;                    // this lane's terms
-    for (; cnt >= 4; cnt -= 4) {
-      k0 = min(k0, prc * W[0] + L[0] + R[0]);
-      k1 = min(k1, prc * W[G] + L[SL] + R[SR]);
-      k0 = min(k0, prc * W[2 * G] + L[2 * SL] + R[2 * SR]);
-      k1 = min(k1, prc * W[3 * G] + L[3 * SL] + R[3 * SR]);
-      L += 4 * SL;
-      R += 4 * SR;
-      W += 4 * G;
-    }
-    if (cnt >= 2) {
-      k0 = min(k0, prc * W[0] + L[0] + R[0]);
-      k1 = min(k1, prc * W[G] + L[SL] + R[SR]);
+  const int r = 1 + i, cA = r + D, cB = cA + 1;
+  const bool liveA = i < nA, liveB = i + 1 < nA;
+  uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, b0 = 0xFFFFFFFFu, b1 = 0xFFFFFFFFu;
+  if (liveA) {
+    const uint32_t pr = g.p[r - 1];
+    const uint32_t prcA = pr * g.p[cA], prcB = pr * g.p[cB];  // p[n+1] is padding when !liveB
+    if (q == 0) a0 = prcA * g.pk[g.sg * r + g.om] + g.M[g.at(r, r)] + g.M[g.at(r + 1, cA)];  // k = r
+    const int kq = g.sg > 0 ? r + 1 + q : cA - 1 - q;  // this lane's first shared split column
+    const uint32_t* L = g.M + g.at(r, kq);             // M'(r, k)
+    const uint32_t* RA = g.M + g.at(kq + 1, cA);       // M'(k+1, cA)
+    const uint32_t* RB = RA + g.sg;                    // M'(k+1, cB)
+    const uint32_t* W = g.pk + g.sg * kq + g.om;       // p''[k]
+    int cnt = (D - 1 - q + G - 1) / G;                 // this lane's shared columns
+    for (; cnt >= 2; cnt -= 2) {
+      const uint32_t l0 = L[0], w0 = W[0], l1 = L[SL], w1 = W[G];
+      a0 = min(a0, prcA * w0 + l0 + RA[0]);
+      b0 = min(b0, prcB * w0 + l0 + RB[0]);
+      a1 = min(a1, prcA * w1 + l1 + RA[SR]);
+      b1 = min(b1, prcB * w1 + l1 + RB[SR]);
       L += 2 * SL;
-      R += 2 * SR;
+      RA += 2 * SR;
+      RB += 2 * SR;
       W += 2 * G;
     }
-    if (cnt & 1) k0 = min(k0, prc * W[0] + L[0] + R[0]);
+    if (cnt) {
+      const uint32_t l0 = L[0], w0 = W[0];
+      a0 = min(a0, prcA * w0 + l0 + RA[0]);
+      b0 = min(b0, prcB * w0 + l0 + RB[0]);
+    }
   }
-  uint32_t key = min(k0, k1);
+  uint32_t ka = min(a0, a1), kb = min(b0, b1);
 #pragma unroll
-  for (int sh = G >> 1; sh > 0; sh >>= 1) key = min(key, __shfl_xor_sync(0xffffffffu, key, sh));
+  for (int sh = G >> 1; sh > 0; sh >>= 1) {
+    ka = min(ka, __shfl_xor_sync(0xffffffffu, ka, sh));
+    kb = min(kb, __shfl_xor_sync(0xffffffffu, kb, sh));
+  }
   bool ovf = false;
-  if (live && q == 0) {
+  if (liveA && q == 0) {
+    ka -= (uint32_t)(cA & 63);
+    const uint32_t v = ka >> 6;
+    g.M[g.at(r, cA)] = (ka & ~63u) | (uint32_t)(cA & 63);
+    oc[r] = (int64_t)v;
+    os[r] = (int64_t)(ka & 63u) - r + 1;
+    ovf = v >= kCellLimit;
+    if (liveB) g.M[kPitch * r + g.spare] = kb;  // B's partial (still carries + (cB & 63))
+  }
+  return ovf;
+}
+
+// Phase 2: B = (r, r+D+1) for r = 1 .. nB, its two terms on diagonal D.
+__device__ __forceinline__ bool pair_finish(int D, int nB, int lane, const Geo& g, int64_t* oc, int64_t* os) {
+  bool ovf = false;
+  for (int i = lane; i < nB; i += 32) {
+    const int r = 1 + i, c = r + D + 1;
+    const uint32_t prc = g.p[r - 1] * g.p[c];
+    uint32_t key = g.M[kPitch * r + g.spare];
+    key = min(key, prc * g.pk[g.sg * r + g.om] + g.M[g.at(r, r)] + g.M[g.at(r + 1, c)]);              // k = r
+    key = min(key, prc * g.pk[g.sg * (c - 1) + g.om] + g.M[g.at(r, c - 1)] + g.M[g.at(c, c)]);        // k = c - 1
     key -= (uint32_t)(c & 63);
     const uint32_t v = key >> 6;
     g.M[g.at(r, c)] = (key & ~63u) | (uint32_t)(c & 63);
     oc[r] = (int64_t)v;
     os[r] = (int64_t)(key & 63u) - r + 1;
-    ovf = v >= kCellLimit;
+    ovf |= v >= kCellLimit;
   }
   return ovf;
 }
@@ -145,39 +181,47 @@ __global__ void __launch_bounds__(64, kCtasPerSm) mcm_batch_warp(int32_t n, int6
   g.sg = warp == 0 ? 1 : -1;
   g.gm = warp == 0 ? 0 : kPitch * (n + 2) + n + 1;
   g.om = warp == 0 ? 0 : n + 1;
+  g.spare = warp == 0 ? 0 : kPitch - 1;
   g.M = s.M;
   g.p = s.p[warp];
   g.pk = s.pk[warp];
-  for (int i = lane; i <= n; i += 32) {
-    const uint32_t d = (uint32_t)gd[i];
+  for (int i = lane; i <= kMaxN + 1; i += 32) {
+    const uint32_t d = i <= n ? (uint32_t)gd[i] : 0u;
     s.p[warp][i] = d;
-    s.pk[warp][g.sg * i + g.om] = d << 6;
-    if (i >= 1) s.M[g.at(i, i)] = (uint32_t)(i & 63);  // base cells m[i][i] = 0
-    oc[i] = 0;  // slot 0 and the base cells (mcm.cpp:77-83)
-    os[i] = 0;
+    if (i <= n) s.pk[warp][g.sg * i + g.om] = d << 6;
+    if (i >= 1 && i <= n) s.M[g.at(i, i)] = (uint32_t)(i & 63);  // base cells m[i][i] = 0
+    if (i <= n) {
+      oc[i] = 0;  // slot 0 and the base cells (mcm.cpp:77-83)
+      os[i] = 0;
+    }
   }
   __syncwarp();
   bool ovf = false;
   int64_t db = 0;  // lin(r, r+D) = db(D) + r
-  for (int D = 1; D < n; ++D) {
+  for (int D = 1; D < n; D += 2) {
     db += n - (D - 1);
-    const int ncell = n - D;
+    const int nA = n - D;  // cells on diagonal D (B: nA - 1 on D + 1)
     int base = 0;
-    for (; base + 32 <= ncell; base += 32) ovf |= diag_pass<1>(D, base, ncell, lane, g, oc + db, os + db);
-    const int rem = ncell - base;
+    for (; base + 32 <= nA; base += 32) ovf |= pair_pass<1>(D, base, nA, lane, g, oc + db, os + db);
+    const int rem = nA - base;
     if (rem > 0) {
       // G = 2^lg lanes per remaining cell: rem G <= 32, and G / 2 < D
       const int lg = min(5 - (rem > 1 ? 32 - __clz(rem - 1) : 0), D > 1 ? 32 - __clz(D - 1) : 0);
       switch (lg) {
-        case 0: ovf |= diag_pass<1>(D, base, ncell, lane, g, oc + db, os + db); break;
-        case 1: ovf |= diag_pass<2>(D, base, ncell, lane, g, oc + db, os + db); break;
-        case 2: ovf |= diag_pass<4>(D, base, ncell, lane, g, oc + db, os + db); break;
-        case 3: ovf |= diag_pass<8>(D, base, ncell, lane, g, oc + db, os + db); break;
-        case 4: ovf |= diag_pass<16>(D, base, ncell, lane, g, oc + db, os + db); break;
-        default: ovf |= diag_pass<32>(D, base, ncell, lane, g, oc + db, os + db); break;
+        case 0: ovf |= pair_pass<1>(D, base, nA, lane, g, oc + db, os + db); break;
+        case 1: ovf |= pair_pass<2>(D, base, nA, lane, g, oc + db, os + db); break;
+        case 2: ovf |= pair_pass<4>(D, base, nA, lane, g, oc + db, os + db); break;
+        case 3: ovf |= pair_pass<8>(D, base, nA, lane, g, oc + db, os + db); break;
+        case 4: ovf |= pair_pass<16>(D, base, nA, lane, g, oc + db, os + db); break;
+        default: ovf |= pair_pass<32>(D, base, nA, lane, g, oc + db, os + db); break;
       }
     }
     __syncwarp();
+    if (nA > 1) {
+      db += n - D;
+      ovf |= pair_finish(D, nA - 1, lane, g, oc + db, os + db);
+      __syncwarp();
+    }
   }
   if (__any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(overflow, 2);
 }
