@@ -89,10 +89,11 @@ struct Geo {
 // immediate offsets).  The per-cell constant c & 63 (the right operand's low
 // field) is taken off once after the fold: every sum is < 2^32 before it, so
 // the min commutes.
-template <int G>
+template <int GT>  // GT > 0: compile-time G; GT == 0: G = gr at run time (the rarer short passes)
 __device__ __forceinline__ bool pair_pass(int D, int base, int nA, int lane, const Geo& g, int64_t* oc,
-                                          int64_t* os) {
-  constexpr int SL = G, SR = G * kPitch;
+                                          int64_t* os, int gr = GT) {
+  const int G = GT > 0 ? GT : gr;
+  const int SL = G, SR = G * kPitch;
   const int q = lane & (G - 1);
   const int i = base + lane / G;
   const int r = 1 + i, cA = r + D, cB = cA + 1;
@@ -127,9 +128,11 @@ __device__ __forceinline__ bool pair_pass(int D, int base, int nA, int lane, con
   }
   uint32_t ka = min(a0, a1), kb = min(b0, b1);
 #pragma unroll
-  for (int sh = G >> 1; sh > 0; sh >>= 1) {
-    ka = min(ka, __shfl_xor_sync(0xffffffffu, ka, sh));
-    kb = min(kb, __shfl_xor_sync(0xffffffffu, kb, sh));
+  for (int sh = 16; sh > 0; sh >>= 1) {
+    if (sh < G) {
+      ka = min(ka, __shfl_xor_sync(0xffffffffu, ka, sh));
+      kb = min(kb, __shfl_xor_sync(0xffffffffu, kb, sh));
+    }
   }
   bool ovf = false;
   if (liveA && q == 0) {
@@ -207,14 +210,9 @@ __global__ void __launch_bounds__(64, kCtasPerSm) mcm_batch_warp(int32_t n, int6
     if (rem > 0) {
       // G = 2^lg lanes per remaining cell: rem G <= 32, and G / 2 < D
       const int lg = min(5 - (rem > 1 ? 32 - __clz(rem - 1) : 0), D > 1 ? 32 - __clz(D - 1) : 0);
-      switch (lg) {
-        case 0: ovf |= pair_pass<1>(D, base, nA, lane, g, oc + db, os + db); break;
-        case 1: ovf |= pair_pass<2>(D, base, nA, lane, g, oc + db, os + db); break;
-        case 2: ovf |= pair_pass<4>(D, base, nA, lane, g, oc + db, os + db); break;
-        case 3: ovf |= pair_pass<8>(D, base, nA, lane, g, oc + db, os + db); break;
-        case 4: ovf |= pair_pass<16>(D, base, nA, lane, g, oc + db, os + db); break;
-        default: ovf |= pair_pass<32>(D, base, nA, lane, g, oc + db, os + db); break;
-      }
+      if (lg == 0) ovf |= pair_pass<1>(D, base, nA, lane, g, oc + db, os + db);
+      else if (lg == 1) ovf |= pair_pass<2>(D, base, nA, lane, g, oc + db, os + db);
+      else ovf |= pair_pass<0>(D, base, nA, lane, g, oc + db, os + db, 1 << lg);
     }
     __syncwarp();
     if (nA > 1) {
