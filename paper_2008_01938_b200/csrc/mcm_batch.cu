@@ -211,7 +211,6 @@ __global__ void __launch_bounds__(64, kCtasPerSm) mcm_batch_warp(int32_t n, int6
       // G = 2^lg lanes per remaining cell: rem G <= 32, and G / 2 < D
       const int lg = min(5 - (rem > 1 ? 32 - __clz(rem - 1) : 0), D > 1 ? 32 - __clz(D - 1) : 0);
       if (lg == 0) ovf |= pair_pass<1>(D, base, nA, lane, g, oc + db, os + db);
-      else if (lg == 1) ovf |= pair_pass<2>(D, base, nA, lane, g, oc + db, os + db);
       else ovf |= pair_pass<0>(D, base, nA, lane, g, oc + db, os + db, 1 << lg);
     }
     __syncwarp();
