@@ -147,21 +147,48 @@ __device__ __forceinline__ bool pair_pass(int D, int base, int nA, int lane, con
   return ovf;
 }
 
-// Phase 2: B = (r, r+D+1) for r = 1 .. nB, its two terms on diagonal D.
+// Phase 2: B = (r, r+D+1) for r = 1 .. nB (nB <= 62: at most two cells per
+// lane), its two terms on diagonal D.  Every address is affine in r along
+// the diagonal, so the second cell's are the first's plus a constant.
 __device__ __forceinline__ bool pair_finish(int D, int nB, int lane, const Geo& g, int64_t* oc, int64_t* os) {
   bool ovf = false;
-  for (int i = lane; i < nB; i += 32) {
-    const int r = 1 + i, c = r + D + 1;
-    const uint32_t prc = g.p[r - 1] * g.p[c];
-    uint32_t key = g.M[kPitch * r + g.spare];
-    key = min(key, prc * g.pk[g.sg * r + g.om] + g.M[g.at(r, r)] + g.M[g.at(r + 1, c)]);              // k = r
-    key = min(key, prc * g.pk[g.sg * (c - 1) + g.om] + g.M[g.at(r, c - 1)] + g.M[g.at(c, c)]);        // k = c - 1
-    key -= (uint32_t)(c & 63);
+  int r = 1 + lane;
+  if (r > nB) return false;
+  const int c = r + D + 1;
+  const int step = 32 * g.sg * (kPitch + 1);  // (r, c) -> (r + 32, c + 32)
+  const uint32_t* mrr = g.M + g.at(r, r);
+  const uint32_t* mr1c = g.M + g.at(r + 1, c);
+  const uint32_t* mrc1 = g.M + g.at(r, c - 1);
+  const uint32_t* mcc = g.M + g.at(c, c);
+  uint32_t* mrc = g.M + g.at(r, c);
+  uint32_t* sp = g.M + kPitch * r + g.spare;
+  const uint32_t* w1 = g.pk + g.sg * r + g.om;
+  const uint32_t* w2 = g.pk + g.sg * (c - 1) + g.om;
+  const uint32_t* pr = g.p + r - 1;
+  int cc = c;
+#pragma unroll 1
+  for (;;) {
+    const uint32_t prc = pr[0] * pr[D + 2];
+    uint32_t key = min(sp[0], prc * w1[0] + mrr[0] + mr1c[0]);  // k = r
+    key = min(key, prc * w2[0] + mrc1[0] + mcc[0]);               // k = c - 1
+    key -= (uint32_t)(cc & 63);
     const uint32_t v = key >> 6;
-    g.M[g.at(r, c)] = (key & ~63u) | (uint32_t)(c & 63);
+    mrc[0] = (key & ~63u) | (uint32_t)(cc & 63);
     oc[r] = (int64_t)v;
     os[r] = (int64_t)(key & 63u) - r + 1;
     ovf |= v >= kCellLimit;
+    r += 32;
+    if (r > nB) break;
+    cc += 32;
+    mrr += step;
+    mr1c += step;
+    mrc1 += step;
+    mcc += step;
+    mrc += step;
+    sp += 32 * kPitch;
+    w1 += 32 * g.sg;
+    w2 += 32 * g.sg;
+    pr += 32;
   }
   return ovf;
 }
