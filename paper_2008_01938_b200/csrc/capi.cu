@@ -765,23 +765,29 @@ int mcm_tiled_launch(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStr
 }
 
 // Task list of the tiled kernel, ordered by readiness (see mcm_tiled.cuh):
-// position 2*Delta for the diagonal/near task of tile (I, I+Delta), position
-// 2*max(K-I, J-K)+1 for far task (I, J, K).
+// far task (I, J, K) at level L = max(K-I, J-K) (its inputs are tiles of
+// levels <= L), its level's tasks by tile distance Delta = J - I ascending; the
+// near task of a tile at level Delta - 1, right after the far tasks of the
+// tiles of distance Delta (its own last far tasks) and before the far tasks
+// that feed farther tiles -- the critical chain (near Delta-1 -> the two last
+// far tasks -> near Delta) is not queued behind a level's whole far work.
 std::vector<unsigned long long> mcm_tiled_tasks(int N) {
-  std::vector<std::vector<unsigned long long>> buckets((size_t)2 * N + 1);
-  for (int I = 0; I < N; ++I) buckets[0].push_back(tiled_task(kTaskDiag, I, I, 0));
-  for (int D = 1; D < N; ++D)
-    for (int I = 0; I + D < N; ++I) buckets[(size_t)2 * D].push_back(tiled_task(kTaskNear, I, I + D, 0));
-  for (int D = 2; D < N; ++D)
-    for (int I = 0; I + D < N; ++I) {
-      const int J = I + D;
-      for (int K = I + 1; K < J; ++K) {
-        const int L = std::max(K - I, J - K);
-        buckets[(size_t)2 * L + 1].push_back(tiled_task(kTaskFar, I, J, K));
-      }
-    }
   std::vector<unsigned long long> out;
-  for (auto& b : buckets) out.insert(out.end(), b.begin(), b.end());
+  for (int I = 0; I < N; ++I) out.push_back(tiled_task(kTaskDiag, I, I, 0));
+  for (int L = 0; L + 1 < N; ++L) {
+    // far tasks of level L (L >= 1) for tiles of distance D in [L+1, 2L], D ascending;
+    // the near tasks of distance L+1 after the D = L+1 group
+    for (int D = L + 1; D <= 2 * L + 1 && D < N; ++D) {
+      if (L >= 1 && D <= 2 * L)
+        for (int I = 0; I + D < N; ++I) {
+          const int J = I + D;
+          out.push_back(tiled_task(kTaskFar, I, J, I + L));
+          if (D != 2 * L) out.push_back(tiled_task(kTaskFar, I, J, J - L));  // D = 2L: the same K
+        }
+      if (D == L + 1)
+        for (int I = 0; I + D < N; ++I) out.push_back(tiled_task(kTaskNear, I, I + D, 0));
+    }
+  }
   return out;
 }
 

@@ -21,6 +21,8 @@ for kind, nm in enumerate(["diag", "near", "far"]):
     tot, wait, cnt = p[32 + 4 * kind], p[33 + 4 * kind], p[34 + 4 * kind]
     if cnt:
         print(f"  {nm:5s} tasks {cnt:8d}  avg {tot / cnt:10.0f} cyc  avg wait+load {wait / cnt:10.0f} cyc  compute {(tot - wait) / cnt:10.0f} cyc")
+if p[42]:
+    print(f"  far: flag wait {p[47] / p[42]:.0f} cyc of the wait+load")
 if p[38]:
     print(f"  near split: init {p[44]/p[38]:.0f}  wavefront {p[45]/p[38]:.0f}  finish {p[46]/p[38]:.0f} cyc")
 if p[38]:
