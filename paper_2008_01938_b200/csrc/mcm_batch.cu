@@ -89,10 +89,11 @@ struct Geo {
 // immediate offsets).  The per-cell constant c & 63 (the right operand's low
 // field) is taken off once after the fold: every sum is < 2^32 before it, so
 // the min commutes.
-template <int GT>  // GT > 0: compile-time G; GT == 0: G = gr at run time (the rarer short passes)
+template <int LGT>  // LGT >= 0: compile-time G = 2^LGT; LGT < 0: G = 2^lgr at run time (the rarer short passes)
 __device__ __forceinline__ bool pair_pass(int D, int base, int nA, int lane, const Geo& g, int64_t* oc,
-                                          int64_t* os, int gr = GT) {
-  const int G = GT > 0 ? GT : gr;
+                                          int64_t* os, int lgr = 0) {
+  const int lg = LGT >= 0 ? LGT : lgr;
+  const int G = 1 << lg;
   const int SL = G, SR = G * kPitch;
   const int q = lane & (G - 1);
   const int i = base + lane / G;
@@ -108,8 +109,25 @@ __device__ __forceinline__ bool pair_pass(int D, int base, int nA, int lane, con
     const uint32_t* RA = g.M + g.at(kq + 1, cA);       // M'(k+1, cA)
     const uint32_t* RB = RA + g.sg;                    // M'(k+1, cB)
     const uint32_t* W = g.pk + g.sg * kq + g.om;       // p''[k]
-    int cnt = (D - 1 - q + G - 1) / G;                 // this lane's shared columns
-    for (; cnt >= 2; cnt -= 2) {
+    int cnt = (D - 1 - q + G - 1) >> lg;               // this lane's shared columns
+    for (; cnt >= 4; cnt -= 4) {
+      const uint32_t l0 = L[0], w0 = W[0], l1 = L[SL], w1 = W[G];
+      const uint32_t l2 = L[2 * SL], w2 = W[2 * G], l3 = L[3 * SL], w3 = W[3 * G];
+      a0 = min(a0, prcA * w0 + l0 + RA[0]);
+      b0 = min(b0, prcB * w0 + l0 + RB[0]);
+      a1 = min(a1, prcA * w1 + l1 + RA[SR]);
+      b1 = min(b1, prcB * w1 + l1 + RB[SR]);
+      a0 = min(a0, prcA * w2 + l2 + RA[2 * SR]);
+      b0 = min(b0, prcB * w2 + l2 + RB[2 * SR]);
+      a1 = min(a1, prcA * w3 + l3 + RA[3 * SR]);
+      b1 = min(b1, prcB * w3 + l3 + RB[3 * SR]);
+      L += 4 * SL;
+      RA += 4 * SR;
+      RB += 4 * SR;
+      W += 4 * G;
+    }
+    if (cnt >= 2) {
+      cnt -= 2;
       const uint32_t l0 = L[0], w0 = W[0], l1 = L[SL], w1 = W[G];
       a0 = min(a0, prcA * w0 + l0 + RA[0]);
       b0 = min(b0, prcB * w0 + l0 + RB[0]);
@@ -232,13 +250,13 @@ __global__ void __launch_bounds__(64, kCtasPerSm) mcm_batch_warp(int32_t n, int6
     db += n - (D - 1);
     const int nA = n - D;  // cells on diagonal D (B: nA - 1 on D + 1)
     int base = 0;
-    for (; base + 32 <= nA; base += 32) ovf |= pair_pass<1>(D, base, nA, lane, g, oc + db, os + db);
+    for (; base + 32 <= nA; base += 32) ovf |= pair_pass<0>(D, base, nA, lane, g, oc + db, os + db);
     const int rem = nA - base;
     if (rem > 0) {
       // G = 2^lg lanes per remaining cell: rem G <= 32, and G / 2 < D
       const int lg = min(5 - (rem > 1 ? 32 - __clz(rem - 1) : 0), D > 1 ? 32 - __clz(D - 1) : 0);
-      if (lg == 0) ovf |= pair_pass<1>(D, base, nA, lane, g, oc + db, os + db);
-      else ovf |= pair_pass<0>(D, base, nA, lane, g, oc + db, os + db, 1 << lg);
+      if (lg == 0) ovf |= pair_pass<0>(D, base, nA, lane, g, oc + db, os + db);
+      else ovf |= pair_pass<-1>(D, base, nA, lane, g, oc + db, os + db, lg);
     }
     __syncwarp();
     if (nA > 1) {
