@@ -1756,7 +1756,8 @@ int32_t pipedp_mcm_plan_describe(pipedp_mcm_plan_t P, char* name, size_t cap, in
   const bool square = mcm_square_bytes(P->n, (P->last_bits ? P->last_bits : P->d.bits) / 8) <= kSmemBudget &&
                       env_int("PIPEDP_MCM_SQUARE", 1) != 0;
   const int lb = P->last_bits ? P->last_bits : P->d.bits;
-  const bool bwarp = lb == 32 && P->n <= pipedp_mcmb::kMaxN && P->batch > 1 && env_int("PIPEDP_MCM_BATCH_WARP", 0) != 0;
+  // the kernel mcm_smem_launch picks (packed_now: this plan's last execute)
+  const bool bwarp = lb == 32 && P->packed_now && P->n <= pipedp_mcmb::kMaxN && env_int("PIPEDP_MCM_BATCH_WARP", 1) != 0;
   const char* nm = P->d.kernel == PIPEDP_MCM_SMEM         ? (bwarp ? "mcm_batch_warp" : square ? "mcm_smem_square" : "mcm_smem_cta")
                    : P->d.kernel == PIPEDP_MCM_TOURNAMENT ? "mcm_tournament_diag"
                    : (P->d.kernel == PIPEDP_MCM_TILED && P->last_bits != 64)

@@ -21,7 +21,7 @@ timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --c
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1
 python tools/launch_summary.py $O/launches_c2.csv 3 > $O/launches_c2_summary.txt 2>&1; head -8 $O/launches_c2_summary.txt
 declare -A K=([c1]='regex:sdp_jump' [c2]='regex:chunk_rank' [c3]='regex:mcm_tiled' [c4]='regex:mcm_tiled'
-             [c5a]='regex:mcm_smem' [c5b]='regex:sdp_batch_dom')
+             [c5a]='regex:mcm_batch_warp' [c5b]='regex:sdp_batch_dom')
 for w in c1 c2 c3 c4 c5a c5b; do
   timeout 900 ncu --set full --clock-control none --import-source on -k "${K[$w]}" -c 1 -f -o /tmp/ncu_$w \
     python bench.py --workload $w --steps 1 --warmup 0 --no-cpu-baseline --e2e-steps 0 > /dev/null 2>&1

@@ -71,7 +71,7 @@ def plain_cases():
         wc, _, ws = orc.mcm_solve(dims)
         assert np.array_equal(t.cells, wc) and np.array_equal(split, ws), label
         print("ok mcm", label, flush=True)
-    insts = [pd.generate_mcm(n=32, seed=s, dims_min=1, dims_max=100) for s in range(12)]
+    insts = [pd.generate_mcm(n=n, seed=s, dims_min=1, dims_max=100) for n in (32, 64) for s in range(5)]
     for inst, (t, split) in zip(insts, pd.solve_mcm_batch(insts)):
         wc, _, ws = orc.mcm_solve(inst.dims)
         assert np.array_equal(t.cells, wc) and np.array_equal(split, ws)
