@@ -107,7 +107,10 @@ __device__ __forceinline__ bool pair_pass(int D, int base, int nA, int lane, con
     const int kq = g.sg > 0 ? r + 1 + q : cA - 1 - q;  // this lane's first shared split column
     const uint32_t* L = g.M + g.at(r, kq);             // M'(r, k)
     const uint32_t* RA = g.M + g.at(kq + 1, cA);       // M'(k+1, cA)
-    const uint32_t* RB = RA + g.sg;                    // M'(k+1, cB)
+    // M'(k+1, cB); without a cell B (cB = n+1) the walk would read the other
+    // instance's spare column (harmless, unused -- but a cross-warp race to
+    // racecheck): walk A's own column instead
+    const uint32_t* RB = liveB ? RA + g.sg : RA;
     const uint32_t* W = g.pk + g.sg * kq + g.om;       // p''[k]
     int cnt = (D - 1 - q + G - 1) >> lg;               // this lane's shared columns
     for (; cnt >= 4; cnt -= 4) {

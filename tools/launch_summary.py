@@ -15,6 +15,8 @@ def main(path, steps=1):
             continue
         scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "ns": 1e-6, "us": 1e-3, "ms": 1.0}.get(r[ui], 1.0)
         name = r[ki].split("(")[0][:70]
+        if "_probe" in name or "at::" in name:  # bench's roofline probes and torch's L2 flush: not the step
+            continue
         tot[name] += float(r[vi].replace(",", "")) * scale
         cnt[name] += 1
     all_ms = sum(tot.values())

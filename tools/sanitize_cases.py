@@ -71,10 +71,11 @@ def plain_cases():
         wc, _, ws = orc.mcm_solve(dims)
         assert np.array_equal(t.cells, wc) and np.array_equal(split, ws), label
         print("ok mcm", label, flush=True)
-    insts = [pd.generate_mcm(n=n, seed=s, dims_min=1, dims_max=100) for n in (32, 64) for s in range(5)]
-    for inst, (t, split) in zip(insts, pd.solve_mcm_batch(insts)):
-        wc, _, ws = orc.mcm_solve(inst.dims)
-        assert np.array_equal(t.cells, wc) and np.array_equal(split, ws)
+    for n in (32, 64):  # mcm_batch_warp: one- and two-pass diagonals, an odd batch
+        insts = [pd.generate_mcm(n=n, seed=s, dims_min=1, dims_max=100) for s in range(5)]
+        for inst, (t, split) in zip(insts, pd.solve_mcm_batch(insts)):
+            wc, _, ws = orc.mcm_solve(inst.dims)
+            assert np.array_equal(t.cells, wc) and np.array_equal(split, ws)
     print("ok mcm batch", flush=True)
     # the lock-step engine with its device analyses, both programs
     r = pd.solve_mcm_pipeline(pd.generate_mcm(n=20, seed=2, dims_min=1, dims_max=50), "paper_literal")
