@@ -781,8 +781,17 @@ std::vector<unsigned long long> mcm_tiled_tasks(int N) {
       if (L >= 1 && D <= 2 * L)
         for (int I = 0; I + D < N; ++I) {
           const int J = I + D;
-          out.push_back(tiled_task(kTaskFar, I, J, I + L));
-          if (D != 2 * L) out.push_back(tiled_task(kTaskFar, I, J, J - L));  // D = 2L: the same K
+          // the two K of level L (J - L < I + L) in one task, except for the
+          // tiles whose near task comes next (D = L + 1): those two run in
+          // parallel, they are the critical chain; D = 2L: one K
+          if (D == 2 * L) {
+            out.push_back(tiled_task(kTaskFar, I, J, I + L));
+          } else if (D == L + 1) {
+            out.push_back(tiled_task(kTaskFar, I, J, I + L));
+            out.push_back(tiled_task(kTaskFar, I, J, J - L));
+          } else {
+            out.push_back(tiled_task(kTaskFar2, I, J, J - L));
+          }
         }
       if (D == L + 1)
         for (int I = 0; I + D < N; ++I) out.push_back(tiled_task(kTaskNear, I, I + D, 0));

@@ -65,7 +65,7 @@ __host__ __device__ __forceinline__ int64_t tiled_index(int64_t I, int64_t J, in
   return I * N - I * (I - 1) / 2 + (J - I);
 }
 
-enum : int { kTaskDiag = 0, kTaskNear = 1, kTaskFar = 2 };
+enum : int { kTaskDiag = 0, kTaskNear = 1, kTaskFar = 2, kTaskFar2 = 3 };  // Far2: K and K2 = I + J - K
 
 __host__ __device__ __forceinline__ unsigned long long tiled_task(int kind, int I, int J, int K) {
   return ((unsigned long long)kind << 48) | ((unsigned long long)I << 32) | ((unsigned long long)J << 16) |
