@@ -21,8 +21,8 @@ while time.time() - t0 < budget:
     it += 1
     seed = int(rng.integers(1 << 31))
     r = np.random.default_rng(seed)
-    kind = r.choice(["sdp_small", "sdp_mid", "sdp_big", "mcm", "sdp_batch", "sdp_cluster"],
-                    p=[0.2, 0.25, 0.1, 0.15, 0.15, 0.15])
+    kind = r.choice(["sdp_small", "sdp_mid", "sdp_big", "mcm", "sdp_batch", "sdp_cluster", "mcm_batch"],
+                    p=[0.18, 0.22, 0.1, 0.15, 0.12, 0.13, 0.1])
     if kind == "sdp_cluster":
         # one instance over the thread-block cluster (chunked mode off for min/max)
         import os
@@ -68,6 +68,18 @@ while time.time() - t0 < budget:
                           np.concatenate([i.init for i in insts]), op)
         name = plan.describe()[0].split("[")[0]
         plan.close()
+    elif kind == "mcm_batch":
+        # n <= 64 batches: mcm_batch_warp (packed keys; dims up to 255 can pass
+        # 2^24 and rerun unpacked; 1290 is never packed), odd and even counts
+        n = int(r.integers(1, 65))
+        dmax = int(r.choice([100, 255, 1290]))
+        cnt = int(r.integers(1, 41))
+        insts = [pd.McmInstance(orc.generate_mcm(n, (seed + i) % 100000, 1, dmax)) for i in range(cnt)]
+        ok = True
+        for inst, (t, split) in zip(insts, pd.solve_mcm_batch(insts)):
+            wc, _, ws = orc.mcm_solve(inst.dims)
+            ok = ok and np.array_equal(t.cells, wc) and np.array_equal(split, ws)
+        name = f"mcm_batch n={n} x{cnt} dmax={dmax}"
     elif kind == "mcm":
         n = int(r.integers(2, 700))
         dims = orc.generate_mcm(n, seed % 1000, 1, int(r.choice([100, 322, 1290])))
