@@ -1976,8 +1976,10 @@ int32_t pipedp_chain_fold_cycles(uint32_t hi, uint32_t m32, int32_t mode, double
 
 int32_t pipedp_profile_read(uint64_t* out, int32_t count, int32_t reset) {
 #ifdef PIPEDP_PROFILE
-  unsigned long long h[128];
+  unsigned long long h[128], hc[128];
   CK(cudaMemcpyFromSymbol(h, pipedp_dev::g_prof, sizeof h));
+  CK(pipedp_cluster::profile_take(hc, reset != 0));  // the cluster TU's counters
+  for (int i = 0; i < 128; ++i) h[i] += hc[i];
   for (int i = 0; i < count && i < 128; ++i) out[i] = h[i];
   if (reset) {
     memset(h, 0, sizeof h);

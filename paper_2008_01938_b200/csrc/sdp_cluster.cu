@@ -223,11 +223,20 @@ __global__ void __launch_bounds__(32 * 20, 1) sdp_cluster_kernel(const Params p)
         for (int d = lane + 32; d >= lane + 1; --d)
           if ((lm.nbits >> (d - lane - 1)) & 1u) nxt = O::apply(nxt, ring[pos0 - d]);
       }
+      PROF_DECL(t_wm);
+      PROF_DECL(t_wf);
+      PROF_DECL(t_tot);
+      const long long t_start = PROF_NOW();
       for (int64_t b = 0; b < nb; ++b) {
         const int64_t c = a1 + 32 * b + lane;
         const int slot = (int)(b % kMid);
+        long long t0 = PROF_NOW();
         mbar_wait(&mid_full[slot], (unsigned)((b / kMid) & 1));
+        PROF_ADD(t_wm, t0);
+        t0 = PROF_NOW();
         mbar_wait(&fm_full[slot], (unsigned)((b / kMid) & 1));
+        PROF_ADD(t_wf, t0);
+        (void)t0;
         T acc = O::apply(O::apply(mid_part[slot * 32 + lane], fm_part[slot * 32 + lane]), nxt);
         if (IsIdem<OP>::value) {
           idem_closure<OP, T>(acc, nxt, im);
@@ -241,6 +250,12 @@ __global__ void __launch_bounds__(32 * 20, 1) sdp_cluster_kernel(const Params p)
         __syncwarp();
         if (lane == 0) mbar_arrive(&batch_done[b % kBars]);
       }
+      PROF_ADD(t_tot, t_start);
+      (void)t_start;
+      PROF_FLUSH(0, t_wm);
+      PROF_FLUSH(1, t_wf);
+      PROF_FLUSH(2, t_tot);
+      PROF_FLUSH(3, nb);
     } else if (role < 0) {
       // idle: shares sub-partition 0 with the chain
     } else if (role < M) {
@@ -258,19 +273,33 @@ __global__ void __launch_bounds__(32 * 20, 1) sdp_cluster_kernel(const Params p)
       const int my = r >> 1;
       const int n96 = p.j_96 - p.j_p, nmid = p.j_64 - p.j_p;
       if (near || M > 1) {
+        PROF_DECL(t_w1);
+        PROF_DECL(t_w2);
+        PROF_DECL(t_f);
+        long long cntb = 0;
         for (int64_t b = my; b < nb; b += slot_stride) {
+          ++cntb;
           const int64_t c = a1 + 32 * b + lane;
           const T* rb = ring + (int)(c & (R - 1)) + R;
           T acc;
+          long long t0 = PROF_NOW();
           if (near) {
             wait_batches(batch_done, b - 1);  // batches <= b-2 final
+            PROF_ADD(t_w1, t0);
+            t0 = PROF_NOW();
             acc = fold_smem<OP>(id, smem_u32(rb), nob_mid + n96, nmid - n96);
             acc = O::apply(acc, la_ring_group<OP, T>(rb, mlm.far));
+            PROF_ADD(t_f, t0);
           } else {
             wait_batches(batch_done, b - 2);  // batches <= b-3 final
+            PROF_ADD(t_w1, t0);
+            t0 = PROF_NOW();
             acc = fold_smem<OP>(id, smem_u32(rb), nob_mid, n96);
+            PROF_ADD(t_f, t0);
+            t0 = PROF_NOW();
             const int rs = (int)(b % kRem);
             mbar_wait(&cl_full[rs], (unsigned)((b / kRem) & 1));
+            PROF_ADD(t_w2, t0);
             for (int q = 0; q < p.C - 1; ++q) acc = O::apply(acc, cl_part[(q * kRem + rs) * 32 + lane]);
             __syncwarp();
             if (lane == 0) arm(&cl_full[rs], 128u * (uint32_t)(p.C - 1));  // phase of batch b + kRem
@@ -280,6 +309,11 @@ __global__ void __launch_bounds__(32 * 20, 1) sdp_cluster_kernel(const Params p)
           __syncwarp();
           if (lane == 0) mbar_arrive(&(near ? mid_full : fm_full)[slot]);
         }
+        PROF_FLUSH(near ? 8 : 12, t_w1);
+        PROF_FLUSH(near ? 9 : 13, t_f);
+        PROF_FLUSH(near ? 10 : 14, t_w2);
+        PROF_FLUSH(near ? 11 : 15, cntb);
+        (void)cntb;
       }
     } else if (role < M + p.writers) {
       // --------------------------------- writers -----------------------------
@@ -446,5 +480,17 @@ cudaError_t launch(const ClusterPlan& P, const int64_t* d_offsets, const int64_t
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
+
+#ifdef PIPEDP_PROFILE
+// this translation unit's own role-profiler counters (each TU is its own module)
+cudaError_t profile_take(unsigned long long* out128, bool reset) {
+  cudaError_t e = cudaMemcpyFromSymbol(out128, pipedp_dev::g_prof, 128 * sizeof(unsigned long long));
+  if (e == cudaSuccess && reset) {
+    static const unsigned long long zero[128] = {};
+    e = cudaMemcpyToSymbol(pipedp_dev::g_prof, zero, sizeof zero);
+  }
+  return e;
+}
+#endif
 
 }  // namespace pipedp_cluster

@@ -34,4 +34,8 @@ bool plan(const int64_t* offsets, int32_t k, int32_t a1, int64_t n, int op, int 
 cudaError_t launch(const ClusterPlan& p, const int64_t* d_offsets, const int64_t* d_init, int64_t* d_out,
                    cudaStream_t st);
 
+#ifdef PIPEDP_PROFILE
+cudaError_t profile_take(unsigned long long* out128, bool reset);
+#endif
+
 }  // namespace pipedp_cluster
