@@ -33,6 +33,7 @@ constexpr int kRem = 32;     // producer -> finisher partial slots (batches)
 constexpr int kBars = 64;    // batch_done ring
 constexpr int kAvail = 256;  // writer -> producer "batch pushed" barriers
 constexpr int kMaxCluster = 16;
+constexpr int kNearWarps = 4;  // two pairs, each splitting one batch's near fold
 
 struct Params {
   int64_t n;
@@ -92,29 +93,42 @@ __device__ __forceinline__ int32_t lds(uint32_t a) {
   return v;
 }
 
-// fold the words at byte offsets nob[0, cnt) below... (nob = -4 a) from base
+// fold the words at byte offsets nob[0, cnt) (nob = -4 a) from base: eight
+// independent loads per trip and the < 8 rest issued together (absent slots
+// read the base word and fold the identity), so no load waits on the previous
+// one's fold -- the [64, 96) group has only ~8 offsets on C2, where a
+// one-at-a-time head / tail loop cost ~430 cycles per batch
 template <int OP>
 __device__ __forceinline__ int32_t fold_smem(int32_t acc, uint32_t base, const int32_t* nob, int cnt) {
   using O = SemiOp<OP, int32_t>;
+  const int32_t id = SemiId<OP, int32_t>::value();
   int j = 0;
-  for (; j < cnt && (reinterpret_cast<uintptr_t>(nob + j) & 15); ++j) acc = O::apply(acc, lds(base + nob[j]));
 #pragma unroll 1
   for (; j + 8 <= cnt; j += 8) {
-    const int4 o0 = *reinterpret_cast<const int4*>(nob + j);
-    const int4 o1 = *reinterpret_cast<const int4*>(nob + j + 4);
-    const int32_t v0 = lds(base + o0.x), v1 = lds(base + o0.y), v2 = lds(base + o0.z), v3 = lds(base + o0.w);
-    const int32_t v4 = lds(base + o1.x), v5 = lds(base + o1.y), v6 = lds(base + o1.z), v7 = lds(base + o1.w);
-    acc = O::apply(O::apply(O::apply(O::apply(acc, v0), v1), O::apply(v2, v3)),
-                   O::apply(O::apply(v4, v5), O::apply(v6, v7)));
+    int32_t v[8];
+#pragma unroll
+    for (int t = 0; t < 8; ++t) v[t] = lds(base + nob[j + t]);
+    acc = O::apply(acc, O::apply(O::apply(O::apply(v[0], v[1]), O::apply(v[2], v[3])),
+                                 O::apply(O::apply(v[4], v[5]), O::apply(v[6], v[7]))));
   }
-#pragma unroll 1
-  for (; j < cnt; ++j) acc = O::apply(acc, lds(base + nob[j]));
+  if (j < cnt) {
+    int32_t v[8];
+#pragma unroll
+    for (int t = 0; t < 7; ++t) {
+      const bool live = j + t < cnt;
+      const int32_t x = lds(base + (live ? nob[j + t] : 0));
+      v[t] = live ? x : id;
+    }
+    v[7] = id;
+    acc = O::apply(acc, O::apply(O::apply(O::apply(v[0], v[1]), O::apply(v[2], v[3])),
+                                 O::apply(O::apply(v[4], v[5]), O::apply(v[6], v[7]))));
+  }
   return acc;
 }
 
 // ---- shared-memory layouts (identical arithmetic in every CTA) ------------
 struct FinLayout {
-  uint32_t ring, small, nob_mid, mid_part, fm_part, cl_part, bars, end;
+  uint32_t ring, small, nob_mid, mid_part, fm_part, nb_part, cl_part, bars, end;
 };
 __host__ __device__ inline FinLayout fin_layout(const Params& p) {
   FinLayout L;
@@ -129,11 +143,13 @@ __host__ __device__ inline FinLayout fin_layout(const Params& p) {
   o += 4u * kMid * 32;
   L.fm_part = o;
   o += 4u * kMid * 32;
+  L.nb_part = o;  // the second near half's partials
+  o += 4u * kMid * 32;
   L.cl_part = o;  // [C-1][kRem][32]
   o += 4u * (p.C - 1) * kRem * 32;
   o = (o + 7) & ~7u;
-  L.bars = o;  // batch_done[kBars] | mid_full[kMid] | cl_full[kRem] | fm_full[kMid]
-  o += 8u * (kBars + kMid + kRem + kMid);
+  L.bars = o;  // batch_done[kBars] | mid_full[kMid] | cl_full[kRem] | fm_full[kMid] | nb_full[kMid]
+  o += 8u * (kBars + kMid + kRem + kMid + kMid);
   L.end = o;
   return L;
 }
@@ -188,7 +204,9 @@ __global__ void __launch_bounds__(32 * 20, 1) sdp_cluster_kernel(const Params p)
     uint64_t* mid_full = batch_done + kBars;
     uint64_t* cl_full = mid_full + kMid;
     uint64_t* fm_full = cl_full + kRem;
+    uint64_t* nb_full = fm_full + kMid;
     T* fm_part = reinterpret_cast<T*>(smem + FL.fm_part);
+    T* nb_part = reinterpret_cast<T*>(smem + FL.nb_part);
     const int R = p.fin_r;
     const int nsmall = p.k - p.j_64;
     for (int j = tid; j < nsmall; j += blockDim.x) small[j] = (int32_t)p.offsets[p.j_64 + j];
@@ -205,6 +223,7 @@ __global__ void __launch_bounds__(32 * 20, 1) sdp_cluster_kernel(const Params p)
       for (int s = 0; s < kBars + kMid; ++s) mbar_init(&batch_done[s], 1);
       for (int s = 0; s < kRem; ++s) mbar_init(&cl_full[s], 1);
       for (int s = 0; s < kMid; ++s) mbar_init(&fm_full[s], 1);
+      for (int s = 0; s < kMid; ++s) mbar_init(&nb_full[s], 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
       for (int s = 0; s < kRem; ++s) arm(&cl_full[s], 128u * (uint32_t)(p.C - 1));
     }
@@ -262,17 +281,21 @@ __global__ void __launch_bounds__(32 * 20, 1) sdp_cluster_kernel(const Params p)
       // ----------------------------------- mid -------------------------------
       // split by how far back the operands are, so only a short fold sits on
       // the chain's critical path:
-      //   near warps (even ids):  [l+33, 63] ring group + [64, 96): batch b-2
-      //                           final, needed when b-1 finishes;
-      //   far-mid warps (odd):    [96, a_p) + the producers' partials: batch
-      //                           b-3 final, two batches of slack.
+      //   near warps (roles 0..3): [l+33, 63] ring group + [64, 96): batch b-2
+      //     final, needed when b-1 finishes -- the pace-setting fold, so each
+      //     batch's is split over a PAIR of warps (pairs alternate batches):
+      //     half A the ring group, half B [64, 96); B hands its partial to A
+      //     (mbarrier), A combines and hands the sum to the chain;
+      //   far-mid warps (roles 4..M-1): [96, a_p) + the producers' partials:
+      //     batch b-3 final, two batches of slack.
       const LaMasks mlm = la_masks(small, nsmall, lane);
       const int r = role;
-      const bool near = (r & 1) == 0;
-      const int slot_stride = near ? (M + 1) / 2 : M / 2;
-      const int my = r >> 1;
+      const bool near = r < kNearWarps;
+      const int slot_stride = near ? kNearWarps / 2 : M - kNearWarps;
+      const int my = near ? r >> 1 : r - kNearWarps;
+      const bool half_b = near && (r & 1);
       const int n96 = p.j_96 - p.j_p, nmid = p.j_64 - p.j_p;
-      if (near || M > 1) {
+      {
         PROF_DECL(t_w1);
         PROF_DECL(t_w2);
         PROF_DECL(t_f);
@@ -281,15 +304,27 @@ __global__ void __launch_bounds__(32 * 20, 1) sdp_cluster_kernel(const Params p)
           ++cntb;
           const int64_t c = a1 + 32 * b + lane;
           const T* rb = ring + (int)(c & (R - 1)) + R;
+          const int slot = (int)(b % kMid);
           T acc;
           long long t0 = PROF_NOW();
           if (near) {
             wait_batches(batch_done, b - 1);  // batches <= b-2 final
             PROF_ADD(t_w1, t0);
             t0 = PROF_NOW();
-            acc = fold_smem<OP>(id, smem_u32(rb), nob_mid + n96, nmid - n96);
-            acc = O::apply(acc, la_ring_group<OP, T>(rb, mlm.far));
+            if (half_b) {
+              acc = fold_smem<OP>(id, smem_u32(rb), nob_mid + n96, nmid - n96);  // [64, 96)
+              nb_part[slot * 32 + lane] = acc;
+              __syncwarp();
+              if (lane == 0) mbar_arrive(&nb_full[slot]);
+              PROF_ADD(t_f, t0);
+              continue;
+            }
+            acc = la_ring_group<OP, T>(rb, mlm.far);  // d in [l+33, 63]
             PROF_ADD(t_f, t0);
+            t0 = PROF_NOW();
+            mbar_wait(&nb_full[slot], (unsigned)((b / kMid) & 1));
+            PROF_ADD(t_w2, t0);
+            acc = O::apply(acc, nb_part[slot * 32 + lane]);
           } else {
             wait_batches(batch_done, b - 2);  // batches <= b-3 final
             PROF_ADD(t_w1, t0);
@@ -304,15 +339,14 @@ __global__ void __launch_bounds__(32 * 20, 1) sdp_cluster_kernel(const Params p)
             __syncwarp();
             if (lane == 0) arm(&cl_full[rs], 128u * (uint32_t)(p.C - 1));  // phase of batch b + kRem
           }
-          const int slot = (int)(b % kMid);
           (near ? mid_part : fm_part)[slot * 32 + lane] = acc;
           __syncwarp();
           if (lane == 0) mbar_arrive(&(near ? mid_full : fm_full)[slot]);
         }
-        PROF_FLUSH(near ? 8 : 12, t_w1);
-        PROF_FLUSH(near ? 9 : 13, t_f);
-        PROF_FLUSH(near ? 10 : 14, t_w2);
-        PROF_FLUSH(near ? 11 : 15, cntb);
+        PROF_FLUSH(near ? (half_b ? 16 : 8) : 12, t_w1);
+        PROF_FLUSH(near ? (half_b ? 17 : 9) : 13, t_f);
+        PROF_FLUSH(near ? (half_b ? 18 : 10) : 14, t_w2);
+        PROF_FLUSH(near ? (half_b ? 19 : 11) : 15, cntb);
         (void)cntb;
       }
     } else if (role < M + p.writers) {
@@ -410,7 +444,7 @@ bool plan(const int64_t* offsets, int32_t k, int32_t a1, int64_t n, int op, int 
   }
   if (P.j_p < 64) return false;  // too little far work for a cluster
   P.cluster = kMaxCluster;
-  P.mid_warps = 6;  // near / far-mid alternate (C2: 4 -> 157 ms, 6 -> 136 ms, 8 -> 146 ms)
+  P.mid_warps = kNearWarps + 3;  // two near pairs + three far-mid warps
   P.writers = 4;
   P.prod_warps = 8;
   P.fin_r = 1;  // >= a_p + 32 (kRem + 4), a power of two

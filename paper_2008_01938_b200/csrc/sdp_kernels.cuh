@@ -485,6 +485,24 @@ __device__ __forceinline__ T la_ring_group(const T* p, uint32_t far) {
   return v[0];
 }
 
+// The ring group's slots i in [I0, I1) only (d = 63 - i), tree-reduced: a
+// batch's group split over several warps.
+template <int OP, typename T, int I0, int I1>
+__device__ __forceinline__ T la_ring_range(const T* p, uint32_t far) {
+  using O = SemiOp<OP, T>;
+  const T id = SemiId<OP, T>::value();
+  constexpr int W = 32;
+  T v[W];
+#pragma unroll
+  for (int i = 0; i < W; ++i) v[i] = (i >= I0 && i < I1 && i < 31) ? sel_or_id(p[-(63 - i)], id, far, 31 - i) : id;
+#pragma unroll
+  for (int w = 16; w >= 1; w >>= 1) {
+#pragma unroll
+    for (int i = 0; i < w; ++i) v[i] = O::apply(v[i], v[i + w]);
+  }
+  return v[0];
+}
+
 // Offset classes of one instance, from its raw offsets in shared memory.
 struct SdpClasses {
   int jr, jf, jn, j32;

@@ -28,6 +28,6 @@ nb = max(p[3], 1)
 print(plan.describe(), f"{e0.elapsed_time(e1):.2f} ms", "batches", nb,
       f"ns/batch {e0.elapsed_time(e1) * 1e6 / nb:.1f}")
 print(f"  chain: wait mid {p[0] / nb:.0f}  wait far-mid {p[1] / nb:.0f}  total {p[2] / nb:.0f} cycles/batch")
-for nm, o in (("near", 8), ("far-mid", 12)):
+for nm, o in (("near A", 8), ("near B", 16), ("far-mid", 12)):
     c = max(p[o + 3], 1)
-    print(f"  {nm}: per batch it folds: wait {p[o] / c:.0f}  fold {p[o + 1] / c:.0f}  wait producers {p[o + 2] / c:.0f} cycles")
+    print(f"  {nm}: per batch it folds: wait {p[o] / c:.0f}  fold {p[o + 1] / c:.0f}  second wait {p[o + 2] / c:.0f} cycles")
