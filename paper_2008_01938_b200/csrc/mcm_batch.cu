@@ -54,12 +54,13 @@ namespace pipedp_mcmb {
 constexpr int kPitch = 66;                          // even, >= kMaxN + 1
 constexpr int kSquare = (kMaxN + 2) * kPitch;       // words (rows 0..n+1)
 constexpr uint32_t kCellLimit = 1u << 24;           // packed-key validity (see above)
-constexpr int kCtasPerSm = 11;                      // 11 x (19 + 1) KB of the 228 KB
+constexpr int kCtasPerSm = 11;                      // 11 x (19.5 + 1) KB of the 228 KB
 
 struct Smem {
   uint32_t M[kSquare];
-  uint32_t p[2][kMaxN + 2];    // raw dimensions, per instance
+  uint32_t p[2][kMaxN + 3];    // raw dimensions, per instance (zero padded: p[n+1], p[n+2])
   uint32_t pk[2][kMaxN + 2];   // dimensions << 6 (instance B: reversed, [n+1-k])
+  uint32_t part[2][2][kMaxN + 2];  // per instance: B's and C's partial keys by row
 };
 
 // One warp's instance in the shared square (see the layout note).
@@ -67,92 +68,93 @@ struct Geo {
   int sg;              // +1 (A) or -1 (B)
   int gm;              // address offset
   int om;              // weight index offset: weight of k at pk[sg k + om]
-  int spare;           // a column no cell of this instance uses (B's partial keys)
   uint32_t* M;
   const uint32_t* p;   // raw dimensions (natural order)
   const uint32_t* pk;  // weights << 6, walked +1 per term
+  uint32_t* partB;     // B's / C's partial keys by row (between the phases)
+  uint32_t* partC;
   __device__ __forceinline__ int at(int r, int c) const { return sg * (kPitch * r + c) + gm; }
 };
 
-// Diagonals are taken in PAIRS (D, D+1): cell A = (r, r+D) and cell B =
-// (r, r+D+1) of the same row share the left operand M'(r, k) and the weight
-// p''[k] of every split column k in [r+1, r+D-1] -- all of those terms only
-// read diagonals < D -- so one lane folds both cells' terms over that range
-// with four loads per two terms (8 B per term instead of 12).  A's remaining
-// term (k = r) is folded too; B's two remaining terms (k = r and k = r+D, whose
-// operands lie on diagonal D) follow after the warp has finished diagonal D,
-// from B's partial key parked in the square's spare column (col 0 for the
-// upper-triangle instance, col P-1 for the reflected one: neither is a cell).
+// Diagonals are taken in TRIPLES (D, D+1, D+2): cells A = (r, r+D), B =
+// (r, r+D+1) and C = (r, r+D+2) of one row share the left operand M'(r, k) and
+// the weight p''[k] of every split column k in [r+2, r+D-1] -- all of those
+// terms only read diagonals < D -- so one lane folds the three cells' terms
+// over that range with five loads per three terms (6.7 B per term instead of
+// 12).  The rest, by when their operands are final:
+//   phase 1 (with the shared fold):  A: k = r, r+1;  B: k = r+1 (D >= 2)
+//   phase 2 (diagonal D final):      B: k = r, r+D (B done);  C: k = r+1, r+D
+//   phase 3 (diagonal D+1 final):    C: k = r, r+D+1 (C done)
+// B's and C's partial keys wait in `part` between the phases.
 //
 // Phase 1: cells [base, base + 32 / G) of diagonal D (r = 1 + i), G lanes
-// per cell, G a compile-time stride (the term loop walks four pointers with
-// immediate offsets).  The per-cell constant c & 63 (the right operand's low
+// per cell; G is compile-time for the one-lane passes (the term loop walks
+// five pointers with immediate offsets) and run-time for the rarer short
+// ones (i-cache).  The per-cell constant c & 63 (the right operand's low
 // field) is taken off once after the fold: every sum is < 2^32 before it, so
 // the min commutes.
-template <int LGT>  // LGT >= 0: compile-time G = 2^LGT; LGT < 0: G = 2^lgr at run time (the rarer short passes)
-__device__ __forceinline__ bool pair_pass(int D, int base, int nA, int lane, const Geo& g, int64_t* oc,
-                                          int64_t* os, int lgr = 0) {
+template <int LGT>  // LGT >= 0: compile-time G = 2^LGT; LGT < 0: G = 2^lgr at run time
+__device__ __forceinline__ bool tri_pass(int D, int base, int nA, int lane, const Geo& g, int64_t* oc,
+                                         int64_t* os, int lgr = 0) {
   const int lg = LGT >= 0 ? LGT : lgr;
   const int G = 1 << lg;
   const int SL = G, SR = G * kPitch;
   const int q = lane & (G - 1);
   const int i = base + lane / G;
-  const int r = 1 + i, cA = r + D, cB = cA + 1;
-  const bool liveA = i < nA, liveB = i + 1 < nA;
+  const int r = 1 + i, cA = r + D, cB = cA + 1, cC = cA + 2;
+  const bool liveA = i < nA, liveB = i + 1 < nA, liveC = i + 2 < nA;
   uint32_t a0 = 0xFFFFFFFFu, a1 = 0xFFFFFFFFu, b0 = 0xFFFFFFFFu, b1 = 0xFFFFFFFFu;
+  uint32_t c0 = 0xFFFFFFFFu, c1 = 0xFFFFFFFFu;
   if (liveA) {
     const uint32_t pr = g.p[r - 1];
-    const uint32_t prcA = pr * g.p[cA], prcB = pr * g.p[cB];  // p[n+1] is padding when !liveB
-    if (q == 0) a0 = prcA * g.pk[g.sg * r + g.om] + g.M[g.at(r, r)] + g.M[g.at(r + 1, cA)];  // k = r
-    const int kq = g.sg > 0 ? r + 1 + q : cA - 1 - q;  // this lane's first shared split column
+    // p[n+1], p[n+2] are padding when B / C do not exist
+    const uint32_t prcA = pr * g.p[cA], prcB = pr * g.p[cB], prcC = pr * g.p[cC];
+    if (q == 0) {
+      a0 = prcA * g.pk[g.sg * r + g.om] + g.M[g.at(r, r)] + g.M[g.at(r + 1, cA)];  // A: k = r
+      if (D >= 2) {
+        const uint32_t w = g.pk[g.sg * (r + 1) + g.om], l = g.M[g.at(r, r + 1)];
+        a1 = prcA * w + l + g.M[g.at(r + 2, cA)];                                   // A: k = r+1
+        if (liveB) b0 = prcB * w + l + g.M[g.at(r + 2, cB)];                        // B: k = r+1
+      }
+    }
+    const int kq = g.sg > 0 ? r + 2 + q : cA - 1 - q;  // this lane's first shared split column
     const uint32_t* L = g.M + g.at(r, kq);             // M'(r, k)
     const uint32_t* RA = g.M + g.at(kq + 1, cA);       // M'(k+1, cA)
-    // M'(k+1, cB); without a cell B (cB = n+1) the walk would read the other
-    // instance's spare column (harmless, unused -- but a cross-warp race to
-    // racecheck): walk A's own column instead
+    // M'(k+1, cB), M'(k+1, cC); without a cell B / C the walks would leave the
+    // instance (harmless, unused -- but a cross-warp race to racecheck): they
+    // walk A's own column instead
     const uint32_t* RB = liveB ? RA + g.sg : RA;
+    const uint32_t* RC = liveC ? RA + 2 * g.sg : RA;
     const uint32_t* W = g.pk + g.sg * kq + g.om;       // p''[k]
-    int cnt = (D - 1 - q + G - 1) >> lg;               // this lane's shared columns
-    for (; cnt >= 4; cnt -= 4) {
-      const uint32_t l0 = L[0], w0 = W[0], l1 = L[SL], w1 = W[G];
-      const uint32_t l2 = L[2 * SL], w2 = W[2 * G], l3 = L[3 * SL], w3 = W[3 * G];
-      a0 = min(a0, prcA * w0 + l0 + RA[0]);
-      b0 = min(b0, prcB * w0 + l0 + RB[0]);
-      a1 = min(a1, prcA * w1 + l1 + RA[SR]);
-      b1 = min(b1, prcB * w1 + l1 + RB[SR]);
-      a0 = min(a0, prcA * w2 + l2 + RA[2 * SR]);
-      b0 = min(b0, prcB * w2 + l2 + RB[2 * SR]);
-      a1 = min(a1, prcA * w3 + l3 + RA[3 * SR]);
-      b1 = min(b1, prcB * w3 + l3 + RB[3 * SR]);
-      L += 4 * SL;
-      RA += 4 * SR;
-      RB += 4 * SR;
-      W += 4 * G;
-    }
-    if (cnt >= 2) {
-      cnt -= 2;
+    int cnt = D >= 2 ? (D - 2 - q + G - 1) >> lg : 0;  // this lane's shared columns
+    for (; cnt >= 2; cnt -= 2) {
       const uint32_t l0 = L[0], w0 = W[0], l1 = L[SL], w1 = W[G];
       a0 = min(a0, prcA * w0 + l0 + RA[0]);
       b0 = min(b0, prcB * w0 + l0 + RB[0]);
+      c0 = min(c0, prcC * w0 + l0 + RC[0]);
       a1 = min(a1, prcA * w1 + l1 + RA[SR]);
       b1 = min(b1, prcB * w1 + l1 + RB[SR]);
+      c1 = min(c1, prcC * w1 + l1 + RC[SR]);
       L += 2 * SL;
       RA += 2 * SR;
       RB += 2 * SR;
+      RC += 2 * SR;
       W += 2 * G;
     }
     if (cnt) {
       const uint32_t l0 = L[0], w0 = W[0];
       a0 = min(a0, prcA * w0 + l0 + RA[0]);
       b0 = min(b0, prcB * w0 + l0 + RB[0]);
+      c0 = min(c0, prcC * w0 + l0 + RC[0]);
     }
   }
-  uint32_t ka = min(a0, a1), kb = min(b0, b1);
+  uint32_t ka = min(a0, a1), kb = min(b0, b1), kc = min(c0, c1);
 #pragma unroll
   for (int sh = 16; sh > 0; sh >>= 1) {
     if (sh < G) {
       ka = min(ka, __shfl_xor_sync(0xffffffffu, ka, sh));
       kb = min(kb, __shfl_xor_sync(0xffffffffu, kb, sh));
+      kc = min(kc, __shfl_xor_sync(0xffffffffu, kc, sh));
     }
   }
   bool ovf = false;
@@ -163,53 +165,60 @@ __device__ __forceinline__ bool pair_pass(int D, int base, int nA, int lane, con
     oc[r] = (int64_t)v;
     os[r] = (int64_t)(ka & 63u) - r + 1;
     ovf = v >= kCellLimit;
-    if (liveB) g.M[kPitch * r + g.spare] = kb;  // B's partial (still carries + (cB & 63))
+    g.partB[r] = kb;  // partials (still carrying + (c & 63)); unused without B / C
+    g.partC[r] = kc;
   }
   return ovf;
 }
 
-// Phase 2: B = (r, r+D+1) for r = 1 .. nB (nB <= 62: at most two cells per
-// lane), its two terms on diagonal D.  Every address is affine in r along
-// the diagonal, so the second cell's are the first's plus a constant.
-__device__ __forceinline__ bool pair_finish(int D, int nB, int lane, const Geo& g, int64_t* oc, int64_t* os) {
+// One more term of cell (r, c) at split column k (operands final).
+__device__ __forceinline__ uint32_t term(const Geo& g, uint32_t prc, int r, int k, int c) {
+  return prc * g.pk[g.sg * k + g.om] + g.M[g.at(r, k)] + g.M[g.at(k + 1, c)];
+}
+
+// finish cell (r, c) from its key (still carrying + (c & 63))
+__device__ __forceinline__ bool finish(const Geo& g, uint32_t key, int r, int c, int64_t* oc, int64_t* os) {
+  key -= (uint32_t)(c & 63);
+  const uint32_t v = key >> 6;
+  g.M[g.at(r, c)] = (key & ~63u) | (uint32_t)(c & 63);
+  oc[r] = (int64_t)v;
+  os[r] = (int64_t)(key & 63u) - r + 1;
+  return v >= kCellLimit;
+}
+
+// Phase 2 (diagonal D final): B = (r, r+D+1) done for r <= nA - 1 (terms
+// k = r, r+D); C = (r, r+D+2) for r <= nA - 2 takes k = r+1 and k = r+D.
+__device__ __forceinline__ bool tri_mid(int D, int nA, int lane, const Geo& g, int64_t* ocB, int64_t* osB) {
   bool ovf = false;
-  int r = 1 + lane;
-  if (r > nB) return false;
-  const int c = r + D + 1;
-  const int step = 32 * g.sg * (kPitch + 1);  // (r, c) -> (r + 32, c + 32)
-  const uint32_t* mrr = g.M + g.at(r, r);
-  const uint32_t* mr1c = g.M + g.at(r + 1, c);
-  const uint32_t* mrc1 = g.M + g.at(r, c - 1);
-  const uint32_t* mcc = g.M + g.at(c, c);
-  uint32_t* mrc = g.M + g.at(r, c);
-  uint32_t* sp = g.M + kPitch * r + g.spare;
-  const uint32_t* w1 = g.pk + g.sg * r + g.om;
-  const uint32_t* w2 = g.pk + g.sg * (c - 1) + g.om;
-  const uint32_t* pr = g.p + r - 1;
-  int cc = c;
 #pragma unroll 1
-  for (;;) {
-    const uint32_t prc = pr[0] * pr[D + 2];
-    uint32_t key = min(sp[0], prc * w1[0] + mrr[0] + mr1c[0]);  // k = r
-    key = min(key, prc * w2[0] + mrc1[0] + mcc[0]);               // k = c - 1
-    key -= (uint32_t)(cc & 63);
-    const uint32_t v = key >> 6;
-    mrc[0] = (key & ~63u) | (uint32_t)(cc & 63);
-    oc[r] = (int64_t)v;
-    os[r] = (int64_t)(key & 63u) - r + 1;
-    ovf |= v >= kCellLimit;
-    r += 32;
-    if (r > nB) break;
-    cc += 32;
-    mrr += step;
-    mr1c += step;
-    mrc1 += step;
-    mcc += step;
-    mrc += step;
-    sp += 32 * kPitch;
-    w1 += 32 * g.sg;
-    w2 += 32 * g.sg;
-    pr += 32;
+  for (int i = lane; i + 1 < nA; i += 32) {
+    const int r = 1 + i, cB = r + D + 1;
+    const uint32_t pr = g.p[r - 1];
+    const uint32_t prcB = pr * g.p[cB];
+    uint32_t kb = min(g.partB[r], term(g, prcB, r, r, cB));
+    kb = min(kb, term(g, prcB, r, r + D, cB));
+    ovf |= finish(g, kb, r, cB, ocB, osB);
+    if (i + 2 < nA) {
+      const int cC = cB + 1;
+      const uint32_t prcC = pr * g.p[cC];
+      uint32_t kc = min(g.partC[r], term(g, prcC, r, r + 1, cC));
+      g.partC[r] = min(kc, term(g, prcC, r, r + D, cC));
+    }
+  }
+  return ovf;
+}
+
+// Phase 3 (diagonal D+1 final): C = (r, r+D+2) done for r <= nA - 2 (terms
+// k = r, r+D+1).
+__device__ __forceinline__ bool tri_end(int D, int nA, int lane, const Geo& g, int64_t* ocC, int64_t* osC) {
+  bool ovf = false;
+#pragma unroll 1
+  for (int i = lane; i + 2 < nA; i += 32) {
+    const int r = 1 + i, cC = r + D + 2;
+    const uint32_t prcC = g.p[r - 1] * g.p[cC];
+    uint32_t kc = min(g.partC[r], term(g, prcC, r, r, cC));
+    kc = min(kc, term(g, prcC, r, r + D + 1, cC));
+    ovf |= finish(g, kc, r, cC, ocC, osC);
   }
   return ovf;
 }
@@ -232,11 +241,12 @@ __global__ void __launch_bounds__(64, kCtasPerSm) mcm_batch_warp(int32_t n, int6
   g.sg = warp == 0 ? 1 : -1;
   g.gm = warp == 0 ? 0 : kPitch * (n + 2) + n + 1;
   g.om = warp == 0 ? 0 : n + 1;
-  g.spare = warp == 0 ? 0 : kPitch - 1;
   g.M = s.M;
   g.p = s.p[warp];
   g.pk = s.pk[warp];
-  for (int i = lane; i <= kMaxN + 1; i += 32) {
+  g.partB = s.part[warp][0];
+  g.partC = s.part[warp][1];
+  for (int i = lane; i <= kMaxN + 2; i += 32) {
     const uint32_t d = i <= n ? (uint32_t)gd[i] : 0u;
     s.p[warp][i] = d;
     if (i <= n) s.pk[warp][g.sg * i + g.om] = d << 6;
@@ -249,24 +259,29 @@ __global__ void __launch_bounds__(64, kCtasPerSm) mcm_batch_warp(int32_t n, int6
   __syncwarp();
   bool ovf = false;
   int64_t db = 0;  // lin(r, r+D) = db(D) + r
-  for (int D = 1; D < n; D += 2) {
+  for (int D = 1; D < n; D += 3) {
     db += n - (D - 1);
-    const int nA = n - D;  // cells on diagonal D (B: nA - 1 on D + 1)
+    const int nA = n - D;  // cells on diagonal D (B: nA - 1, C: nA - 2)
     int base = 0;
-    for (; base + 32 <= nA; base += 32) ovf |= pair_pass<0>(D, base, nA, lane, g, oc + db, os + db);
+    for (; base + 32 <= nA; base += 32) ovf |= tri_pass<0>(D, base, nA, lane, g, oc + db, os + db);
     const int rem = nA - base;
     if (rem > 0) {
       // G = 2^lg lanes per remaining cell: rem G <= 32, and G / 2 < D
       const int lg = min(5 - (rem > 1 ? 32 - __clz(rem - 1) : 0), D > 1 ? 32 - __clz(D - 1) : 0);
-      if (lg == 0) ovf |= pair_pass<0>(D, base, nA, lane, g, oc + db, os + db);
-      else ovf |= pair_pass<-1>(D, base, nA, lane, g, oc + db, os + db, lg);
+      if (lg == 0) ovf |= tri_pass<0>(D, base, nA, lane, g, oc + db, os + db);
+      else ovf |= tri_pass<-1>(D, base, nA, lane, g, oc + db, os + db, lg);
     }
     __syncwarp();
+    const int64_t dbB = db + (n - D), dbC = dbB + (n - D - 1);  // lin bases of diagonals D+1, D+2
     if (nA > 1) {
-      db += n - D;
-      ovf |= pair_finish(D, nA - 1, lane, g, oc + db, os + db);
+      ovf |= tri_mid(D, nA, lane, g, oc + dbB, os + dbB);
       __syncwarp();
     }
+    if (nA > 2) {
+      ovf |= tri_end(D, nA, lane, g, oc + dbC, os + dbC);
+      __syncwarp();
+    }
+    db = dbC;
   }
   if (__any_sync(0xffffffffu, ovf) && lane == 0) atomicOr(overflow, 2);
 }
