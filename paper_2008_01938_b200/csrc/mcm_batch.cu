@@ -171,54 +171,104 @@ __device__ __forceinline__ bool tri_pass(int D, int base, int nA, int lane, cons
   return ovf;
 }
 
-// One more term of cell (r, c) at split column k (operands final).
-__device__ __forceinline__ uint32_t term(const Geo& g, uint32_t prc, int r, int k, int c) {
-  return prc * g.pk[g.sg * k + g.om] + g.M[g.at(r, k)] + g.M[g.at(k + 1, c)];
-}
-
-// finish cell (r, c) from its key (still carrying + (c & 63))
-__device__ __forceinline__ bool finish(const Geo& g, uint32_t key, int r, int c, int64_t* oc, int64_t* os) {
-  key -= (uint32_t)(c & 63);
-  const uint32_t v = key >> 6;
-  g.M[g.at(r, c)] = (key & ~63u) | (uint32_t)(c & 63);
-  oc[r] = (int64_t)v;
-  os[r] = (int64_t)(key & 63u) - r + 1;
-  return v >= kCellLimit;
-}
-
 // Phase 2 (diagonal D final): B = (r, r+D+1) done for r <= nA - 1 (terms
 // k = r, r+D); C = (r, r+D+2) for r <= nA - 2 takes k = r+1 and k = r+D.
+// Every address is affine in r along the diagonal: a lane's second cell
+// (r + 32) is its first's plus a constant.
 __device__ __forceinline__ bool tri_mid(int D, int nA, int lane, const Geo& g, int64_t* ocB, int64_t* osB) {
   bool ovf = false;
+  int i = lane;
+  if (i + 1 >= nA) return false;
+  const int r0 = 1 + i;
+  const int dm = 32 * g.sg * (kPitch + 1), dw = 32 * g.sg;
+  // B: k = r (left M'(r,r), right M'(r+1, cB)), k = r+D (left M'(r, r+D), right M'(r+D+1, cB))
+  const uint32_t* mrr = g.M + g.at(r0, r0);
+  const uint32_t* mr1B = g.M + g.at(r0 + 1, r0 + D + 1);
+  const uint32_t* mrD = g.M + g.at(r0, r0 + D);
+  const uint32_t* mD1B = g.M + g.at(r0 + D + 1, r0 + D + 1);
+  uint32_t* mB = g.M + g.at(r0, r0 + D + 1);
+  // C: k = r+1 (left M'(r, r+1), right M'(r+2, cC)), k = r+D (left M'(r, r+D), right M'(r+D+1, cC))
+  const uint32_t* mr_1 = g.M + g.at(r0, r0 + 1);
+  const uint32_t* m2C = g.M + g.at(r0 + 2, r0 + D + 2);
+  const uint32_t* mD1C = g.M + g.at(r0 + D + 1, r0 + D + 2);
+  const uint32_t* wr = g.pk + g.sg * r0 + g.om;
+  const uint32_t* wD = g.pk + g.sg * (r0 + D) + g.om;
+  const uint32_t* pr = g.p + r0 - 1;
 #pragma unroll 1
-  for (int i = lane; i + 1 < nA; i += 32) {
-    const int r = 1 + i, cB = r + D + 1;
-    const uint32_t pr = g.p[r - 1];
-    const uint32_t prcB = pr * g.p[cB];
-    uint32_t kb = min(g.partB[r], term(g, prcB, r, r, cB));
-    kb = min(kb, term(g, prcB, r, r + D, cB));
-    ovf |= finish(g, kb, r, cB, ocB, osB);
+  for (int r = r0;;) {
+    const uint32_t prv = pr[0], prcB = prv * pr[D + 2];
+    const uint32_t wrv = wr[0], wDv = wD[0], lD = mrD[0];
+    uint32_t kb = min(g.partB[r], prcB * wrv + mrr[0] + mr1B[0]);
+    kb = min(kb, prcB * wDv + lD + mD1B[0]);
+    const int cB = r + D + 1;
+    kb -= (uint32_t)(cB & 63);
+    const uint32_t v = kb >> 6;
+    mB[0] = (kb & ~63u) | (uint32_t)(cB & 63);
+    ocB[r] = (int64_t)v;
+    osB[r] = (int64_t)(kb & 63u) - r + 1;
+    ovf |= v >= kCellLimit;
     if (i + 2 < nA) {
-      const int cC = cB + 1;
-      const uint32_t prcC = pr * g.p[cC];
-      uint32_t kc = min(g.partC[r], term(g, prcC, r, r + 1, cC));
-      g.partC[r] = min(kc, term(g, prcC, r, r + D, cC));
+      const uint32_t prcC = prv * pr[D + 3];
+      uint32_t kc = min(g.partC[r], prcC * wr[g.sg] + mr_1[0] + m2C[0]);
+      g.partC[r] = min(kc, prcC * wDv + lD + mD1C[0]);
     }
+    i += 32;
+    if (i + 1 >= nA) break;
+    r += 32;
+    mrr += dm;
+    mr1B += dm;
+    mrD += dm;
+    mD1B += dm;
+    mB += dm;
+    mr_1 += dm;
+    m2C += dm;
+    mD1C += dm;
+    wr += dw;
+    wD += dw;
+    pr += 32;
   }
   return ovf;
 }
 
 // Phase 3 (diagonal D+1 final): C = (r, r+D+2) done for r <= nA - 2 (terms
-// k = r, r+D+1).
+// k = r: M'(r,r) + M'(r+1, cC); k = r+D+1: M'(r, r+D+1) + M'(cC, cC)).
 __device__ __forceinline__ bool tri_end(int D, int nA, int lane, const Geo& g, int64_t* ocC, int64_t* osC) {
   bool ovf = false;
+  int i = lane;
+  if (i + 2 >= nA) return false;
+  const int r0 = 1 + i;
+  const int dm = 32 * g.sg * (kPitch + 1), dw = 32 * g.sg;
+  const uint32_t* mrr = g.M + g.at(r0, r0);
+  const uint32_t* mr1C = g.M + g.at(r0 + 1, r0 + D + 2);
+  const uint32_t* mrD1 = g.M + g.at(r0, r0 + D + 1);
+  const uint32_t* mCC = g.M + g.at(r0 + D + 2, r0 + D + 2);
+  uint32_t* mC = g.M + g.at(r0, r0 + D + 2);
+  const uint32_t* wr = g.pk + g.sg * r0 + g.om;
+  const uint32_t* wD1 = g.pk + g.sg * (r0 + D + 1) + g.om;
+  const uint32_t* pr = g.p + r0 - 1;
 #pragma unroll 1
-  for (int i = lane; i + 2 < nA; i += 32) {
-    const int r = 1 + i, cC = r + D + 2;
-    const uint32_t prcC = g.p[r - 1] * g.p[cC];
-    uint32_t kc = min(g.partC[r], term(g, prcC, r, r, cC));
-    kc = min(kc, term(g, prcC, r, r + D + 1, cC));
-    ovf |= finish(g, kc, r, cC, ocC, osC);
+  for (int r = r0;;) {
+    const uint32_t prcC = pr[0] * pr[D + 3];
+    uint32_t kc = min(g.partC[r], prcC * wr[0] + mrr[0] + mr1C[0]);
+    kc = min(kc, prcC * wD1[0] + mrD1[0] + mCC[0]);
+    const int cC = r + D + 2;
+    kc -= (uint32_t)(cC & 63);
+    const uint32_t v = kc >> 6;
+    mC[0] = (kc & ~63u) | (uint32_t)(cC & 63);
+    ocC[r] = (int64_t)v;
+    osC[r] = (int64_t)(kc & 63u) - r + 1;
+    ovf |= v >= kCellLimit;
+    i += 32;
+    if (i + 2 >= nA) break;
+    r += 32;
+    mrr += dm;
+    mr1C += dm;
+    mrD1 += dm;
+    mCC += dm;
+    mC += dm;
+    wr += dw;
+    wD1 += dw;
+    pr += 32;
   }
   return ovf;
 }
