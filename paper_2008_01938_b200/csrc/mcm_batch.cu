@@ -120,11 +120,12 @@ __device__ __forceinline__ bool tri_pass(int D, int base, int nA, int lane, cons
     const int kq = g.sg > 0 ? r + 2 + q : cA - 1 - q;  // this lane's first shared split column
     const uint32_t* L = g.M + g.at(r, kq);             // M'(r, k)
     const uint32_t* RA = g.M + g.at(kq + 1, cA);       // M'(k+1, cA)
-    // M'(k+1, cB), M'(k+1, cC); without a cell B / C the walks would leave the
-    // instance (harmless, unused -- but a cross-warp race to racecheck): they
-    // walk A's own column instead
-    const uint32_t* RB = liveB ? RA + g.sg : RA;
-    const uint32_t* RC = liveC ? RA + 2 * g.sg : RA;
+    // M'(k+1, cB), M'(k+1, cC).  Without a cell B / C (cB = n+1, cC = n+2) the
+    // walks run down column 65 or 0 of the square, which no cell of either
+    // instance uses (unused values, no race) -- and keep the pass's loads on
+    // distinct banks (redirecting them to A's column made 2-way conflicts)
+    const uint32_t* RB = RA + g.sg;
+    const uint32_t* RC = RA + 2 * g.sg;
     const uint32_t* W = g.pk + g.sg * kq + g.om;       // p''[k]
     int cnt = D >= 2 ? (D - 2 - q + G - 1) >> lg : 0;  // this lane's shared columns
     for (; cnt >= 2; cnt -= 2) {
