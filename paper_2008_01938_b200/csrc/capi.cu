@@ -694,7 +694,10 @@ struct pipedp_mcm_plan {
   int* h_overflow;    // pinned
   int64_t total_chunks;
   int launches;
-  int last_bits;
+  int last_bits;      // 0: an async execute not resolved yet (mcm_resolve)
+  int gate;           // overflow bits the next launch is conditional on (0: always)
+  bool pending;       // last execute ran with on-device reruns; flag not read yet
+  cudaEvent_t ev_done;
   int64_t maxd3;      // max_dim^3 over the plan's instances
   bool packed_now;    // this execute's tiled launch uses them
   // tiled kernel
@@ -731,9 +734,9 @@ int mcm_wave_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split
     McmWave W{n, P->total_chunks, P->d_chunk_base, P->d_done, P->d_next};
     if (bits == 32) {
       CK(cudaMemsetAsync(P->d_v32, 0, sizeof(uint32_t) * (n + 1), st));
-      mcm_wavefront<uint32_t><<<(unsigned)grid, threads, 0, st>>>(W, pb, P->d_v32, cb, sb, P->d_overflow);
+      mcm_wavefront<uint32_t><<<(unsigned)grid, threads, 0, st>>>(W, pb, P->d_v32, cb, sb, P->d_overflow, P->gate);
     } else {
-      mcm_wavefront<int64_t><<<(unsigned)grid, threads, 0, st>>>(W, pb, cb, cb, sb, P->d_overflow);
+      mcm_wavefront<int64_t><<<(unsigned)grid, threads, 0, st>>>(W, pb, cb, cb, sb, P->d_overflow, P->gate);
     }
     CK(cudaGetLastError());
   }
@@ -750,7 +753,8 @@ int mcm_tiled_launch(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStr
   CK(cudaMemsetAsync(split, 0, sizeof(int64_t) * (n + 1), st));
   McmTiled S{n, (int32_t)N, P->ntasks, P->d_pp, P->d_tiles, P->d_keys, P->d_tile_flags,
              P->d_tile_flags + ntiles, P->d_tasks, P->d_next, cells, split, P->d_overflow,
-             env_int("PIPEDP_MCM_BLOCKED", 0) ? 1 : env_int("PIPEDP_MCM_NEAR", 2), P->packed_now ? 1 : 0};
+             env_int("PIPEDP_MCM_BLOCKED", 0) ? 1 : env_int("PIPEDP_MCM_NEAR", 2), P->packed_now ? 1 : 0,
+             P->gate};
   if (P->d.tile == 32) {
     CK(cudaFuncSetAttribute(t32::mcm_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)t32::kTiledSmemBytes));
@@ -805,6 +809,12 @@ size_t mcm_square_bytes(int64_t n, size_t vb) {
   return (size_t)(P * P + 1) * vb + (size_t)(n + 1 + 4) * 4;
 }
 
+// CTAs of a square / triangle batch launch: one per instance, or for a gated
+// rerun (usually a no-op) a few per SM looping over the instances
+unsigned mcm_grid(const pipedp_mcm_plan* P) {
+  return (unsigned)(P->gate ? std::min<int64_t>(P->batch, 4 * (int64_t)sm_count()) : P->batch);
+}
+
 int mcm_smem_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split, cudaStream_t st) {
   const int64_t n = P->n;
   const size_t sq = mcm_square_bytes(n, bits / 8);
@@ -820,16 +830,16 @@ int mcm_smem_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split
     const int thr = std::max(32, std::min(128, env_int("PIPEDP_MCM_SQ_THREADS", n <= 96 ? 64 : 128))) / 32 * 32;
     if (bits == 32 && P->packed_now && n <= 64) {
       CK(cudaFuncSetAttribute(mcm_smem_square<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq));
-      mcm_smem_square<uint32_t, true><<<(unsigned)P->batch, thr, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
-                                                                            split, P->d_overflow);
+      mcm_smem_square<uint32_t, true><<<mcm_grid(P), thr, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
+                                                                            split, P->d_overflow, P->gate);
     } else if (bits == 32) {
       CK(cudaFuncSetAttribute(mcm_smem_square<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq));
-      mcm_smem_square<uint32_t><<<(unsigned)P->batch, thr, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
-                                                                      split, P->d_overflow);
+      mcm_smem_square<uint32_t><<<mcm_grid(P), thr, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
+                                                                      split, P->d_overflow, P->gate);
     } else {
       CK(cudaFuncSetAttribute(mcm_smem_square<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sq));
-      mcm_smem_square<int64_t><<<(unsigned)P->batch, thr, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
-                                                                     split, P->d_overflow);
+      mcm_smem_square<int64_t><<<mcm_grid(P), thr, sq, st>>>((int32_t)n, P->batch, P->d_dims, cells,
+                                                                     split, P->d_overflow, P->gate);
     }
     CK(cudaGetLastError());
     return PIPEDP_OK;
@@ -837,13 +847,13 @@ int mcm_smem_launch(pipedp_mcm_plan* P, int bits, int64_t* cells, int64_t* split
   if (bits == 32) {
     CK(cudaFuncSetAttribute(mcm_smem_cta<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)P->d.smem32));
-    mcm_smem_cta<uint32_t><<<(unsigned)P->batch, P->d.threads, P->d.smem32, st>>>(
-        n, P->batch, P->d_dims, cells, split, P->d_overflow);
+    mcm_smem_cta<uint32_t><<<mcm_grid(P), P->d.threads, P->d.smem32, st>>>(
+        n, P->batch, P->d_dims, cells, split, P->d_overflow, P->gate);
   } else {
     CK(cudaFuncSetAttribute(mcm_smem_cta<int64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)P->d.smem64));
-    mcm_smem_cta<int64_t><<<(unsigned)P->batch, P->d.threads, P->d.smem64, st>>>(
-        n, P->batch, P->d_dims, cells, split, P->d_overflow);
+    mcm_smem_cta<int64_t><<<mcm_grid(P), P->d.threads, P->d.smem64, st>>>(
+        n, P->batch, P->d_dims, cells, split, P->d_overflow, P->gate);
   }
   CK(cudaGetLastError());
   return PIPEDP_OK;
@@ -867,13 +877,53 @@ int mcm_execute(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t
                          P->maxd3 < (1ll << 24) && env_int("PIPEDP_MCM_PACKED_SQUARE", 1) != 0;
   P->packed_now = (tiled_pk || square_pk) && env_int("PIPEDP_MCM_PACKED", 1) != 0;
   int kernel = P->d.kernel;  // this execute's kernel (the plan itself is never changed)
+  // 64-bit fallback of this plan's kernel: one launch (asynchronous reruns), or
+  // an instance-by-instance wavefront for a batch whose 64-bit table does not
+  // fit shared memory (those few shapes keep the host round trip)
+  const int kernel64 = kernel == PIPEDP_MCM_SMEM && P->d.smem64 > 227 * 1024 ? PIPEDP_MCM_WAVEFRONT
+                       : kernel == PIPEDP_MCM_TILED                          ? PIPEDP_MCM_WAVEFRONT
+                                                                             : kernel;
+  auto launch = [&](int kern, int b, int gate) -> int32_t {
+    P->gate = gate;
+    int32_t rc;
+    if (kern == PIPEDP_MCM_SMEM) rc = mcm_smem_launch(P, b, cells, split, st);
+    else if (kern == PIPEDP_MCM_TILED && b == 32) rc = mcm_tiled_launch(P, cells, split, st);
+    else rc = mcm_wave_launch(P, b, cells, split, st);
+    P->gate = 0;
+    P->launches += kern == PIPEDP_MCM_WAVEFRONT ? (int)P->batch : 1;
+    return rc;
+  };
+  CK(cudaMemsetAsync(P->d_overflow, 0, sizeof(int), st));
+  if (bits == 64) {
+    TRY(launch(kernel, 64, 0));
+    P->last_bits = 64;
+    P->pending = false;
+    return PIPEDP_OK;
+  }
+  if (!(kernel64 == PIPEDP_MCM_WAVEFRONT && P->batch > 1)) {
+    // no host round trip: the reruns are launched behind the attempt and do
+    // their work only if it raised their overflow bit (mcm_gated_off), so the
+    // device plan stays asynchronous (and CUDA-graph capturable)
+    const bool packed = P->packed_now;
+    TRY(launch(kernel, 32, 0));
+    if (packed) {  // bit 2: a packed key could wrap -> the unpacked fold
+      P->packed_now = false;
+      const int32_t rc = launch(kernel, 32, 2);
+      P->packed_now = packed;
+      TRY(rc);
+    }
+    TRY(launch(kernel64, 64, 1));  // bit 1: a value reached 2^30 -> exact int64
+    if (!P->ev_done) CK(cudaEventCreateWithFlags(&P->ev_done, cudaEventDisableTiming));
+    CK(cudaEventRecord(P->ev_done, st));
+    P->last_bits = 0;
+    P->pending = true;
+    return PIPEDP_OK;
+  }
   for (;;) {
     CK(cudaMemsetAsync(P->d_overflow, 0, sizeof(int), st));
-    if (kernel == PIPEDP_MCM_SMEM) TRY(mcm_smem_launch(P, bits, cells, split, st));
-    else if (kernel == PIPEDP_MCM_TILED && bits == 32) TRY(mcm_tiled_launch(P, cells, split, st));
-    else TRY(mcm_wave_launch(P, bits, cells, split, st));
-    P->launches += kernel == PIPEDP_MCM_WAVEFRONT ? (int)P->batch : 1;
+    TRY(launch(kernel, bits, 0));
     P->last_bits = bits;
+    P->pending = false;
     if (bits == 64) return PIPEDP_OK;
     CK(cudaMemcpyAsync(P->h_overflow, P->d_overflow, sizeof(int), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -883,10 +933,21 @@ int mcm_execute(pipedp_mcm_plan* P, int64_t* cells, int64_t* split, cudaStream_t
       continue;
     }
     bits = 64;  // a value reached 2^30: redo exactly in 64-bit
-    // a 64-bit square/triangle table that no longer fits shared memory: the
-    // exact int64 wavefront, instance by instance
-    if (kernel == PIPEDP_MCM_SMEM && P->d.smem64 > 227 * 1024) kernel = PIPEDP_MCM_WAVEFRONT;
+    kernel = kernel64;
   }
+}
+
+// After an asynchronous execute: which attempt's output stands (waits for the
+// execute; the host-buffer path and describe() need it).
+int32_t mcm_resolve(pipedp_mcm_plan* P) {
+  if (!P->pending) return PIPEDP_OK;
+  CK(cudaEventSynchronize(P->ev_done));
+  int f = 0;
+  CK(cudaMemcpy(&f, P->d_overflow, sizeof(int), cudaMemcpyDeviceToHost));
+  P->last_bits = (f & 1) ? 64 : 32;
+  if (f & 2) P->packed_now = false;
+  P->pending = false;
+  return PIPEDP_OK;
 }
 
 }  // namespace
@@ -1762,6 +1823,7 @@ int32_t pipedp_mcm_plan_execute(pipedp_mcm_plan_t P, int64_t* d_cells, int64_t* 
 int32_t pipedp_mcm_plan_describe(pipedp_mcm_plan_t P, char* name, size_t cap, int32_t* bits,
                                  int32_t* launches) {
   if (!P) return fail(PIPEDP_E_INVALID_PARAMS, "null plan");
+  TRY(mcm_resolve(P));  // an asynchronous execute: read its overflow bits
   const bool square = mcm_square_bytes(P->n, (P->last_bits ? P->last_bits : P->d.bits) / 8) <= kSmemBudget &&
                       env_int("PIPEDP_MCM_SQUARE", 1) != 0;
   const int lb = P->last_bits ? P->last_bits : P->d.bits;
@@ -1794,6 +1856,7 @@ int32_t pipedp_mcm_plan_destroy(pipedp_mcm_plan_t P) {
   cudaFree(P->d_tile_flags);
   cudaFree(P->d_tasks);
   if (P->h_overflow) cudaFreeHost(P->h_overflow);
+  if (P->ev_done) cudaEventDestroy(P->ev_done);
   delete P;
   return PIPEDP_OK;
 }
@@ -1872,7 +1935,8 @@ static int32_t mcm_solve_host(int64_t batch, int64_t n, const int64_t* dims, int
         fill->p = nullptr;
       }
     });
-  const int32_t rc = pipedp_mcm_plan_execute(P, (int64_t*)d_cells, (int64_t*)d_split, W->stream);
+  int32_t rc = pipedp_mcm_plan_execute(P, (int64_t*)d_cells, (int64_t*)d_split, W->stream);
+  if (rc == PIPEDP_OK) rc = mcm_resolve(P);  // which attempt's table stands (its value width)
   if (touch.joinable()) touch.join();
   TRY(rc);
   // 32-bit run without the overflow flag: every cell < 2^30; split indices

@@ -87,6 +87,15 @@ __device__ __forceinline__ McmBest<T> mcm_cell_terms(const T* V, const int32_t* 
   return best;
 }
 
+// A rerun launched behind the first attempt without a host round trip: it
+// does its work only if the attempt raised one of the `gate` overflow bits
+// (bit 2: a packed key could wrap -> unpacked rerun; bit 1: a 32-bit value
+// reached 2^30 -> 64-bit rerun); gate 0 = unconditional.  Stream order makes
+// the earlier launches' flag visible.
+__device__ __forceinline__ bool mcm_gated_off(const int* overflow, int gate) {
+  return gate != 0 && (*reinterpret_cast<const volatile int*>(overflow) & gate) == 0;
+}
+
 // -----------------------------------------------------------------------------
 // Small n: one CTA per instance, the whole triangle in shared memory,
 // diagonal by diagonal (n-1 __syncthreads).  Also the batched kernel.
@@ -95,10 +104,13 @@ template <typename T>
 __global__ void __launch_bounds__(512)
     mcm_smem_cta(int64_t n, int64_t batch, const int64_t* __restrict__ g_dims,
                  int64_t* __restrict__ out_cells, int64_t* __restrict__ out_split,
-                 int* __restrict__ overflow) {
+                 int* __restrict__ overflow, int gate = 0) {
   extern __shared__ __align__(16) unsigned char smem[];
-  const int64_t inst = blockIdx.x;
-  if (inst >= batch) return;
+  if (mcm_gated_off(overflow, gate)) return;
+  bool ovf = false;
+  // instance loop: a gated rerun launches a small grid (its gated-off cost
+  // stays a few hundred CTAs), the first attempt one CTA per instance
+  for (int64_t inst = blockIdx.x; inst < batch; inst += gridDim.x) {
   const int64_t cc = n * (n + 1) / 2;
   T* V = reinterpret_cast<T*>(smem);  // cc + 1 entries
   int32_t* p = reinterpret_cast<int32_t*>(V + ((cc + 1 + 3) & ~3ll));
@@ -113,7 +125,6 @@ __global__ void __launch_bounds__(512)
     os[i] = 0;
   }
   __syncthreads();
-  bool ovf = false;
   for (int64_t D = 1; D < n; ++D) {
     const int64_t ncell = n - D;
     int G = 1;  // lanes per cell: spread the terms when the diagonal is short
@@ -139,6 +150,7 @@ __global__ void __launch_bounds__(512)
     }
     __syncthreads();
   }
+  }  // instances
   if (ovf) atomicOr(overflow, 1);
 }
 
@@ -169,7 +181,8 @@ template <typename T>
 __global__ void __launch_bounds__(256)
     mcm_wavefront(const McmWave W, const int32_t* __restrict__ p, T* V, int64_t* out_cells,
                   int64_t* __restrict__ out_split,
-                  int* __restrict__ overflow) {
+                  int* __restrict__ overflow, int gate = 0) {
+  if (mcm_gated_off(overflow, gate)) return;
   const int lane = threadIdx.x & 31;
   const int64_t n = W.n;
   for (;;) {
@@ -265,10 +278,13 @@ template <typename T, bool PACKED = false>
 __global__ void __launch_bounds__(128)
     mcm_smem_square(int32_t n, int64_t batch, const int64_t* __restrict__ g_dims,
                     int64_t* __restrict__ out_cells, int64_t* __restrict__ out_split,
-                    int* __restrict__ overflow) {
+                    int* __restrict__ overflow, int gate = 0) {
+  if (mcm_gated_off(overflow, gate)) return;
   extern __shared__ __align__(16) unsigned char smem[];
-  const int64_t inst = blockIdx.x;
-  if (inst >= batch) return;
+  bool ovf = false, ovf2 = false;
+  // instance loop: a gated rerun launches a small grid (its gated-off cost
+  // stays a few hundred CTAs), the first attempt one CTA per instance
+  for (int64_t inst = blockIdx.x; inst < batch; inst += gridDim.x) {
   const int P = n + 1;
   T* M = reinterpret_cast<T*>(smem);                         // [P][P], row r = 1..n
   int32_t* p = reinterpret_cast<int32_t*>(M + P * P + 1);    // dims p_0..p_n
@@ -284,7 +300,6 @@ __global__ void __launch_bounds__(128)
     os[i] = 0;
   }
   __syncthreads();
-  bool ovf = false, ovf2 = false;
   int64_t db = 0;  // lin(r, r+D) = db(D) + r, db(D) = D*n - D(D-1)/2
   for (int D = 1; D < n; ++D) {
     db += n - (D - 1);
@@ -337,6 +352,7 @@ __global__ void __launch_bounds__(128)
     }
     __syncthreads();
   }
+  }  // instances
   if (ovf) atomicOr(overflow, 1);
   if (ovf2) atomicOr(overflow, 2);
 }

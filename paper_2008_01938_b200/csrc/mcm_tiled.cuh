@@ -59,6 +59,7 @@ struct McmTiled {
   int32_t blocked;             // near in-tile pipeline: 0 CTA-wide folds per step, 1 8x8 sub-blocks, 2 pull
   int32_t packed;              // far tasks fold (value << 5 | k-in-half) keys: every cell < 2^25 required
                                // (a finished cell >= 2^25 raises overflow bit 2 -> unpacked rerun)
+  int32_t gate;                // rerun gate (mcm_gated_off): 0 = always run
 };
 
 __host__ __device__ __forceinline__ int64_t tiled_index(int64_t I, int64_t J, int64_t N) {

@@ -185,3 +185,40 @@ def test_batch_warp_kernel_and_square(gpu, oracle, monkeypatch, warp):
         for inst, (t, split) in zip(insts, gpu.solve_mcm_batch(insts)):
             wc, _, ws = oracle.mcm_solve(inst.dims)
             assert np.array_equal(t.cells, wc) and np.array_equal(split, ws)
+
+
+@pytest.mark.parametrize("shape", [(1, 300, 1, 100), (1, 300, 5000, 20000), (40, 64, 1, 100), (9, 64, 240, 255)])
+def test_plan_execute_is_graph_capturable(gpu, oracle, shape):
+    # the device plan's overflow reruns are launched behind the first attempt,
+    # gated on its flag on the device (no host round trip), so a whole
+    # execute -- including a rerun it turns out to need (wide dims: 64-bit;
+    # dims near 255: cells past 2^24 -> unpacked) -- replays from a CUDA graph
+    import torch
+    batch, n, lo, hi = shape
+    insts = [oracle.generate_mcm(n, 40 + i, lo, hi) for i in range(batch)]
+    dims = np.concatenate([np.asarray(d, np.int64) for d in insts])
+    plan = gpu.McmPlan(batch, n, dims)
+    size = gpu.cell_count(n) + 1
+    c = torch.full((batch * size,), -1, dtype=torch.int64, device="cuda")
+    s = torch.full_like(c, -1)
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        plan.execute(c.data_ptr(), s.data_ptr(), st.cuda_stream)  # warm-up: kernel attributes, scratch
+    torch.cuda.synchronize()
+    c.fill_(-1)
+    s.fill_(-1)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        plan.execute(c.data_ptr(), s.data_ptr(), st.cuda_stream)
+    for _ in range(2):
+        g.replay()
+        torch.cuda.synchronize()
+        cc, ss = c.cpu().numpy(), s.cpu().numpy()
+        for b, d in enumerate(insts):
+            wc, _, ws = oracle.mcm_solve(d)
+            assert np.array_equal(cc[b * size:(b + 1) * size], wc)
+            assert np.array_equal(ss[b * size:(b + 1) * size], ws)
+        c.fill_(-1)
+        s.fill_(-1)
+    plan.close()
