@@ -382,3 +382,41 @@ def test_cluster_pipeline(gpu, oracle, op, n, k, cap):
             os.environ["PIPEDP_SDP_CHUNKED"] = old
     want, _ = oracle.sdp_solve(inst.offsets, inst.init, n, op)
     assert np.array_equal(t.cells, want)
+
+
+@pytest.mark.parametrize("shape", [
+    ("chunked rank", 3_000_000 + 77, 300, 21, 2048, "min", {}),
+    ("cluster", 300_000 + 5, 400, 22, 4096, "max", {"PIPEDP_SDP_CHUNKED": "0"}),
+    ("jump", 200_000, 3, 23, 6, "saturating-add", {}),
+    ("v2 mod-add", 150_000, 200, 24, 1500, "modular-add", {"PIPEDP_SDP_CLUSTER": "0"}),
+])
+def test_plan_execute_is_graph_capturable(gpu, oracle, shape, monkeypatch):
+    # the device plans are asynchronous: a whole execute (matrix powers, the
+    # cooperative entry-state chain, the chunk batch / the cluster pipeline /
+    # jump segments) replays from a CUDA graph with the same table
+    import torch
+    _, n, k, seed, cap, op, env = shape
+    for key, v in env.items():
+        monkeypatch.setenv(key, v)
+    offs, init = oracle.generate_sdp(n, k, seed, False, cap)
+    if op == "saturating-add":
+        init = np.abs(init) % 1000
+    want, _ = oracle.sdp_solve(offs, init, n, op)
+    plan = gpu.SdpPlan(1, n, len(offs), len(init), offs, init, op)
+    d_init = torch.from_numpy(np.asarray(init, np.int64)).cuda()
+    out = torch.full((n,), -1, dtype=torch.int64, device="cuda")
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        plan.execute(d_init.data_ptr(), out.data_ptr(), st.cuda_stream)  # warm-up
+    torch.cuda.synchronize()
+    out.fill_(-1)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        plan.execute(d_init.data_ptr(), out.data_ptr(), st.cuda_stream)
+    for _ in range(2):
+        g.replay()
+        torch.cuda.synchronize()
+        assert np.array_equal(out.cpu().numpy(), want)
+        out.fill_(-1)
+    plan.close()
