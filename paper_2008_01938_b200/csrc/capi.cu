@@ -69,6 +69,7 @@ struct SdpDispatch {
   int method;   // 0 pipeline, 1 the paper's tournament (prefix), 2 the paper's naive method
   SdpV2Shape s2;
   bool cluster = false;  // one instance over a thread-block cluster (sdp_cluster.cu)
+  bool vals32 = false;   // the paper's methods: every value of the instance fits int32 (a 4-byte ring)
   pipedp_cluster::ClusterPlan cplan{};
 };
 
@@ -489,7 +490,27 @@ template <int OP, typename T, bool ASSOC>
 int launch_sdp_t(const SdpDispatch& d, int64_t batch, const int64_t* offs, const int64_t* init,
                  int64_t* out, const SdpRemote& rm, cudaStream_t st) {
   if (ASSOC && d.method != 0) {  // the paper's comparison methods (one instance, int64)
-    if (d.method == 1) sdp_tournament<OP><<<1, 1024, 0, st>>>(d.shape.n, d.shape.k, offs, init, out);
+    if (d.method == 1) {
+      // the last a_1 + 1 cells in shared memory when they fit (Table I bucket 1)
+      // the last a_1 + 1 cells in shared memory when they fit -- as 4-byte
+      // words for a 32-bit value class (Table I buckets 1, 2) -- else operands
+      // through L2 (a single SM's L2 bandwidth bounds that path)
+      const int64_t a1 = d.shape.a1;
+      const size_t ring64 = sizeof(int64_t) * (size_t)(a1 + 1), ring32 = sizeof(int32_t) * (size_t)(a1 + 1);
+      const bool few = (d.shape.k + 1023) / 1024 <= 8;  // offsets per thread: 8 or 32 register slots
+      auto ring_launch = [&](auto kern, size_t bytes) -> int32_t {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        kern<<<1, 1024, bytes, st>>>(d.shape.n, d.shape.k, offs, init, out, (int32_t)(a1 + 1));
+        return PIPEDP_OK;
+      };
+      if (ring64 <= 200 * 1024) {
+        TRY(few ? ring_launch(sdp_tournament<OP, int64_t, 8>, ring64) : ring_launch(sdp_tournament<OP, int64_t, 32>, ring64));
+      } else if (d.vals32 && ring32 <= 200 * 1024) {
+        TRY(few ? ring_launch(sdp_tournament<OP, int32_t, 8>, ring32) : ring_launch(sdp_tournament<OP, int32_t, 32>, ring32));
+      } else {
+        sdp_tournament<OP, void><<<1, 1024, 0, st>>>(d.shape.n, d.shape.k, offs, init, out, 1);
+      }
+    }
     else sdp_naive<OP><<<1, 1024, 0, st>>>(d.shape.n, d.shape.k, offs, init, out);
     CK(cudaGetLastError());
     return PIPEDP_OK;
@@ -1613,6 +1634,7 @@ int32_t pipedp_sdp_plan_set_method(pipedp_sdp_plan_t P, int32_t method) {
   // keeps the strict-order pipeline, which is what the reference computes
   if (method != PIPEDP_SDP_PIPELINE && P->d.bits == 32) {
     P->d.bits = 64;
+    P->d.vals32 = true;  // (the tournament keeps its shared-memory ring in 4-byte words)
   }
   P->d.method = method;
   if (method != PIPEDP_SDP_PIPELINE) P->d.chunked = false;  // the paper's methods run the instance as is

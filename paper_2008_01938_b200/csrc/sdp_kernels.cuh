@@ -35,6 +35,8 @@
 //    with a gpu-scope release every few batches.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace pipedp_dev {
@@ -1215,47 +1217,94 @@ namespace pipedp_dev {
 // the host keeps the strict pipeline for mixed-sign saturating-add.
 //
 // prefix (tournament): thread t folds a contiguous slice of offsets in j order,
-// then a ceil(log2)-level tree (one barrier per level) combines the slices in
-// order: O(n log k) steps.
-template <int OP>
+// then a ceil(log2)-level tree combines the slices in order: the levels inside
+// a warp are shuffles (no barrier), the levels across the CTA's warps one
+// shared-memory exchange and a last warp of shuffles -- two barriers per cell
+// instead of one per level: O(n log k) steps, as the method is meant to run.
+// RT (int64_t / int32_t for a 32-bit value class; void: none): the last
+// R >= a_1 + 1 cells also live in shared memory (when they fit), so a cell's
+// operands are shared-memory loads instead of L2 round trips.
+template <int OP, typename RT, int NR = 32>  // NR: register-resident slice size (ring path)
 __global__ void __launch_bounds__(1024, 1)
     sdp_tournament(int64_t n, int32_t k, const int64_t* __restrict__ g_offsets,
-                   const int64_t* __restrict__ g_init, int64_t* out) {
+                   const int64_t* __restrict__ g_init, int64_t* out, int32_t R) {
   using O = SemiOp<OP, int64_t>;
-  __shared__ int64_t red[1024];
-  __shared__ uint8_t hv[1024];
-  const int t = threadIdx.x, nt = blockDim.x;
+  const int64_t id = SemiId<OP, int64_t>::value();
+  constexpr bool RING = !std::is_same<RT, void>::value;
+  using W = typename std::conditional<RING, RT, int64_t>::type;
+  extern __shared__ __align__(16) unsigned char ring_raw[];
+  W* ring = reinterpret_cast<W*>(ring_raw);  // [R] (RING)
+  __shared__ int64_t red[32];
+  const int t = threadIdx.x, nt = blockDim.x, lane = t & 31, warp = t >> 5, nw = nt >> 5;
   const int64_t a1 = g_offsets[0];
-  for (int64_t i = t; i < a1; i += nt) out[i] = g_init[i];
+  for (int64_t i = t; i < a1; i += nt) {
+    out[i] = g_init[i];
+    if (RING) ring[i % R] = (W)g_init[i];
+  }
   __threadfence();
   __syncthreads();
   const int per = (k + nt - 1) / nt;
   const int lo = min(k, t * per), hi = min(k, lo + per);
-  int P = 1;
-  while (P < nt && (P * per) < k) P <<= 1;  // threads holding a slice, rounded up
+  int32_t pos = (int32_t)(a1 % R);  // i mod R
+  // a slice of <= 32 offsets stays in registers (ring path): every cell's
+  // loads then issue back to back
+  constexpr int kRegOffs = NR;
+  int32_t roff[kRegOffs];
+#pragma unroll
+  for (int u = 0; u < kRegOffs; ++u) roff[u] = lo + u < hi ? (int32_t)g_offsets[lo + u] : 0;
   for (int64_t i = a1; i < n; ++i) {
-    int64_t acc = 0;
-    bool have = false;
-    for (int j = lo; j < hi; ++j) {
-      const int64_t v = __ldcg(reinterpret_cast<const long long*>(out + i - __ldg(g_offsets + j)));
-      acc = have ? O::apply(acc, v) : v;
-      have = true;
-    }
-    red[t] = acc;
-    hv[t] = have;
-    __syncthreads();
-    for (int s = 1; s < P; s <<= 1) {  // tournament levels, left (x) right
-      if ((t & (2 * s - 1)) == 0 && t + s < P && hv[t + s]) {
-        red[t] = hv[t] ? O::apply(red[t], red[t + s]) : red[t + s];
-        hv[t] = 1;
+    int64_t acc = id;
+    if (RING && hi - lo <= kRegOffs) {
+#pragma unroll
+      for (int u = 0; u < kRegOffs; ++u) {
+        if (lo + u < hi) {
+          int32_t q = pos - roff[u];
+          q += q < 0 ? R : 0;
+          acc = O::apply(acc, (int64_t)ring[q]);
+        }
       }
-      __syncthreads();
+    } else if (RING) {
+      for (int j = lo; j < hi; ++j) {
+        int32_t q = pos - (int32_t)__ldg(g_offsets + j);
+        q += q < 0 ? R : 0;
+        acc = O::apply(acc, (int64_t)ring[q]);
+      }
+    } else {
+      // the slice's L2 round trips in flight together: its offsets are
+      // loop-invariant (registers, loaded once), sixteen operand loads per trip
+      int j = lo;
+      for (; j < hi; j += 16) {
+        int64_t v[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u)
+          v[u] = j + u < hi ? (int64_t)__ldcg(reinterpret_cast<const long long*>(out + i - __ldg(g_offsets + j + u)))
+                            : id;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) acc = O::apply(acc, v[u]);
+      }
     }
-    if (t == 0) {
-      out[i] = red[0];
-      __threadfence();
+#pragma unroll
+    for (int s = 1; s < 32; s <<= 1) {  // tournament levels inside the warp: left (x) right
+      const int64_t r = (int64_t)__shfl_down_sync(0xffffffffu, (long long)acc, s);
+      if ((lane & (2 * s - 1)) == 0) acc = O::apply(acc, r);
+    }
+    if (lane == 0) red[warp] = acc;
+    __syncthreads();
+    if (warp == 0) {  // the levels across warps
+      acc = lane < nw ? red[lane] : id;
+#pragma unroll
+      for (int s = 1; s < 32; s <<= 1) {
+        const int64_t r = (int64_t)__shfl_down_sync(0xffffffffu, (long long)acc, s);
+        if ((lane & (2 * s - 1)) == 0) acc = O::apply(acc, r);
+      }
+      if (lane == 0) {
+        out[i] = acc;
+        if (RING) ring[pos] = (W)acc;
+        else __threadfence();
+      }
     }
     __syncthreads();
+    pos = pos + 1 == R ? 0 : pos + 1;
   }
 }
 
