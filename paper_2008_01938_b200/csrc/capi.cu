@@ -1263,19 +1263,21 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
   unsigned long long *R = ZT + mat, *RT = R + mat;
   // out = A B for the power M^t_new: rows >= t_new (t_new < a1) are shifts,
   // written directly; only the rows above them are multiplied
+  // out = A B (and outT = out^T, written by the same kernels: the next
+  // product's right operand)
   auto product = [&](const unsigned long long* A, const unsigned long long* BT, unsigned long long* out,
-                     int64_t t_new, const int* prev, int* chg) {
+                     unsigned long long* outT, int64_t t_new, const int* prev, int* chg) {
     const int64_t rows = 64ll * W;
     const int64_t lim = t_new < a1 ? std::min<int64_t>(rows, (t_new + kBmR - 1) / kBmR * kBmR) : rows;
-    bm_mul<<<dim3((unsigned)W, (unsigned)(lim / kBmR)), 256, smem, st>>>(x32(A), x32(BT), 2 * W, out, prev, chg);
+    bm_mul<<<dim3((unsigned)W, (unsigned)(lim / kBmR)), 256, smem, st>>>(x32(A), x32(BT), 2 * W, out, prev, chg,
+                                                                          outT);
     if (lim < rows)
       bm_shift_rows<<<(unsigned)std::min<int64_t>(1024, ((rows - lim) * W + 255) / 256), 256, 0, st>>>(
-          out, W, t_new, lim, a1, chg);
+          out, W, t_new, lim, a1, chg, outT);
   };
   int64_t ex = 1, er = 0;  // exponents of X and R
   auto square = [&](int i) {  // X <- X X (then its transpose); flags track idempotence
-    product(X, XT, Z, 2 * ex, i ? flags + i - 1 : nullptr, flags + i);
-    bm_transpose<<<dim3((unsigned)W, (unsigned)W), 64, 0, st>>>(Z, W, ZT);
+    product(X, XT, Z, ZT, 2 * ex, i ? flags + i - 1 : nullptr, flags + i);
     std::swap(X, Z);
     std::swap(XT, ZT);
     ex *= 2;
@@ -1291,8 +1293,7 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
         have_r = true;
         er = ex;
       } else {  // R <- R X (powers of M commute)
-        product(R, XT, Z, er + ex, nullptr, nullptr);
-        bm_transpose<<<dim3((unsigned)W, (unsigned)W), 64, 0, st>>>(Z, W, ZT);
+        product(R, XT, Z, ZT, er + ex, nullptr, nullptr);
         std::swap(R, Z);
         std::swap(RT, ZT);
         er += ex;
@@ -1319,8 +1320,7 @@ static int32_t sdp_chunked_run(pipedp_sdp_plan_t P, const int64_t* d_init, int64
       CK(cudaMemcpyAsync(P->d_q, X, sizeof(unsigned long long) * mat, cudaMemcpyDeviceToDevice, st));
       Q = P->d_q;
       for (int b = 1, i = nsq + 1; b < B; b *= 2, ++i) {
-        product(X, XT, Z, er * 2 * b, flags + i - 1, flags + i);
-        bm_transpose<<<dim3((unsigned)W, (unsigned)W), 64, 0, st>>>(Z, W, ZT);
+        product(X, XT, Z, ZT, er * 2 * b, flags + i - 1, flags + i);
         CK(cudaGetLastError());
         std::swap(X, Z);
         std::swap(XT, ZT);
@@ -1581,7 +1581,7 @@ int32_t pipedp_sdp_plan_describe(pipedp_sdp_plan_t P, char* name, size_t cap, in
     int32_t nl = 1;
     if (P->d.chunked) {  // the launches of sdp_chunked_run, counted by replaying its ladder
       const int top = 63 - __builtin_clzll((unsigned long long)P->Lc);
-      auto prod = [&](int64_t t_new) { return 2 + (t_new < P->a1 ? 1 : 0); };  // mul + transpose (+ shift rows)
+      auto prod = [&](int64_t t_new) { return 1 + (t_new < P->a1 ? 1 : 0); };  // mul (+ shift rows), transposes fused
       int64_t ex = 1, er = 0;
       nl = 1;  // build
       for (int i = 0; i <= top; ++i) {

@@ -46,13 +46,16 @@ __global__ void bm_build(const int64_t* __restrict__ offsets, int32_t k, int32_t
 // shared memory 64 words at a time.  Grid (A1P/64, A1P/128).
 // Squaring support: `prev_changed` (nullable) = did the previous squaring
 // change the matrix; if not, X is idempotent (X X = X) and the tile is copied.
-// `changed` (nullable) records whether this product differs from X.
+// `changed` (nullable) records whether this product differs from X.  The
+// epilogue also writes the tile transposed into ZT (the next product's right
+// operand), so no separate transpose pass runs.
 constexpr int kBmR = 128;  // CTA output rows
 constexpr int kBmC = 64;   // CTA output columns (one 64-bit word)
 constexpr int kBmK = 32;   // 32-bit words per K stage (early exit between stages)
 __global__ void __launch_bounds__(256, 2) bm_mul(const uint32_t* __restrict__ X, const uint32_t* __restrict__ YT,
                                                  int32_t W32, unsigned long long* __restrict__ Z,
-                                                 const int* __restrict__ prev_changed, int* __restrict__ changed) {
+                                                 const int* __restrict__ prev_changed, int* __restrict__ changed,
+                                                 unsigned long long* __restrict__ ZT) {
   extern __shared__ __align__(16) uint32_t bm_smem[];
   constexpr int P = kBmK + 4;  // padded pitch (words), 16-byte rows
   uint32_t* xs = bm_smem;            // [128][P]
@@ -62,8 +65,13 @@ __global__ void __launch_bounds__(256, 2) bm_mul(const uint32_t* __restrict__ X,
   const int64_t r0 = (int64_t)blockIdx.y * kBmR, c0 = (int64_t)blockIdx.x * kBmC;
   const int W64 = W32 / 2;
   const unsigned long long* X64 = reinterpret_cast<const unsigned long long*>(X);
-  if (prev_changed && *prev_changed == 0) {  // stable: X X = X
+  if (prev_changed && *prev_changed == 0) {  // stable: X X = X (and Z^T = X^T = YT)
     if (t < kBmR) Z[(r0 + t) * W64 + c0 / 64] = X64[(r0 + t) * W64 + c0 / 64];
+    if (t < kBmR) {
+      const unsigned long long* YT64 = reinterpret_cast<const unsigned long long*>(YT);
+      const int64_t o = (c0 + (t & 63)) * W64 + r0 / 64 + (t >> 6);
+      ZT[o] = YT64[o];
+    }
     return;
   }
   const int tr = t / 16, tc = t % 16;  // rows 8 tr .. +8, columns tc + 16 j (j < 4)
@@ -120,6 +128,13 @@ __global__ void __launch_bounds__(256, 2) bm_mul(const uint32_t* __restrict__ X,
     const int64_t o = (r0 + t) * W64 + c0 / 64;
     Z[o] = zw[t];
     if (changed && zw[t] != X64[o]) atomicOr(changed, 1);
+    // the transposed tile (64 rows of Z^T, two words each) for the next
+    // product's right operand -- instead of a separate transpose launch
+    const int c = t & 63, h = t >> 6;
+    unsigned long long out = 0;
+#pragma unroll 8
+    for (int i = 0; i < 64; ++i) out |= ((zw[64 * h + i] >> c) & 1ull) << i;
+    ZT[(c0 + c) * W64 + r0 / 64 + h] = out;
   }
 }
 
@@ -127,29 +142,22 @@ __global__ void __launch_bounds__(256, 2) bm_mul(const uint32_t* __restrict__ X,
 // at time T + t) is state position r - t at time T.  Written directly instead
 // of multiplied; they differ from every other power's rows, so `changed` is set.
 __global__ void bm_shift_rows(unsigned long long* __restrict__ Z, int32_t W, int64_t t, int64_t r0, int32_t a1,
-                              int* changed) {
+                              int* changed, unsigned long long* __restrict__ ZT) {
   const int64_t rows = 64ll * W;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (rows - r0) * W;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = r0 + e / W, w = e % W, c = r - t;
     Z[r * W + w] = (r < a1 && c >= 0 && c / 64 == w) ? 1ull << (c % 64) : 0ull;
   }
+  // the same rows in Z^T: words [r0 / 64, W) of every row c hold bit r = c + t
+  // (r0 is a multiple of 128, so those words lie wholly in the shift rows)
+  const int64_t w0 = r0 / 64, nw = W - w0;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < rows * nw;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / nw, w = w0 + e % nw, r = c + t;
+    ZT[c * W + w] = (r < a1 && r >= r0 && r / 64 == w) ? 1ull << (r % 64) : 0ull;
+  }
   if (changed && blockIdx.x == 0 && threadIdx.x == 0) atomicOr(changed, 1);
-}
-
-// ZT = Z^T for bit-packed square matrices (W words per row): one 64 x 64 bit
-// block per CTA (64 threads), through shared memory.
-__global__ void __launch_bounds__(64) bm_transpose(const unsigned long long* __restrict__ Z, int32_t W,
-                                                   unsigned long long* __restrict__ ZT) {
-  __shared__ unsigned long long blk[64];
-  const int t = threadIdx.x;
-  const int64_t bi = blockIdx.y, bj = blockIdx.x;  // source block (rows 64 bi, word bj)
-  blk[t] = Z[(64 * bi + t) * W + bj];
-  __syncthreads();
-  unsigned long long out = 0;  // row t of the transposed block = bit t of every source row
-#pragma unroll 8
-  for (int i = 0; i < 64; ++i) out |= ((blk[i] >> t) & 1ull) << i;
-  ZT[(64 * bj + t) * W + bi] = out;
 }
 
 // E1 = Q (.) E0 over rows [0, a1): one warp per row; lane l takes columns
