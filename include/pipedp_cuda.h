@@ -214,9 +214,12 @@ int32_t pipedp_mcm_solve_batch(int64_t batch, int64_t n, const int64_t* dims, in
 typedef struct pipedp_mcm_plan* pipedp_mcm_plan_t;
 int32_t pipedp_mcm_plan_create(int64_t batch, int64_t n, const int64_t* h_dims, int32_t kernel,
                                int32_t device, pipedp_mcm_plan_t* plan_out);
-/* d_cells / d_split: [batch*(cell_count(n)+1)].  Synchronises `stream` once at
- * the end (the 32-bit kernels report a device-side overflow flag that decides
- * whether the 64-bit kernel must run). */
+/* d_cells / d_split: [batch*(cell_count(n)+1)].  Asynchronous (CUDA-graph
+ * capturable): the 32-bit attempt raises a device-side overflow flag, and the
+ * unpacked / 64-bit reruns queued behind it on `stream` run only if it did.
+ * (Batches whose 64-bit table does not fit shared memory synchronise `stream`
+ * once instead.)  describe() reports the value width that stood, waiting for
+ * the last execute if needed. */
 int32_t pipedp_mcm_plan_execute(pipedp_mcm_plan_t plan, int64_t* d_cells, int64_t* d_split,
                                 void* stream);
 int32_t pipedp_mcm_plan_describe(pipedp_mcm_plan_t plan, char* name, size_t name_cap,
