@@ -117,7 +117,7 @@ inline void parallel_memcpy(void* dst, const void* src, size_t bytes) {
 // the pool) so the later copy does not take the first-touch faults; run while
 // the kernel that produces the data is still executing.
 inline void parallel_prefault(void* dst, size_t bytes) {
-  constexpr size_t kPage = 4096, kPiece = 8u << 20;
+  constexpr size_t kPage = 4096, kPiece = 1u << 20;  // 1 MiB pieces: every pool thread busy from 16 MiB on
   const int pieces = (int)((bytes + kPiece - 1) / kPiece);
   CopyPool::get().parallel_for(pieces, [&](int i) {
     char* p = static_cast<char*>(dst) + (size_t)i * kPiece;
@@ -144,7 +144,7 @@ inline void parallel_fill(void* dst, int value, size_t bytes) {
 // dst[i] = src[i] widened, split over the pool (the host half of a narrowed
 // device -> host copy).
 inline void parallel_widen(int64_t* dst, const int32_t* src, size_t count) {
-  constexpr size_t kSlice = 256u << 10;  // values per slice (>= 1 MiB of int32)
+  constexpr size_t kSlice = 32u << 10;  // values per slice (128 KiB of int32): a few MiB already spread over the pool
   const int pieces = (int)std::min<size_t>((count + kSlice - 1) / kSlice, (size_t)CopyPool::get().size());
   if (pieces <= 1) {
     for (size_t i = 0; i < count; ++i) dst[i] = src[i];
@@ -159,7 +159,7 @@ inline void parallel_widen(int64_t* dst, const int32_t* src, size_t count) {
 
 // dst[i] = table[src[i]]: 16-bit ranks back to their int64 values
 inline void parallel_lookup16(int64_t* dst, const uint16_t* src, size_t count, const int64_t* table) {
-  constexpr size_t kSlice = 512u << 10;
+  constexpr size_t kSlice = 64u << 10;
   const int pieces = (int)std::min<size_t>((count + kSlice - 1) / kSlice, (size_t)CopyPool::get().size());
   if (pieces <= 1) {
     for (size_t i = 0; i < count; ++i) dst[i] = table[src[i]];
