@@ -117,11 +117,15 @@ inline void parallel_memcpy(void* dst, const void* src, size_t bytes) {
 // the pool) so the later copy does not take the first-touch faults; run while
 // the kernel that produces the data is still executing.
 inline void parallel_prefault(void* dst, size_t bytes) {
-  constexpr size_t kPage = 4096, kPiece = 1u << 20;  // 1 MiB pieces: every pool thread busy from 16 MiB on
-  const int pieces = (int)((bytes + kPiece - 1) / kPiece);
+  // one piece per pool thread, in whole 2 MiB units (a transparent huge page
+  // is faulted by one thread, never two at once), at least 2 MiB
+  constexpr size_t kPage = 4096, kUnit = 2u << 20;
+  const size_t threads = (size_t)CopyPool::get().size();
+  const size_t piece = std::max(kUnit, ((bytes + threads - 1) / threads + kUnit - 1) / kUnit * kUnit);
+  const int pieces = (int)((bytes + piece - 1) / piece);
   CopyPool::get().parallel_for(pieces, [&](int i) {
-    char* p = static_cast<char*>(dst) + (size_t)i * kPiece;
-    const size_t len = std::min(kPiece, bytes - (size_t)i * kPiece);
+    char* p = static_cast<char*>(dst) + (size_t)i * piece;
+    const size_t len = std::min(piece, bytes - (size_t)i * piece);
     for (size_t o = 0; o < len; o += kPage) reinterpret_cast<volatile char*>(p)[o] = 0;
   });
 }
